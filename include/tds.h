@@ -1,0 +1,188 @@
+/*
+ * tds.h — C-ABI of the B200 distance threshold search over 4-D trajectory
+ * line segments (Gowanlock & Casanova, arXiv 1410.2698).
+ *
+ * Citations: "P:a-b" = lines of the paper text; section / figure /
+ * algorithm named beside it.  Readings of silent or garbled points are listed
+ * in DESIGN.md ("Readings", C1-C24).
+ *
+ * The operation (§3.1 "Problem Definition"):
+ *   D is a database of n entry line segments, each a 4-D segment from
+ *   (x,y,z,t)_start to (x,y,z,t)_end, moving linearly in between
+ *   (P:102-104).  For a query set Q, a threshold d and a window [T0,T1], the
+ *   result set is every (query q, entry e, [t_in, t_out]) such that the shared
+ *   span [a,b] = [max(t0q,t0e,T0), min(t1q,t1e,T1)] has a < b and
+ *   [t_in,t_out] = { t in [a,b] : ||Pq(t) - Pe(t)||_2 <= d } is non-empty
+ *   ("(q1, l1, [0.1, 0.3])").  Distance is synchronous Euclidean
+ *   3-D distance.
+ *
+ * Candidate selection, chosen per search:
+ *   TDS_TEMPORAL        GPUTemporal  (§4.2, Alg. 2)
+ *   TDS_SPATIAL         GPUSpatial   (§4.1, Alg. 1)
+ *   TDS_SPATIOTEMPORAL  GPUSpatioTemporal (§4.3, Alg. 3)
+ * Every variant returns the same result set (the indexes are filters).
+ *
+ * Conventions for every entry point:
+ *   - Return 0 (TDS_OK) on success, else a tds_status; a message describing
+ *     the failure is available from tds_last_error() (thread-local).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Calls enqueue work on it and synchronise it before returning
+ *     unless stated otherwise.
+ *   - Input pointers may be DEVICE or HOST memory (detected with
+ *     cudaPointerGetAttributes); host inputs are copied to the device inside
+ *     the call.  Inputs are read only during the call and never retained.
+ *   - Ids in results are row numbers in the caller's input arrays (reading
+ *     C9), not positions after the internal sorts.
+ *   - The library never falls back to a CPU implementation.
+ */
+#ifndef TDS_H
+#define TDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One segment, 32 bytes: (x0,y0,z0,t0, x1,y1,z1,t1) in float32.
+ * Arrays of tds_seg must be 16-byte aligned. */
+typedef struct { float x0, y0, z0, t0, x1, y1, z1, t1; } tds_seg;
+
+/* Index variants (bit flags for tds_index_params.kinds; one value for tds_search). */
+enum {
+    TDS_TEMPORAL = 1,          /* temporal bins */
+    TDS_SPATIAL = 2,           /* flatly structured grid */
+    TDS_SPATIOTEMPORAL = 4,    /* temporal bins split into spatial subbins */
+    TDS_ALL = 7
+};
+
+typedef enum {
+    TDS_OK = 0,
+    TDS_EINVAL = 1,     /* bad argument: n==0, d<=0 or not finite, T0>T1, m<1, v<1 or v above the
+                           admissible bound of P:816-821, grid<1, NULL pointer, unbuilt variant */
+    TDS_EDATA = 2,      /* a segment has a non-finite value or t_end <= t_start (message: first index) */
+    TDS_ENOMEM = 3,     /* device allocation failed */
+    TDS_ECAPACITY = 4,  /* one query alone produces more records than `capacity` */
+    TDS_ECUDA = 5       /* CUDA runtime error (message carries cudaGetErrorString) */
+} tds_status;
+
+typedef struct {
+    uint32_t kinds;     /* OR of TDS_TEMPORAL / TDS_SPATIAL / TDS_SPATIOTEMPORAL to build
+                           (the temporal structure is always built: ST refines it) */
+    int32_t m_bins;     /* m, number of temporal bins, >= 1 (10,000 for S1, 1,000 S2/S3) */
+    int32_t v_subbins;  /* v, spatial subbins per dimension per bin, 1 <= v <= floor(extent_c /
+                           max per-segment extent_c) for c = x,y,z */
+    int32_t grid[3];    /* FSG cells per dimension, >= 1 (50 each in P:1391) */
+} tds_index_params;
+
+typedef struct tds_index_s *tds_index;
+typedef struct tds_result_s *tds_result;
+
+typedef struct {
+    uint64_t n_results;         /* records in the result set */
+    uint64_t n_queries;         /* queries searched (after dropping empty windows) */
+    uint64_t pair_tests;        /* candidate pairs the schedule assigns (sum of range lengths;
+                                   GPUSpatial: sum over (query, cell) of cell sizes) */
+    uint64_t pairs_executed;    /* pairs the kernel actually evaluated (tiles cover unions) */
+    uint64_t refined_pairs;     /* pairs re-evaluated in fp64 (near threshold or hits) */
+    uint64_t passes;            /* pair-kernel passes (1 + overflow re-launches) */
+    uint64_t spilled;           /* records moved out of the pass buffer on overflow */
+    uint64_t fallback_queries;  /* GPUSpatioTemporal queries using the temporal fallback */
+    float ms_schedule;          /* device time of query sort + schedule (CUDA events) */
+    float ms_pairs;             /* device time of the pair kernel passes */
+    float ms_compact;           /* device time of overflow compaction / re-planning */
+    float ms_total;             /* tds_search device time */
+} tds_stats;
+
+/*
+ * tds_build_index — build the resident index over D (D is stored
+ * once on the GPU and queried many times; build time is excluded from the
+ * paper's response times).
+ *
+ *   entries : n segments (device or host memory), copied into index-owned memory
+ *   n       : number of entry segments (>= 1, < 2^32)
+ *   params  : see tds_index_params
+ *   out     : receives the index handle; free with tds_index_free
+ *
+ * Steps: validate + extents;
+ * stable radix sort by t_start and renumbering; bins;
+ * optional subbin arrays X/Y/Z and FSG cell lists G/A.
+ * Errors: TDS_EINVAL, TDS_EDATA, TDS_ENOMEM, TDS_ECUDA.  Synchronises stream.
+ */
+int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *params,
+                    void *stream, tds_index *out);
+
+/*
+ * tds_search — the distance threshold search of Q against the index
+ * (Alg. 1 / 2 / 3).
+ *
+ *   kind      : TDS_TEMPORAL, TDS_SPATIAL or TDS_SPATIOTEMPORAL (must have been built)
+ *   queries   : nq segments (device or host memory); nq == 0 gives an empty result
+ *   d         : distance threshold, finite and > 0 ("within d" is <= d, reading C4)
+ *   t_start, t_end : query window [T0, T1]; pass -INFINITY / +INFINITY for none
+ *   capacity  : records the pass buffer holds (the paper's fixed result buffer);
+ *               0 = automatic.  When a pass overflows, the records of the queries that
+ *               lost records are discarded and those queries are re-run in batches that
+ *               fit (reading C22); never duplicates, always progresses.
+ *   out       : receives the result handle (free with tds_result_free)
+ *   n_results : receives the number of records (may be NULL)
+ * Errors: TDS_EINVAL, TDS_EDATA (bad query segment), TDS_ENOMEM, TDS_ECAPACITY, TDS_ECUDA.
+ * Synchronises stream (one host synchronisation per pass).
+ */
+int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, float d,
+               float t_start, float t_end, uint64_t capacity, void *stream,
+               tds_result *out, uint64_t *n_results);
+
+/*
+ * tds_fetch_results — copy records [first, first+count) into caller arrays
+ * (each `count` long): query_id / entry_id (row numbers of the caller's Q and
+ * D), t_in / t_out (the closed interval, float32).  Any output pointer may be
+ * NULL to skip that column.  dst_is_device: 1 = outputs are device memory,
+ * 0 = host memory.  sorted: 1 = records ordered by (query_id, entry_id)
+ * (the order is otherwise unspecified: atomic appends).
+ * Errors: TDS_EINVAL (range outside the result), TDS_ECUDA.  Synchronises stream.
+ */
+int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *query_id,
+                      uint32_t *entry_id, float *t_in, float *t_out, int dst_is_device,
+                      int sorted, void *stream);
+
+/* tds_result_stats — counters and device timings of the search that made r. */
+int tds_result_stats(tds_result r, tds_stats *out);
+
+/* tds_result_count — number of records in r. */
+uint64_t tds_result_count(tds_result r);
+
+void tds_result_free(tds_result r);
+void tds_index_free(tds_index idx);
+
+/* tds_last_error — message of the last failed call on this thread ("" if none). */
+const char *tds_last_error(void);
+
+/*
+ * tds_index_export — copy one internal index array to HOST memory, for tests
+ * that pin the build against the paper's figures.  `what` selects:
+ *   0 perm       uint32[n]      original row of sorted entry i (renumbering)
+ *   1 bin_off    uint32[m+1]    first sorted entry of bin j (B_j^first; B_j^last = next-1)
+ *   2 bin_hi     float[m]       max t_end over bin j's members (-inf if empty) (B_j^end)
+ *   3 st_x/4 st_y/5 st_z uint32[len]   arrays X, Y, Z of sorted-entry ids
+ *   6/7/8 st_off_x/y/z uint32[v*m+1]  start of subbin (slab j, bin i) at [j*m+i]
+ *   9 fsg_cell_off uint32[gx*gy*gz+1]  dense CSR of cell h (row-major)
+ *  10 fsg_A     uint32[len]     lookup array A of sorted-entry ids
+ *  11 extents   float[16]       t_min, t_max, lo[3], hi[3], maxext[3], w_st[3], pad
+ *  12 sorted_t0 float[n]        t_start of the sorted entries
+ * Writes min(cap_bytes, size) bytes to dst (may be NULL to query the size) and the
+ * full size to *n_bytes.  Errors: TDS_EINVAL (unknown / unbuilt array).
+ */
+int tds_index_export(tds_index idx, int what, void *dst, uint64_t cap_bytes, uint64_t *n_bytes);
+
+/* tds_index_info — n, m, v, grid of a built index (any pointer may be NULL). */
+int tds_index_info(tds_index idx, uint64_t *n, int32_t *m, int32_t *v, int32_t *grid3,
+                   uint32_t *kinds);
+
+/* tds_version — library build string. */
+const char *tds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDS_H */

@@ -1,0 +1,237 @@
+"""tds-b200: distance threshold search over 4-D trajectory segments on B200.
+
+Thin ctypes binding of the C-ABI in ``include/tds.h`` (argument marshalling
+only — every step of the search runs in the CUDA kernels of ``libtds.so``).
+Paper: Gowanlock & Casanova, arXiv 1410.2698; see DESIGN.md.
+
+    import torch, paper_1410_2698_b200 as tds
+    idx = tds.Index(entries_cuda_f32_n_by_8, kinds=tds.ALL, m=1000, v=2, grid=(50, 50, 50))
+    res = idx.search(queries, d=0.03, kind="spatiotemporal")
+    qid, eid, t_in, t_out = res.fetch(sorted=True)
+
+There is no CPU fallback: if ``libtds.so`` is missing or cannot be loaded the
+import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtds.so")
+
+TEMPORAL, SPATIAL, SPATIOTEMPORAL, ALL = 1, 2, 4, 7
+KINDS = {"temporal": TEMPORAL, "spatial": SPATIAL, "spatiotemporal": SPATIOTEMPORAL}
+STATUS = {0: "TDS_OK", 1: "TDS_EINVAL", 2: "TDS_EDATA", 3: "TDS_ENOMEM", 4: "TDS_ECAPACITY", 5: "TDS_ECUDA"}
+
+EXPORT = {"perm": 0, "bin_off": 1, "bin_hi": 2, "st_x": 3, "st_y": 4, "st_z": 5, "st_off_x": 6,
+          "st_off_y": 7, "st_off_z": 8, "fsg_cell_off": 9, "fsg_A": 10, "extents": 11, "sorted_t0": 12}
+_EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float32}
+
+# every symbol include/tds.h declares
+ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
+               "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
+               "tds_version"]
+
+
+class TdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("kinds", ctypes.c_uint32), ("m_bins", ctypes.c_int32), ("v_subbins", ctypes.c_int32),
+                ("grid", ctypes.c_int32 * 3)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in ("n_results", "n_queries", "pair_tests", "pairs_executed",
+                                               "refined_pairs", "passes", "spilled", "fallback_queries")] + \
+               [(k, ctypes.c_float) for k in ("ms_schedule", "ms_pairs", "ms_compact", "ms_total")]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libtds.so (raises if missing: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libtds.so not found at {path}: run `python -m paper_1410_2698_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    vp, u64, i32, f32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_float
+    lib.tds_build_index.argtypes = [vp, u64, ctypes.POINTER(_Params), vp, ctypes.POINTER(vp)]
+    lib.tds_search.argtypes = [vp, i32, vp, u64, f32, f32, f32, u64, vp, ctypes.POINTER(vp),
+                               ctypes.POINTER(u64)]
+    lib.tds_fetch_results.argtypes = [vp, u64, u64, vp, vp, vp, vp, i32, i32, vp]
+    lib.tds_result_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
+    lib.tds_result_count.argtypes = [vp]
+    lib.tds_result_count.restype = u64
+    lib.tds_result_free.argtypes = [vp]
+    lib.tds_result_free.restype = None
+    lib.tds_index_free.argtypes = [vp]
+    lib.tds_index_free.restype = None
+    lib.tds_last_error.restype = ctypes.c_char_p
+    lib.tds_version.restype = ctypes.c_char_p
+    lib.tds_index_export.argtypes = [vp, i32, vp, u64, ctypes.POINTER(u64)]
+    lib.tds_index_info.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_uint32)]
+    for name in ("tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats",
+                 "tds_index_export", "tds_index_info"):
+        getattr(lib, name).restype = i32
+    _lib = lib
+    return lib
+
+
+def _check(code):
+    if code != 0:
+        raise TdsError(code, _lib.tds_last_error().decode())
+
+
+def _stream_ptr(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:
+        pass
+    return ctypes.c_void_p(0)
+
+
+def _segments(x):
+    """Return (pointer, n, keepalive) for an [n, 8] float32 array (torch cuda/cpu or numpy)."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if x.dtype != torch.float32 or x.dim() != 2 or x.shape[1] != 8:
+                raise ValueError("segments must be a float32 tensor of shape [n, 8]")
+            x = x.contiguous()
+            return ctypes.c_void_p(x.data_ptr()), x.shape[0], x
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32).reshape(-1, 8))
+    if a.ctypes.data % 16:
+        b = np.empty(a.shape[0] * 8 + 4, np.float32)
+        off = (-b.ctypes.data % 16) // 4
+        b = b[off:off + a.size].reshape(-1, 8)
+        b[...] = a
+        a = b
+    return ctypes.c_void_p(a.ctypes.data), a.shape[0], a
+
+
+class Index:
+    """Resident index over the database D (tds_build_index, §4)."""
+
+    def __init__(self, entries, kinds: int = ALL, m: int = 1000, v: int = 1, grid=(50, 50, 50), stream=None):
+        lib = load_library()
+        p = _Params(int(kinds), int(m), int(v), (ctypes.c_int32 * 3)(*[int(g) for g in grid]))
+        ptr, n, keep = _segments(entries)
+        h = ctypes.c_void_p()
+        _check(lib.tds_build_index(ptr, n, ctypes.byref(p), _stream_ptr(stream), ctypes.byref(h)))
+        del keep
+        self._h = h
+        self.n = n
+        self.m, self.v, self.grid, self.kinds = int(m), int(v), tuple(grid), int(kinds)
+
+    def search(self, queries, d: float, window=(-math.inf, math.inf), kind="temporal", capacity: int = 0,
+               stream=None) -> "Result":
+        lib = load_library()
+        k = KINDS[kind] if isinstance(kind, str) else int(kind)
+        ptr, nq, keep = _segments(queries)
+        h = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        _check(lib.tds_search(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), int(capacity),
+                              _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
+        del keep
+        return Result(h, n.value)
+
+    def export(self, what: str) -> np.ndarray:
+        lib = load_library()
+        nb = ctypes.c_uint64()
+        _check(lib.tds_index_export(self._h, EXPORT[what], None, 0, ctypes.byref(nb)))
+        out = np.empty(nb.value // 4, dtype=_EXPORT_DT.get(what, np.uint32))
+        _check(lib.tds_index_export(self._h, EXPORT[what], out.ctypes.data_as(ctypes.c_void_p), nb.value,
+                                    ctypes.byref(nb)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().tds_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Result:
+    """Result set of one search (tds_result)."""
+
+    def __init__(self, h, n):
+        self._h = h
+        self.count = int(n)
+
+    def stats(self) -> dict:
+        st = _Stats()
+        _check(load_library().tds_result_stats(self._h, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+    def fetch(self, sorted: bool = False, device: bool = True, first: int = 0, count=None, stream=None,
+              out=None):
+        """Return (query_id, entry_id, t_in, t_out).
+
+        device=True -> torch CUDA tensors (int32 ids, float32 times);
+        device=False -> numpy arrays.  ``out`` may supply preallocated buffers.
+        """
+        lib = load_library()
+        cnt = self.count - first if count is None else int(count)
+        if device:
+            import torch
+            if out is None:
+                q = torch.empty(cnt, dtype=torch.int32, device="cuda")
+                e = torch.empty(cnt, dtype=torch.int32, device="cuda")
+                ti = torch.empty(cnt, dtype=torch.float32, device="cuda")
+                to = torch.empty(cnt, dtype=torch.float32, device="cuda")
+            else:
+                q, e, ti, to = out
+            ptrs = [ctypes.c_void_p(t.data_ptr()) for t in (q, e, ti, to)]
+        else:
+            if out is None:
+                q = np.empty(cnt, np.uint32)
+                e = np.empty(cnt, np.uint32)
+                ti = np.empty(cnt, np.float32)
+                to = np.empty(cnt, np.float32)
+            else:
+                q, e, ti, to = out
+            ptrs = [ctypes.c_void_p(a.ctypes.data) for a in (q, e, ti, to)]
+        _check(lib.tds_fetch_results(self._h, int(first), cnt, *ptrs, 1 if device else 0, 1 if sorted else 0,
+                                     _stream_ptr(stream)))
+        return q, e, ti, to
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().tds_result_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def version() -> str:
+    return load_library().tds_version().decode()

@@ -1,0 +1,274 @@
+// abi.cu — the extern "C" boundary declared in include/tds.h: argument
+// checking, host/device input detection, error reporting, handle lifetime.
+#include <cstdarg>
+#include <cstdio>
+#include <new>
+
+#include "tds_internal.cuh"
+
+namespace tds {
+
+static thread_local std::string g_err;
+
+void set_error(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    (void)code;
+    g_err = buf;
+}
+
+const char *last_error() { return g_err.c_str(); }
+
+void fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    throw Error{code, buf};
+}
+
+static void init_pool_once() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;   // keep freed memory in the pool (no re-mapping per search)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+void *dalloc(size_t bytes, cudaStream_t s) {
+    init_pool_once();
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? TDS_ENOMEM : TDS_ECUDA, "cudaMallocAsync(%zu bytes): %s", bytes,
+             cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void dfree(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// device copy of a caller buffer that may live in host memory
+struct Staged {
+    const float4 *p = nullptr;
+    DBuf<float4> own;
+};
+
+static void stage(const tds_seg *src, uint64_t n, cudaStream_t s, Staged &out) {
+    if (!src) fail(TDS_EINVAL, "NULL segment pointer");
+    if (((uintptr_t)src & 15) != 0) fail(TDS_EINVAL, "segment array must be 16-byte aligned");
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, src);
+    if (e != cudaSuccess) cudaGetLastError();
+    bool dev = (e == cudaSuccess) && (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    if (dev) {
+        out.p = reinterpret_cast<const float4 *>(src);
+        return;
+    }
+    out.own = DBuf<float4>(2 * n, s);
+    TDS_CUDA(cudaMemcpyAsync(out.own.p, src, n * sizeof(tds_seg), cudaMemcpyHostToDevice, s));
+    out.p = out.own.p;
+}
+
+}  // namespace tds
+
+using namespace tds;
+
+#define ABI_TRY try {
+#define ABI_CATCH                                                   \
+    }                                                               \
+    catch (const tds::Error &err) {                                 \
+        return err.code;                                            \
+    }                                                               \
+    catch (const std::bad_alloc &) {                                \
+        tds::set_error(TDS_ENOMEM, "host allocation failed");       \
+        return TDS_ENOMEM;                                          \
+    }                                                               \
+    catch (...) {                                                   \
+        tds::set_error(TDS_ECUDA, "unexpected exception");          \
+        return TDS_ECUDA;                                           \
+    }
+
+extern "C" {
+
+const char *tds_last_error(void) { return tds::last_error(); }
+
+const char *tds_version(void) { return "tds-b200 0.1 (sm_100a)"; }
+
+int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *params, void *stream,
+                    tds_index *out) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!out || !params) fail(TDS_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (n == 0) fail(TDS_EINVAL, "n == 0");
+    if (n >= (1ull << 32) - 1) fail(TDS_EINVAL, "n = %llu exceeds 2^32 - 2", (unsigned long long)n);
+    if (params->m_bins < 1) fail(TDS_EINVAL, "m_bins = %d < 1", params->m_bins);
+    if ((params->kinds & TDS_SPATIOTEMPORAL) && params->v_subbins < 1)
+        fail(TDS_EINVAL, "v_subbins = %d < 1", params->v_subbins);
+    if ((params->kinds & TDS_SPATIAL))
+        for (int c = 0; c < 3; ++c)
+            if (params->grid[c] < 1) fail(TDS_EINVAL, "grid[%d] = %d < 1", c, params->grid[c]);
+    if (params->kinds & ~(uint32_t)TDS_ALL) fail(TDS_EINVAL, "unknown kinds bits 0x%x", params->kinds);
+    if ((uint64_t)params->m_bins * (uint64_t)std::max(params->v_subbins, 1) >= (1ull << 31))
+        fail(TDS_EINVAL, "m * v too large");
+    cudaStream_t s = (cudaStream_t)stream;
+    Staged in;
+    stage(entries, n, s, in);
+    tds_index_s *idx = new tds_index_s();
+    cudaGetDevice(&idx->device);
+    try {
+        build_index(reinterpret_cast<const tds_seg *>(in.p), n, params, s, idx);
+    } catch (...) {
+        free_index(idx);
+        delete idx;
+        throw;
+    }
+    *out = idx;
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, float d, float t_start, float t_end,
+               uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!idx || !out) fail(TDS_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (kind != TDS_TEMPORAL && kind != TDS_SPATIAL && kind != TDS_SPATIOTEMPORAL)
+        fail(TDS_EINVAL, "kind = %d is not one of TDS_TEMPORAL/SPATIAL/SPATIOTEMPORAL", kind);
+    if (!(idx->kinds & (uint32_t)kind)) fail(TDS_EINVAL, "index was not built for kind %d", kind);
+    if (!(d > 0.f) || !isfinite(d)) fail(TDS_EINVAL, "d = %g must be finite and > 0", (double)d);
+    if (isnan(t_start) || isnan(t_end) || t_start > t_end) fail(TDS_EINVAL, "bad window [%g, %g]",
+                                                               (double)t_start, (double)t_end);
+    cudaStream_t s = (cudaStream_t)stream;
+    tds_result_s *r = new tds_result_s();
+    cudaGetDevice(&r->device);
+    try {
+        if (nq > 0) {
+            Staged in;
+            stage(queries, nq, s, in);
+            tds::search(idx, kind, in.p, nq, d, t_start, t_end, capacity, s, r);
+        }
+    } catch (...) {
+        free_result(r);
+        delete r;
+        throw;
+    }
+    *out = r;
+    if (n_results) *n_results = r->n;
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *query_id, uint32_t *entry_id,
+                      float *t_in, float *t_out, int dst_is_device, int sorted, void *stream) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!r) fail(TDS_EINVAL, "NULL result");
+    tds::fetch(r, first, count, query_id, entry_id, t_in, t_out, dst_is_device != 0, sorted != 0,
+               (cudaStream_t)stream);
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_result_stats(tds_result r, tds_stats *out) {
+    if (!r || !out) {
+        tds::set_error(TDS_EINVAL, "NULL argument");
+        return TDS_EINVAL;
+    }
+    *out = r->stats;
+    return TDS_OK;
+}
+
+uint64_t tds_result_count(tds_result r) { return r ? r->n : 0; }
+
+void tds_result_free(tds_result r) {
+    if (!r) return;
+    free_result(r);
+    delete r;
+}
+
+void tds_index_free(tds_index idx) {
+    if (!idx) return;
+    free_index(idx);
+    delete idx;
+}
+
+int tds_index_info(tds_index idx, uint64_t *n, int32_t *m, int32_t *v, int32_t *grid3, uint32_t *kinds) {
+    if (!idx) {
+        tds::set_error(TDS_EINVAL, "NULL index");
+        return TDS_EINVAL;
+    }
+    if (n) *n = idx->n;
+    if (m) *m = idx->m;
+    if (v) *v = idx->v;
+    if (grid3) for (int c = 0; c < 3; ++c) grid3[c] = idx->grid[c];
+    if (kinds) *kinds = idx->kinds;
+    return TDS_OK;
+}
+
+int tds_index_export(tds_index idx, int what, void *dst, uint64_t cap_bytes, uint64_t *n_bytes) {
+    ABI_TRY
+    if (!idx) fail(TDS_EINVAL, "NULL index");
+    const void *src = nullptr;
+    uint64_t bytes = 0;
+    bool host = false;
+    std::vector<float> tmp;
+    switch (what) {
+        case 0: src = idx->perm; bytes = 4 * idx->n; break;
+        case 1: src = idx->bin_off; bytes = 4ull * (idx->m + 1); break;
+        case 2: src = idx->bin_hi; bytes = 4ull * idx->m; break;
+        case 3: case 4: case 5:
+            src = idx->st_arr[what - 3]; bytes = 4 * idx->st_len[what - 3]; break;
+        case 6: case 7: case 8:
+            src = idx->st_off[what - 6];
+            bytes = idx->st_off[what - 6] ? 4ull * ((uint64_t)idx->v * idx->m + 1) : 0; break;
+        case 9: src = idx->cell_off; bytes = idx->cell_off ? 4 * (idx->n_cells + 1) : 0; break;
+        case 10: src = idx->fsg_A; bytes = 4 * idx->A_len; break;
+        case 11: src = &idx->ext; bytes = sizeof(tds::Extents); host = true; break;
+        case 12: {
+            tmp.resize(idx->n);
+            std::vector<float4> r(2 * idx->n);
+            TDS_CUDA(cudaMemcpy(r.data(), idx->rec, 32 * idx->n, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < idx->n; ++i) tmp[i] = r[2 * i].w;
+            src = tmp.data(); bytes = 4 * idx->n; host = true; break;
+        }
+        default: fail(TDS_EINVAL, "unknown export %d", what);
+    }
+    if (!src && what != 11 && what != 12) fail(TDS_EINVAL, "array %d was not built", what);
+    if (n_bytes) *n_bytes = bytes;
+    if (dst && bytes) {
+        uint64_t b = bytes < cap_bytes ? bytes : cap_bytes;
+        if (host) memcpy(dst, src, b);
+        else TDS_CUDA(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost));
+    }
+    return TDS_OK;
+    ABI_CATCH
+}
+
+}  // extern "C"

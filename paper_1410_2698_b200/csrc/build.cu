@@ -1,0 +1,428 @@
+// build.cu — GPU index build (§4, build steps A1-A5 of DESIGN.md).
+//
+//   A1 validate + extents      P:571-573 (t_min, t_max), P:807-815 (spatial extents,
+//                              maximum per-segment extents)
+//   A2 sort by t_start         P:569-571 ("sorting the entries in D by ascending
+//                              t_start values, re-numbering the entry segments")
+//   A3 temporal bins           P:573-590 (b = (t_max - t_min)/m, bin of l_i,
+//                              B_j^first / B_j^last / B_j^end)
+//   A5 subbin arrays X, Y, Z   P:816-886 (v slabs per dimension, ids stored per
+//                              subbin in (slab, bin) lexicographic order)
+//   A4 FSG                     P:282-361 (rasterise each MBB to cells; lookup array A)
+#include <float.h>
+#include <vector>
+#include <algorithm>
+
+#include "tds_internal.cuh"
+
+namespace tds {
+
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ void atomic_min_key(uint32_t *a, float v) { atomicMin(a, float_key(v)); }
+__device__ __forceinline__ void atomic_max_key(uint32_t *a, float v) { atomicMax(a, float_key(v)); }
+
+__host__ __device__ inline float key_float(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+// A1: validate + reduce extents.  red[] layout (order-preserving keys):
+// 0 t_min, 1 t_max, 2..4 lo, 5..7 hi, 8..10 maxext
+__global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
+                                   unsigned long long *__restrict__ bad, uint32_t *__restrict__ red) {
+    float tmin = FLT_MAX, tmax = -FLT_MAX, lo[3], hi[3], mx[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { lo[c] = FLT_MAX; hi[c] = -FLT_MAX; mx[c] = 0.f; }
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        float4 a = rec[2 * i], b = rec[2 * i + 1];
+        bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) &&
+                  isfinite(b.y) && isfinite(b.z) && isfinite(b.w) && (b.w > a.w);
+        if (!ok) { atomicMin(bad, (unsigned long long)i); continue; }
+        tmin = fminf(tmin, a.w);
+        tmax = fmaxf(tmax, b.w);
+        float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = fminf(lo[c], fminf(p0[c], p1[c]));
+            hi[c] = fmaxf(hi[c], fmaxf(p0[c], p1[c]));
+            mx[c] = fmaxf(mx[c], fabsf(__fsub_rn(p1[c], p0[c])));
+        }
+    }
+    // warp reduce then one atomic per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+            hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomic_min_key(&red[0], tmin);
+        atomic_max_key(&red[1], tmax);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            atomic_min_key(&red[2 + c], lo[c]);
+            atomic_max_key(&red[5 + c], hi[c]);
+            atomic_max_key(&red[8 + c], mx[c]);
+        }
+    }
+}
+
+__global__ void k_init_red(uint32_t *red, unsigned long long *bad) {
+    int i = threadIdx.x;
+    if (i < 11) {
+        bool is_min = (i == 0) || (i >= 2 && i <= 4);
+        red[i] = is_min ? 0xffffffffu : 0u;
+    }
+    if (i == 0) *bad = ~0ull;
+}
+
+__global__ void k_time_keys(const float4 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ keys,
+                            uint32_t *__restrict__ vals) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        keys[i] = float_key(rec[2 * i].w);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_gather_records(const float4 *__restrict__ src, const uint32_t *__restrict__ perm, uint64_t n,
+                                 float4 *__restrict__ dst) {
+    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one float4 per thread
+    if (t < 2 * n) {
+        uint64_t i = t >> 1;
+        dst[t] = src[2 * (uint64_t)perm[i] + (t & 1)];
+    }
+}
+
+// A3: bin of each sorted entry, literal (P:575-576 with reading C12), in fp64
+__global__ void k_bin_of(const float4 *__restrict__ rec, uint64_t n, double t_min, double b, int m,
+                         uint32_t *__restrict__ bin) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        double j = floor(((double)rec[2 * i].w - t_min) / b);
+        int k = j < 0.0 ? 0 : (j >= (double)m ? m - 1 : (int)j);
+        bin[i] = (uint32_t)k;
+    }
+}
+
+// off[k] = first i with key[i] >= k, k = 0..nk (keys sorted, all < nk)
+__global__ void k_bucket_offsets(const uint32_t *__restrict__ key, uint64_t n, uint32_t nk,
+                                 uint32_t *__restrict__ off) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    int64_t prev = (i == 0) ? -1 : (int64_t)key[i - 1];
+    int64_t cur = (i == n) ? (int64_t)nk : (int64_t)key[i];
+    for (int64_t k = prev + 1; k <= cur; ++k) off[k] = (uint32_t)i;
+}
+
+// A3: per bin, one warp reduces max t_end over its members; lo = first member t_start
+__global__ void k_bin_extents(const float4 *__restrict__ rec, uint64_t n, const uint32_t *__restrict__ off, int m,
+                              float *__restrict__ bin_lo, float *__restrict__ bin_hi) {
+    int j = (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int lane = threadIdx.x & 31;
+    if (j >= m) return;
+    uint32_t a = off[j], b = off[j + 1];
+    float hmax = -INFINITY;
+    for (uint32_t i = a + lane; i < b; i += 32) hmax = fmaxf(hmax, rec[2 * (uint64_t)i + 1].w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    if (lane == 0) {
+        bin_hi[j] = hmax;
+        bin_lo[j] = (a < n) ? rec[2 * (uint64_t)a].w : INFINITY;   // empty bins: next bin's first
+    }
+}
+
+// prefix max over m values, single block of 1024 threads
+__global__ void __launch_bounds__(1024) k_prefix_max(const float *__restrict__ in, float *__restrict__ out, int m) {
+    __shared__ float wmax[32];
+    __shared__ float carry_s;
+    if (threadIdx.x == 0) carry_s = -INFINITY;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < m; b0 += 1024) {
+        int k = b0 + threadIdx.x;
+        float x = (k < m) ? in[k] : -INFINITY;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            float y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = fmaxf(x, y);
+        }
+        if (lane == 31) wmax[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            float v = wmax[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                float y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v = fmaxf(v, y);
+            }
+            wmax[lane] = v;
+        }
+        __syncthreads();
+        float pre = (w > 0) ? wmax[w - 1] : -INFINITY;
+        float r = fmaxf(fmaxf(x, pre), carry_s);
+        if (k < m) out[k] = r;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = r;
+        __syncthreads();
+    }
+}
+
+// A5 / A4: number of slabs (cells) of each entry in dimension c / in 3-D
+__global__ void k_slab_count(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v,
+                             uint32_t *__restrict__ cnt) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 a = rec[2 * i], b = rec[2 * i + 1];
+    float p0 = c == 0 ? a.x : (c == 1 ? a.y : a.z);
+    float p1 = c == 0 ? b.x : (c == 1 ? b.y : b.z);
+    int s0 = cell_of(fminf(p0, p1), o, w, v), s1 = cell_of(fmaxf(p0, p1), o, w, v);
+    cnt[i] = (uint32_t)(s1 - s0 + 1);
+}
+
+__global__ void k_slab_emit(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v, int m,
+                            const uint32_t *__restrict__ bin, const uint32_t *__restrict__ pos,
+                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 a = rec[2 * i], b = rec[2 * i + 1];
+    float p0 = c == 0 ? a.x : (c == 1 ? a.y : a.z);
+    float p1 = c == 0 ? b.x : (c == 1 ? b.y : b.z);
+    int s0 = cell_of(fminf(p0, p1), o, w, v), s1 = cell_of(fmaxf(p0, p1), o, w, v);
+    uint32_t k = pos[i];
+    for (int s = s0; s <= s1; ++s, ++k) {
+        keys[k] = (uint32_t)s * (uint32_t)m + bin[i];    // subbin (slab j, bin i) at j*m + i
+        vals[k] = (uint32_t)i;
+    }
+}
+
+struct Grid3 {
+    float o[3], w[3];
+    int g[3];
+};
+
+__device__ __forceinline__ void cell_box(const float4 &a, const float4 &b, const Grid3 &G, int lo[3], int hi[3]) {
+    float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        lo[c] = cell_of(fminf(p0[c], p1[c]), G.o[c], G.w[c], G.g[c]);
+        hi[c] = cell_of(fmaxf(p0[c], p1[c]), G.o[c], G.w[c], G.g[c]);
+    }
+}
+
+__global__ void k_cell_count(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint32_t *__restrict__ cnt,
+                             unsigned long long *__restrict__ total) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c = 0;
+    if (i < n) {
+        int lo[3], hi[3];
+        cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
+        c = (unsigned long long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+        cnt[i] = (uint32_t)c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
+}
+
+__global__ void k_cell_emit(const float4 *__restrict__ rec, uint64_t n, Grid3 G, const uint32_t *__restrict__ pos,
+                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo[3], hi[3];
+    cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
+    uint32_t k = pos[i];
+    for (int x = lo[0]; x <= hi[0]; ++x)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int z = lo[2]; z <= hi[2]; ++z, ++k) {
+                keys[k] = (uint32_t)(((uint64_t)x * G.g[1] + y) * G.g[2] + z);   // row-major h
+                vals[k] = (uint32_t)i;
+            }
+}
+
+inline unsigned nblk(uint64_t n, int nt = NT) { return (unsigned)((n + nt - 1) / nt); }
+
+int bits_for(uint64_t nk) {
+    int b = 0;
+    while ((1ull << b) < nk) ++b;
+    return b;
+}
+
+// group (key, val) pairs by key with a stable radix sort; vals -> out ids,
+// offsets of the nk buckets -> off[nk+1]
+void group_by_key(uint32_t *keys, uint32_t *vals, uint64_t len, uint64_t nk, uint32_t *off, cudaStream_t s) {
+    radix_sort_pairs(keys, vals, len, 0, bits_for(nk), s);
+    k_bucket_offsets<<<nblk(len + 1), NT, 0, s>>>(keys, len, (uint32_t)nk, off);
+    TDS_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+uint64_t validate_segments(const float4 *rec, uint64_t n, cudaStream_t s) {
+    DBuf<unsigned long long> bad(1, s);
+    DBuf<uint32_t> red(16, s);
+    k_init_red<<<1, 32, 0, s>>>(red.p, bad.p);
+    TDS_CHECK_LAUNCH();
+    k_validate_extents<<<std::min<uint64_t>(nblk(n), 4096), NT, 0, s>>>(rec, n, bad.p, red.p);
+    TDS_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    TDS_CUDA(cudaMemcpyAsync(&h, bad.p, 8, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, cudaStream_t s,
+                 tds_index_s *idx) {
+    const float4 *in = reinterpret_cast<const float4 *>(entries);
+    idx->n = n;
+    idx->m = p->m_bins;
+    idx->v = p->v_subbins;
+    for (int c = 0; c < 3; ++c) idx->grid[c] = p->grid[c];
+    idx->kinds = p->kinds | TDS_TEMPORAL;
+
+    // ---- A1: validate + extents --------------------------------------------
+    DBuf<unsigned long long> bad(1, s);
+    DBuf<uint32_t> red(16, s);
+    k_init_red<<<1, 32, 0, s>>>(red.p, bad.p);
+    TDS_CHECK_LAUNCH();
+    k_validate_extents<<<std::min<uint64_t>(nblk(n), (uint64_t)num_sms() * 8), NT, 0, s>>>(in, n, bad.p, red.p);
+    TDS_CHECK_LAUNCH();
+    unsigned long long hbad;
+    uint32_t hred[16];
+    TDS_CUDA(cudaMemcpyAsync(&hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaMemcpyAsync(hred, red.p, 11 * 4, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaStreamSynchronize(s));
+    if (hbad != ~0ull)
+        fail(TDS_EDATA, "entry segment %llu has a non-finite value or t_end <= t_start", hbad);
+    Extents &E = idx->ext;
+    E.t_min = key_float(hred[0]);
+    E.t_max = key_float(hred[1]);
+    for (int c = 0; c < 3; ++c) {
+        E.lo[c] = key_float(hred[2 + c]);
+        E.hi[c] = key_float(hred[5 + c]);
+        E.maxext[c] = key_float(hred[8 + c]);
+    }
+    const bool want_st = (p->kinds & TDS_SPATIOTEMPORAL) != 0;
+    const bool want_fsg = (p->kinds & TDS_SPATIAL) != 0;
+    if (want_st) {   // admissible v: v <= (c_max - c_min) / max |c_start - c_end|
+        for (int c = 0; c < 3; ++c) {
+            double ext = (double)E.hi[c] - (double)E.lo[c];
+            if (E.maxext[c] > 0.f && (double)idx->v > ext / (double)E.maxext[c])
+                fail(TDS_EINVAL, "v_subbins=%d exceeds the admissible bound %.3f in dimension %d (P:816-821)",
+                     idx->v, ext / (double)E.maxext[c], c);
+        }
+    }
+
+    // ---- A2: stable radix sort by t_start, renumber, gather -----------------
+    DBuf<uint32_t> keys(n, s), perm(n, s);
+    k_time_keys<<<nblk(n), NT, 0, s>>>(in, n, keys.p, perm.p);
+    TDS_CHECK_LAUNCH();
+    radix_sort_pairs(keys.p, perm.p, n, 0, 32, s);
+    DBuf<float4> rec(2 * n, s);
+    k_gather_records<<<nblk(2 * n), NT, 0, s>>>(in, perm.p, n, rec.p);
+    TDS_CHECK_LAUNCH();
+    keys.reset();
+
+    // ---- A3: temporal bins ---------------------------------------------------
+    const int m = idx->m;
+    double t_min = E.t_min, b = ((double)E.t_max - (double)E.t_min) / (double)m;
+    if (!(b > 0.0)) b = 1.0;
+    DBuf<uint32_t> bin(n, s), bin_off(m + 1, s);
+    DBuf<float> bin_lo(m, s), bin_hi(m, s), bin_pmhi(m, s);
+    k_bin_of<<<nblk(n), NT, 0, s>>>(rec.p, n, t_min, b, m, bin.p);
+    TDS_CHECK_LAUNCH();
+    k_bucket_offsets<<<nblk(n + 1), NT, 0, s>>>(bin.p, n, (uint32_t)m, bin_off.p);
+    TDS_CHECK_LAUNCH();
+    k_bin_extents<<<nblk((uint64_t)m * 32), NT, 0, s>>>(rec.p, n, bin_off.p, m, bin_lo.p, bin_hi.p);
+    TDS_CHECK_LAUNCH();
+    k_prefix_max<<<1, 1024, 0, s>>>(bin_hi.p, bin_pmhi.p, m);
+    TDS_CHECK_LAUNCH();
+
+    // ---- A5: spatiotemporal subbin arrays ------------------------------------
+    if (want_st) {
+        const int v = idx->v;
+        for (int c = 0; c < 3; ++c) {
+            float ext = E.hi[c] - E.lo[c];
+            E.w_st[c] = ext > 0.f ? ext / (float)v : 1.0f;
+            DBuf<uint32_t> cnt(n, s), pos(n, s), total(1, s);
+            k_slab_count<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, cnt.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u32(cnt.p, pos.p, n, total.p, s);
+            uint32_t len = 0;
+            TDS_CUDA(cudaMemcpyAsync(&len, total.p, 4, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            DBuf<uint32_t> k2(len, s), v2(len, s), off((uint64_t)v * m + 1, s);
+            k_slab_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, pos.p, k2.p, v2.p);
+            TDS_CHECK_LAUNCH();
+            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, s);
+            idx->st_arr[c] = v2.release();
+            idx->st_len[c] = len;
+            idx->st_off[c] = off.release();
+        }
+    }
+
+    // ---- A4: FSG (dense CSR over all cells) ----------------------------------
+    if (want_fsg) {
+        Grid3 G;
+        uint64_t ncell = 1;
+        for (int c = 0; c < 3; ++c) {
+            if (idx->grid[c] < 1) fail(TDS_EINVAL, "grid[%d] = %d < 1", c, idx->grid[c]);
+            float ext = E.hi[c] - E.lo[c];
+            G.o[c] = E.lo[c];
+            G.g[c] = idx->grid[c];
+            G.w[c] = ext > 0.f ? ext / (float)idx->grid[c] : 1.0f;
+            idx->w_fsg[c] = G.w[c];
+            ncell *= (uint64_t)idx->grid[c];
+        }
+        if (ncell >= (1ull << 31)) fail(TDS_EINVAL, "grid has %llu cells (limit 2^31)", (unsigned long long)ncell);
+        DBuf<uint32_t> cnt(n, s), pos(n, s);
+        DBuf<unsigned long long> total(1, s);
+        TDS_CUDA(cudaMemsetAsync(total.p, 0, 8, s));
+        k_cell_count<<<nblk(n), NT, 0, s>>>(rec.p, n, G, cnt.p, total.p);
+        TDS_CHECK_LAUNCH();
+        unsigned long long len = 0;
+        TDS_CUDA(cudaMemcpyAsync(&len, total.p, 8, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        if (len >= (1ull << 32) - 1)
+            fail(TDS_EINVAL, "FSG lookup array would hold %llu ids (limit 2^32); use a coarser grid", len);
+        exclusive_scan_u32(cnt.p, pos.p, n, nullptr, s);
+        DBuf<uint32_t> k2(len, s), v2(len, s), off(ncell + 1, s);
+        k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, pos.p, k2.p, v2.p);
+        TDS_CHECK_LAUNCH();
+        group_by_key(k2.p, v2.p, len, ncell, off.p, s);
+        idx->fsg_A = v2.release();
+        idx->A_len = len;
+        idx->cell_off = off.release();
+        idx->n_cells = ncell;
+    }
+
+    idx->rec = rec.release();
+    idx->perm = perm.release();
+    idx->bin_off = bin_off.release();
+    idx->bin_lo = bin_lo.release();
+    idx->bin_hi = bin_hi.release();
+    idx->bin_pmhi = bin_pmhi.release();
+    TDS_CUDA(cudaStreamSynchronize(s));
+}
+
+void free_index(tds_index_s *idx) {
+    cudaStream_t s = 0;
+    auto f = [&](void *p) { if (p) dfree(p, s); };
+    f(idx->rec); f(idx->perm); f(idx->bin_off); f(idx->bin_lo); f(idx->bin_hi); f(idx->bin_pmhi);
+    for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); }
+    f(idx->cell_off); f(idx->fsg_A);
+    cudaStreamSynchronize(s);
+}
+
+}  // namespace tds

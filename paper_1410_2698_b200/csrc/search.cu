@@ -1,0 +1,1326 @@
+// search.cu — the distance threshold search on the GPU (DESIGN.md steps A6-A11).
+//
+//   A6  query prep: sort Q by t_start, clip to the window [T0,T1]
+//   A7  schedule: candidate range per query (temporal E_k; spatiotemporal
+//       dimension choice; FSG cell rows)
+//   A8  pair kernels (Alg. 1/2/3), B200 mapping:
+//       lane = query, warp = 32 consecutive schedule entries, candidate records
+//       broadcast to the warp (GPUTemporal / GPUSpatioTemporal); lane = candidate
+//       over a flattened (query, cell-row) work list (GPUSpatial)
+//   A9  pair test: fp32 certified filter + fp64 evaluation of the closed form
+//   A10 result append: warp-aggregated, chunk-reserved; overflow -> exact re-plan
+//       of the affected queries (reading C22)
+//   A11 fetch
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "tds_internal.cuh"
+
+namespace tds {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int PT = 256;                  // threads per block of the pair kernels
+constexpr int RANGE_BPS = 3;             // resident blocks per SM (range kernel)
+constexpr int SPATIAL_BPS = 3;
+constexpr int UNROLL = 4;                // candidates per inner step (range kernel)
+constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
+// fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
+// (derived bound 20 u M, u = 2^-24; 64 u used)
+constexpr float KU = 64.0f / 16777216.0f;
+
+struct DevStats {
+    unsigned long long reserved;     // slots reserved in the pass buffer
+    unsigned long long hits;         // records produced (kept or dropped)
+    unsigned long long dropped;      // records dropped (buffer full)
+    unsigned long long refined;      // pairs evaluated in fp64
+    unsigned long long executed;     // lane-pair slots evaluated
+    unsigned long long pair_tests;   // algorithmic candidate pairs
+    unsigned long long fallback;     // ST temporal fallbacks
+    unsigned long long total_slots;  // spatial: flattened slots
+    unsigned int work_ctr;           // dynamic work distribution
+    unsigned int total_items;
+    unsigned int ch;                 // candidates per work item
+    unsigned int cat_cnt[5];         // schedule entries per category
+    unsigned int pad[5];
+};
+
+struct Sched {                       // 16 B schedule entry
+    uint32_t qid;                    // query row
+    uint32_t lo, hi;                 // candidate range [lo, hi) in D (sel<0) or in X/Y/Z[sel]
+    int32_t sel;                     // -1 temporal, 0/1/2 = X/Y/Z, 3 = empty
+};
+
+struct Tile {
+    uint32_t tb, te;                 // schedule entries [tb, te), te - tb <= 32, one category
+    uint32_t ulo, uhi;               // union of their ranges
+    int32_t sel;
+    uint32_t pad[3];
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// A9: pair test
+// ---------------------------------------------------------------------------
+struct QConst {                      // per-lane query constants for the fp32 filter
+    float px, py, pz;                // start point
+    float vx, vy, vz;                // velocity
+    float t0;                        // t_start
+    float t0c, t1c;                  // span clipped to the window
+    float ext;                       // |p1 - p0|_1
+};
+
+__device__ __forceinline__ QConst make_qconst(float4 a, float4 b, float T0, float T1) {
+    QConst q;
+    float dx = __fsub_rn(b.x, a.x), dy = __fsub_rn(b.y, a.y), dz = __fsub_rn(b.z, a.z);
+    float r = rcp_approx(__fsub_rn(b.w, a.w));
+    q.px = a.x; q.py = a.y; q.pz = a.z;
+    q.vx = dx * r; q.vy = dy * r; q.vz = dz * r;
+    q.t0 = a.w;
+    q.t0c = fmaxf(a.w, T0);
+    q.t1c = fminf(b.w, T1);
+    q.ext = fabsf(dx) + fabsf(dy) + fabsf(dz);
+    return q;
+}
+
+// Certified fp32 filter: returns false only if the pair is certainly not within
+// d (shared span empty, or min distance over the span > d).  The computed
+// closest-approach distance differs from the exact one by at most 20 u M
+// (DESIGN.md), M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e - p0e|_1; the test
+// keeps every pair with dist <= d + 64 u M for the fp64 evaluation.
+__device__ __forceinline__ bool filter32(const QConst &q, float4 ea, float4 eb, float d) {
+    float a = fmaxf(q.t0c, ea.w), b = fminf(q.t1c, eb.w);
+    float dex = eb.x - ea.x, dey = eb.y - ea.y, dez = eb.z - ea.z;
+    float r = rcp_approx(eb.w - ea.w);
+    float evx = dex * r, evy = dey * r, evz = dez * r;
+    float aq = a - q.t0, ae = a - ea.w;
+    float dpx = q.px - ea.x, dpy = q.py - ea.y, dpz = q.pz - ea.z;
+    float Dx = fmaf(-ae, evx, fmaf(aq, q.vx, dpx));
+    float Dy = fmaf(-ae, evy, fmaf(aq, q.vy, dpy));
+    float Dz = fmaf(-ae, evz, fmaf(aq, q.vz, dpz));
+    float Vx = q.vx - evx, Vy = q.vy - evy, Vz = q.vz - evz;
+    float L = b - a;
+    float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);     // NaN (A=B=0) -> 0
+    float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + q.ext + fabsf(dex) + fabsf(dey) + fabsf(dez);
+    float thr = fmaf(KU, M, d);
+    return (a < b) & (h <= thr * thr);
+}
+
+// fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
+// the sublevel interval of the convex quadratic ||Pq(t)-Pe(t)||^2 <= d^2 on [a,b].
+__device__ __noinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 eb, double d, double T0, double T1,
+                                    float &t_in, float &t_out) {
+    double t0q = qa.w, t1q = qb.w, t0e = ea.w, t1e = eb.w;
+    double a = fmax(fmax(t0q, t0e), T0);
+    double b = fmin(fmin(t1q, t1e), T1);
+    if (!(a < b)) return false;
+    double dq = t1q - t0q, de = t1e - t0e;
+    double vqx = ((double)qb.x - (double)qa.x) / dq, vqy = ((double)qb.y - (double)qa.y) / dq,
+           vqz = ((double)qb.z - (double)qa.z) / dq;
+    double vex = ((double)eb.x - (double)ea.x) / de, vey = ((double)eb.y - (double)ea.y) / de,
+           vez = ((double)eb.z - (double)ea.z) / de;
+    double Dx = ((double)qa.x + (a - t0q) * vqx) - ((double)ea.x + (a - t0e) * vex);
+    double Dy = ((double)qa.y + (a - t0q) * vqy) - ((double)ea.y + (a - t0e) * vey);
+    double Dz = ((double)qa.z + (a - t0q) * vqz) - ((double)ea.z + (a - t0e) * vez);
+    double Vx = vqx - vex, Vy = vqy - vey, Vz = vqz - vez;
+    double L = b - a;
+    double A = Vx * Vx + Vy * Vy + Vz * Vz;
+    double d2 = d * d;
+    if (A == 0.0) {
+        double h = Dx * Dx + Dy * Dy + Dz * Dz;
+        if (h <= d2) { t_in = (float)a; t_out = (float)b; return true; }
+        return false;
+    }
+    double su = -(Dx * Vx + Dy * Vy + Dz * Vz) / A;
+    double ss = su < 0.0 ? 0.0 : (su > L ? L : su);
+    double xs = Dx + ss * Vx, ys = Dy + ss * Vy, zs = Dz + ss * Vz;
+    double hs = xs * xs + ys * ys + zs * zs;
+    if (!(hs <= d2)) return false;
+    double xu = Dx + su * Vx, yu = Dy + su * Vy, zu = Dz + su * Vz;
+    double hu = xu * xu + yu * yu + zu * zu;
+    double rem = d2 - hu;
+    if (rem < 0.0) rem = 0.0;
+    double w = sqrt(rem / A);
+    double lo = fmin(fmax(su - w, 0.0), L), hi = fmin(fmax(su + w, 0.0), L);
+    t_in = (float)(a + lo);
+    t_out = (float)(a + hi);
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// A10: result append
+// ---------------------------------------------------------------------------
+struct OutArgs {
+    Rec *buf;                        // pass buffer (chunked) or store (exact)
+    unsigned long long cap;          // pass buffer slots
+    uint32_t CS;                     // chunk size (slots)
+    uint32_t *chunk_used;            // [ceil(cap/CS)]
+    uint8_t *redo;                   // [nq] 1 = query lost a record
+    uint32_t *qcount;                // [nq] records produced per query
+    const unsigned long long *qoff;  // exact mode: per-query output offset
+    uint32_t *qfill;                 // exact mode: per-query fill
+    DevStats *st;
+};
+
+struct Appender {                    // per-warp (uniform) chunk state
+    unsigned long long base;
+    uint32_t used, size;
+    bool full;
+    __device__ void init() { base = 0; used = 0; size = 0; full = false; }
+};
+
+// warp-wide: every lane calls with its own hit flag / record; EXACT places the
+// record at the query's planned offset instead.
+template <bool EXACT>
+__device__ __forceinline__ void append(const OutArgs &o, Appender &ap, bool hit, const Rec &r, int lane) {
+    const unsigned hm = __ballot_sync(FULL, hit);
+    if (!hm) return;
+    if (EXACT) {
+        if (hit) {
+            uint32_t k = atomicAdd(&o.qfill[r.qid], 1u);
+            unsigned long long slot = o.qoff[r.qid] + k;
+            reinterpret_cast<uint4 *>(o.buf)[slot] = make_uint4(r.qid, r.eid, __float_as_uint(r.t_in),
+                                                                __float_as_uint(r.t_out));
+        }
+        return;
+    }
+    const uint32_t k = __popc(hm);
+    if (!ap.full && ap.used + k > ap.size) {
+        if (ap.size && lane == 0) o.chunk_used[ap.base / o.CS] = ap.used;
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(&o.st->reserved, (unsigned long long)o.CS);
+        nb = __shfl_sync(FULL, nb, 0);
+        if (nb >= o.cap) {
+            ap.full = true;
+            ap.size = 0;
+            ap.used = 0;
+        } else {
+            ap.base = nb;
+            ap.used = 0;
+            unsigned long long room = o.cap - nb;
+            ap.size = room < o.CS ? (uint32_t)room : o.CS;
+        }
+    }
+    const uint32_t rk = __popc(hm & ((1u << lane) - 1u));
+    if (hit) {
+        if (!ap.full && ap.used + rk < ap.size) {
+            reinterpret_cast<uint4 *>(o.buf)[ap.base + ap.used + rk] =
+                make_uint4(r.qid, r.eid, __float_as_uint(r.t_in), __float_as_uint(r.t_out));
+        } else {
+            o.redo[r.qid] = 1;
+            atomicAdd(&o.st->dropped, 1ull);
+        }
+    }
+    if (!ap.full) ap.used = min(ap.used + k, ap.size);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void close_chunk(const OutArgs &o, Appender &ap, int lane) {
+    if (!EXACT && !ap.full && ap.size && lane == 0) o.chunk_used[ap.base / o.CS] = ap.used;
+}
+
+// ---------------------------------------------------------------------------
+// A6/A7: query sort and schedules
+// ---------------------------------------------------------------------------
+__global__ void k_query_keys(const float4 *__restrict__ Q, uint64_t nq, uint32_t *keys, uint32_t *vals,
+                             unsigned long long *bad) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    float4 a = Q[2 * i], b = Q[2 * i + 1];
+    bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) && isfinite(b.y) &&
+              isfinite(b.z) && isfinite(b.w) && (b.w > a.w);
+    if (!ok) atomicMin(bad, (unsigned long long)i);
+    keys[i] = float_key(a.w);
+    vals[i] = (uint32_t)i;
+}
+
+struct SchedArgs {
+    const float4 *Q;
+    const uint32_t *order;           // t_start-sorted query rows (or a redo list)
+    uint32_t nq;
+    float d, T0, T1;
+    int m, v;
+    const uint32_t *bin_off;
+    const float *bin_lo, *bin_pmhi;
+    const uint32_t *st_off0, *st_off1, *st_off2;
+    float st_o[3], st_w[3];
+    int use_st;
+    Sched *out;
+    uint32_t *keys;                  // sort keys (category-major, then lo) or null
+    DevStats *st;
+};
+
+// first j in [0, m) with a[j] > x (a non-decreasing); m if none
+__device__ __forceinline__ int upper_bound_f(const float *a, int m, float x) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] > x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+// first j with a[j] >= x
+__device__ __forceinline__ int lower_bound_f(const float *a, int m, float x) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] >= x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+__global__ void k_schedule(SchedArgs A) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long work = 0, fb = 0;
+    if (p < A.nq) {
+        uint32_t k = A.order[p];
+        float4 a = A.Q[2 * (uint64_t)k], b = A.Q[2 * (uint64_t)k + 1];
+        float t0c = fmaxf(a.w, A.T0), t1c = fminf(b.w, A.T1);
+        Sched S{k, 0u, 0u, 3};
+        if (t0c < t1c) {
+            // temporal bins overlapping (t0c, t1c): strict member-extent tests (C13)
+            int jlo = upper_bound_f(A.bin_pmhi, A.m, t0c);     // first bin with PMhi > t0c
+            int jhe = lower_bound_f(A.bin_lo, A.m, t1c);       // first bin with lo >= t1c
+            if (jlo < jhe) {
+                S.lo = A.bin_off[jlo];
+                S.hi = A.bin_off[jhe];
+                S.sel = S.lo < S.hi ? -1 : 3;
+                if (A.use_st && S.sel == -1) {
+                    // per dimension, the subbins (slabs) the d-inflated MBB
+                    // overlaps; a dimension is usable only with a single slab
+                    float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+                    const uint32_t *offs[3] = {A.st_off0, A.st_off1, A.st_off2};
+                    uint32_t best = 0xffffffffu;
+                    for (int c = 0; c < 3; ++c) {
+                        float lo = __fsub_rd(fminf(p0[c], p1[c]), A.d);
+                        float hi = __fadd_ru(fmaxf(p0[c], p1[c]), A.d);
+                        int s0 = cell_of(lo, A.st_o[c], A.st_w[c], A.v);
+                        int s1 = cell_of(hi, A.st_o[c], A.st_w[c], A.v);
+                        if (s0 != s1) continue;
+                        uint32_t r0 = offs[c][(uint64_t)s0 * A.m + jlo];
+                        uint32_t r1 = offs[c][(uint64_t)s0 * A.m + jhe];
+                        if (r1 - r0 < best) {               // ties -> lowest dimension (C15)
+                            best = r1 - r0;
+                            S.sel = c;
+                            S.lo = r0;
+                            S.hi = r1;
+                        }
+                    }
+                    if (S.sel == -1) fb = 1;
+                    if (S.lo >= S.hi) S.sel = 3;
+                }
+                if (S.sel == 3) { S.lo = S.hi = 0; }
+                work = S.hi - S.lo;
+            }
+        }
+        A.out[p] = S;
+        if (A.keys) A.keys[p] = S.lo;
+        atomicAdd(&A.st->cat_cnt[S.sel + 1], 1u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        work += __shfl_xor_sync(FULL, work, o);
+        fb += __shfl_xor_sync(FULL, fb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (work) atomicAdd(&A.st->pair_tests, work);
+        if (fb) atomicAdd(&A.st->fallback, fb);
+    }
+}
+
+__global__ void k_cat_keys(const Sched *__restrict__ S, uint32_t n, uint32_t *keys) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) keys[p] = (uint32_t)(S[p].sel + 1);
+}
+
+__global__ void k_permute_sched(const Sched *__restrict__ in, const uint32_t *__restrict__ idx, uint32_t n,
+                                Sched *__restrict__ out) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) out[p] = in[idx[p]];
+}
+
+// tiles: runs of <= 32 consecutive schedule entries within one category
+__global__ void k_make_tiles(const Sched *__restrict__ S, uint32_t n_base, uint32_t n_total_entries,
+                             const DevStats *__restrict__ st, uint32_t range_lo, uint32_t range_hi,
+                             Tile *__restrict__ tiles, uint32_t max_tiles, uint32_t *__restrict__ nchunk_len) {
+    // one warp per tile slot; the tile layout is derived from the category counts
+    uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (t >= max_tiles) return;
+    // category boundaries among entries [range_lo, range_hi) of the sorted schedule
+    uint32_t start[6];
+    start[0] = 0;
+    for (int c = 0; c < 5; ++c) start[c + 1] = start[c] + st->cat_cnt[c];
+    (void)n_base; (void)n_total_entries;
+    // tiles per category (only categories 0..3 carry work; empties are skipped)
+    uint32_t tb = 0, te = 0;
+    int sel = 3;
+    uint32_t acc = 0;
+    bool found = false;
+    for (int c = 0; c < 4 && !found; ++c) {
+        uint32_t a = max(start[c], range_lo), b = min(start[c + 1], range_hi);
+        uint32_t cnt = b > a ? b - a : 0;
+        uint32_t nt = (cnt + 31) / 32;
+        if (t < acc + nt) {
+            tb = a + 32 * (t - acc);
+            te = min(tb + 32, b);
+            sel = c - 1;
+            found = true;
+        }
+        acc += nt;
+    }
+    Tile T{0, 0, 0, 0, 3, {0, 0, 0}};
+    if (found) {
+        uint32_t lo = 0xffffffffu, hi = 0;
+        uint32_t p = tb + lane;
+        if (p < te) {
+            Sched e = S[p];
+            if (e.lo < e.hi) { lo = e.lo; hi = e.hi; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+            hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+        }
+        T.tb = tb; T.te = te; T.sel = sel;
+        if (lo < hi) { T.ulo = lo; T.uhi = hi; } else { T.ulo = T.uhi = 0; }
+    }
+    if (lane == 0) {
+        tiles[t] = T;
+        nchunk_len[t] = T.uhi - T.ulo;
+    }
+}
+
+// chunk size from the total union length, then chunks per tile
+__global__ void k_tile_chunks(uint32_t *len_to_chunks, uint32_t ntiles, const unsigned long long *total_len,
+                              DevStats *st, uint32_t target_items) {
+    unsigned long long tl = *total_len;
+    unsigned long long ch = (tl + target_items - 1) / (target_items ? target_items : 1);
+    ch = ch < 64 ? 64 : (ch > 8192 ? 8192 : ch);
+    uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) st->ch = (uint32_t)ch;
+    if (t < ntiles) len_to_chunks[t] = (uint32_t)((len_to_chunks[t] + ch - 1) / ch);
+}
+
+__global__ void k_sum_u32(const uint32_t *__restrict__ a, uint32_t n, unsigned long long *out) {
+    unsigned long long s = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s += a[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+__global__ void k_set_total_items(const uint32_t *item_start, uint32_t ntiles, DevStats *st) {
+    st->total_items = item_start[ntiles];
+    st->work_ctr = 0;
+}
+
+// ---------------------------------------------------------------------------
+// A8: pair kernel for GPUTemporal / GPUSpatioTemporal (Alg. 2 / Alg. 3)
+// ---------------------------------------------------------------------------
+struct RangeArgs {
+    const float4 *Q;                 // queries (original rows)
+    const float4 *rec;               // sorted entries
+    const uint32_t *perm;
+    const uint32_t *arr[3];          // X, Y, Z
+    const Sched *sched;
+    const Tile *tiles;
+    const uint32_t *item_start;      // [ntiles+1]
+    uint32_t ntiles;
+    float d, T0, T1;
+    OutArgs o;
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(RangeArgs A) {
+    const int lane = threadIdx.x & 31;
+    DevStats *st = A.o.st;
+    const uint32_t total = st->total_items;
+    const uint32_t CH = st->ch;
+    const double d64 = (double)A.d, T064 = (double)A.T0, T164 = (double)A.T1;
+    Appender ap;
+    ap.init();
+    unsigned long long exec = 0, refined = 0, hits = 0;
+    while (true) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= total) break;
+        uint32_t lo = 0, hi = A.ntiles;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (A.item_start[mid] <= item) lo = mid; else hi = mid;
+        }
+        const Tile T = A.tiles[lo];
+        const uint32_t chunk = item - A.item_start[lo];
+        const uint32_t c_lo = T.ulo + chunk * CH;
+        const uint32_t c_hi = min(c_lo + CH, T.uhi);
+        const uint32_t p = T.tb + lane;
+        const bool active = p < T.te;
+        Sched S{0, 0, 0, 3};
+        if (active) S = A.sched[p];
+        uint32_t llo = max(S.lo, c_lo), lhi = min(S.hi, c_hi);
+        if (!active || llo >= lhi) { llo = 0xffffffffu; lhi = 0; }
+        float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
+        if (active) { qa = A.Q[2 * (uint64_t)S.qid]; qb = A.Q[2 * (uint64_t)S.qid + 1]; }
+        const QConst q = make_qconst(qa, qb, A.T0, A.T1);
+        uint32_t wlo = llo, whi = lhi;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wlo = min(wlo, __shfl_xor_sync(FULL, wlo, o));
+            whi = max(whi, __shfl_xor_sync(FULL, whi, o));
+        }
+        if (wlo >= whi) continue;
+        exec += (unsigned long long)(whi - wlo) * __popc(__ballot_sync(FULL, active));
+        const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
+        uint32_t myhits = 0;
+        for (uint32_t i = wlo; i < whi; i += UNROLL) {
+            uint32_t jj[UNROLL];
+            float4 ea[UNROLL], eb[UNROLL];
+            bool mb[UNROLL];
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                uint32_t ii = i + u;
+                bool v = ii < whi;
+                uint32_t j = v ? (arr ? __ldg(arr + ii) : ii) : 0u;
+                jj[u] = j;
+                ea[u] = __ldg(A.rec + 2 * (uint64_t)j);
+                eb[u] = __ldg(A.rec + 2 * (uint64_t)j + 1);
+                mb[u] = v && ii >= llo && ii < lhi && filter32(q, ea[u], eb[u], A.d);
+                any |= mb[u];
+            }
+            if (__any_sync(FULL, any)) {
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    if (!__any_sync(FULL, mb[u])) continue;
+                    float tin = 0.f, tout = 0.f;
+                    bool hit = false;
+                    if (mb[u]) {
+                        ++refined;
+                        hit = pair64(qa, qb, ea[u], eb[u], d64, T064, T164, tin, tout);
+                    }
+                    uint32_t eid = 0;
+                    if (__any_sync(FULL, hit)) eid = __ldg(A.perm + jj[u]);
+                    myhits += hit;
+                    Rec r{S.qid, eid, tin, tout};
+                    append<EXACT>(A.o, ap, hit, r, lane);
+                }
+            }
+        }
+        if (myhits) atomicAdd(&A.o.qcount[S.qid], myhits);
+        hits += myhits;
+    }
+    close_chunk<EXACT>(A.o, ap, lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        refined += __shfl_xor_sync(FULL, refined, o);
+        hits += __shfl_xor_sync(FULL, hits, o);
+    }
+    if (lane == 0) {
+        if (exec) atomicAdd(&st->executed, exec);
+        if (refined) atomicAdd(&st->refined, refined);
+        if (hits) atomicAdd(&st->hits, hits);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GPUSpatial (Alg. 1) work list: per query, the rows (cx, cy) of FSG cells its
+// d-inflated MBB overlaps; a row's cells cz_lo..cz_hi are contiguous in the
+// dense CSR, so one row is one contiguous slice of the lookup array A.
+// ---------------------------------------------------------------------------
+struct FsgGrid {
+    float o[3], w[3];
+    int g[3];
+};
+
+__device__ __forceinline__ void query_box(float4 a, float4 b, float d, const FsgGrid &G, int lo[3], int hi[3]) {
+    float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        lo[c] = cell_of(__fsub_rd(fminf(p0[c], p1[c]), d), G.o[c], G.w[c], G.g[c]);
+        hi[c] = cell_of(__fadd_ru(fmaxf(p0[c], p1[c]), d), G.o[c], G.w[c], G.g[c]);
+    }
+}
+
+__global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__restrict__ list, uint32_t n, float d,
+                            float T0, float T1, FsgGrid G, uint32_t *__restrict__ nrows, int4 *__restrict__ qbox) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    uint32_t k = list ? list[p] : p;
+    float4 a = Q[2 * (uint64_t)k], b = Q[2 * (uint64_t)k + 1];
+    int lo[3], hi[3];
+    query_box(a, b, d, G, lo, hi);
+    bool live = fmaxf(a.w, T0) < fminf(b.w, T1);
+    nrows[p] = live ? (uint32_t)((hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1)) : 0u;
+    qbox[2 * p] = make_int4(lo[0], lo[1], lo[2], (int)k);
+    qbox[2 * p + 1] = make_int4(hi[0], hi[1], hi[2], 0);
+}
+
+__global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, const int4 *__restrict__ qbox,
+                           FsgGrid G, const uint32_t *__restrict__ cell_off, uint32_t *__restrict__ row_q,
+                           uint32_t *__restrict__ row_alo, uint32_t *__restrict__ row_len,
+                           uint32_t *__restrict__ row_cxy) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int4 lo = qbox[2 * p], hi = qbox[2 * p + 1];
+    uint32_t r = row_start[p], rend = row_start[p + 1];
+    if (r == rend) return;
+    for (int x = lo.x; x <= hi.x; ++x)
+        for (int y = lo.y; y <= hi.y; ++y, ++r) {
+            uint64_t h0 = ((uint64_t)x * G.g[1] + y) * G.g[2];
+            uint32_t a0 = cell_off[h0 + lo.z], a1 = cell_off[h0 + hi.z + 1];
+            row_q[r] = p;                       // index into the query list / qbox
+            row_alo[r] = a0;
+            row_len[r] = a1 - a0;
+            row_cxy[r] = ((uint32_t)x << 16) | (uint32_t)y;
+        }
+}
+
+struct SpatialArgs {
+    const float4 *Q;
+    const float4 *rec;
+    const uint32_t *perm;
+    const uint32_t *A;               // lookup array
+    const uint32_t *cell_off;
+    const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
+    const uint32_t *row_q, *row_alo, *row_cxy;
+    const unsigned long long *slot_start;   // [nrows + 1]
+    uint32_t nrows;
+    FsgGrid G;
+    float d, T0, T1;
+    OutArgs o;
+};
+
+__device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint32_t lo, uint32_t hi,
+                                             unsigned long long s) {
+    // last r in [lo, hi) with ss[r] <= s
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (ss[mid] <= s) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(SpatialArgs A) {
+    const int lane = threadIdx.x & 31;
+    DevStats *st = A.o.st;
+    const unsigned long long total = A.slot_start[A.nrows];
+    const double d64 = (double)A.d, T064 = (double)A.T0, T164 = (double)A.T1;
+    Appender ap;
+    ap.init();
+    unsigned long long refined = 0, hits = 0, exec = 0;
+    uint32_t cur_p = 0xffffffffu;
+    uint32_t cur_qrow = 0;
+    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
+    QConst q = make_qconst(qa, qb, A.T0, A.T1);
+    int4 qlo = make_int4(0, 0, 0, 0);
+    constexpr unsigned long long GRAB = 32ull * SP_PER_LANE;
+    while (true) {
+        unsigned long long B = 0;
+        if (lane == 0) B = atomicAdd(&st->total_slots, GRAB);
+        B = __shfl_sync(FULL, B, 0);
+        if (B >= total) break;
+        const unsigned long long Bend = min(B + GRAB, total);
+        // rows of the first and last slot of the grab (lanes 0 / 1), then per-lane search
+        uint32_t rr = 0;
+        if (lane < 2) rr = find_row(A.slot_start, 0, A.nrows, lane == 0 ? B : Bend - 1);
+        const uint32_t rlo = __shfl_sync(FULL, rr, 0), rhi = __shfl_sync(FULL, rr, 1) + 1;
+        uint32_t rprev = rlo;
+        exec += Bend - B;
+        for (int u = 0; u < SP_PER_LANE; ++u) {
+            const unsigned long long s = B + (unsigned long long)u * 32 + lane;
+            const bool v = s < Bend;
+            bool mb = false;
+            uint32_t e = 0, i = 0;
+            float4 ea = make_float4(0.f, 0.f, 0.f, 0.f), eb = make_float4(0.f, 0.f, 0.f, 1.f);
+            if (v) {
+                const uint32_t r = find_row(A.slot_start, rprev, rhi, s);
+                rprev = r;
+                const uint32_t pl = A.row_q[r];
+                i = A.row_alo[r] + (uint32_t)(s - A.slot_start[r]);
+                e = __ldg(A.A + i);
+                ea = __ldg(A.rec + 2 * (uint64_t)e);
+                eb = __ldg(A.rec + 2 * (uint64_t)e + 1);
+                if (pl != cur_p) {
+                    cur_p = pl;
+                    qlo = A.qbox[2 * pl];
+                    cur_qrow = (uint32_t)qlo.w;
+                    qa = A.Q[2 * (uint64_t)cur_qrow];
+                    qb = A.Q[2 * (uint64_t)cur_qrow + 1];
+                    q = make_qconst(qa, qb, A.T0, A.T1);
+                }
+                // duplicate avoidance: test (q, e) only in the first cell (index-space min
+                // corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
+                const int ex = cell_of(fminf(ea.x, eb.x), A.G.o[0], A.G.w[0], A.G.g[0]);
+                const int ey = cell_of(fminf(ea.y, eb.y), A.G.o[1], A.G.w[1], A.G.g[1]);
+                const int ez = cell_of(fminf(ea.z, eb.z), A.G.o[2], A.G.w[2], A.G.g[2]);
+                const uint32_t cxy = A.row_cxy[r];
+                const int rx = max(ex, qlo.x), ry = max(ey, qlo.y), rz = max(ez, qlo.z);
+                bool first = (rx == (int)(cxy >> 16)) && (ry == (int)(cxy & 0xffffu));
+                if (first) {
+                    const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
+                    first = __ldg(A.cell_off + h) <= i && i < __ldg(A.cell_off + h + 1);
+                }
+                mb = first && filter32(q, ea, eb, A.d);
+            }
+            if (!__any_sync(FULL, mb)) continue;
+            float tin = 0.f, tout = 0.f;
+            bool hit = false;
+            if (mb) {
+                ++refined;
+                hit = pair64(qa, qb, ea, eb, d64, T064, T164, tin, tout);
+            }
+            uint32_t eid = hit ? __ldg(A.perm + e) : 0u;
+            Rec rec{cur_qrow, eid, tin, tout};
+            append<EXACT>(A.o, ap, hit, rec, lane);
+            const unsigned hm = __ballot_sync(FULL, hit);
+            if (hit) {
+                // per-query counts, aggregated over lanes of the same query
+                unsigned peers = __match_any_sync(hm, cur_qrow);
+                if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&A.o.qcount[cur_qrow], __popc(peers));
+                ++hits;
+            }
+        }
+    }
+    close_chunk<EXACT>(A.o, ap, lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        refined += __shfl_xor_sync(FULL, refined, o);
+        hits += __shfl_xor_sync(FULL, hits, o);
+    }
+    if (lane == 0) {
+        if (refined) atomicAdd(&st->refined, refined);
+        if (hits) atomicAdd(&st->hits, hits);
+        if (exec) atomicAdd(&st->executed, exec);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// overflow handling (A10): keep records of complete queries, re-plan the rest
+// ---------------------------------------------------------------------------
+__global__ void k_keep_flags(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                             const uint32_t *__restrict__ chunk_used, const uint64_t *__restrict__ chunk_off,
+                             const uint8_t *__restrict__ redo, Rec *__restrict__ flat, uint8_t *__restrict__ keep,
+                             uint64_t nflat) {
+    // flatten the chunked buffer (one warp per chunk) and flag records to keep
+    uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (c >= nchunks) return;
+    uint32_t u = chunk_used[c];
+    uint64_t o = chunk_off[c];
+    for (uint32_t k = lane; k < u; k += 32) {
+        Rec r = buf[c * CS + k];
+        if (o + k < nflat) {
+            flat[o + k] = r;
+            keep[o + k] = redo[r.qid] ? 0 : 1;
+        }
+    }
+}
+
+__global__ void k_flatten(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                          const uint32_t *__restrict__ chunk_used, const uint64_t *__restrict__ chunk_off,
+                          Rec *__restrict__ flat) {
+    uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (c >= nchunks) return;
+    uint32_t u = chunk_used[c];
+    uint64_t o = chunk_off[c];
+    for (uint32_t k = lane; k < u; k += 32) flat[o + k] = buf[c * CS + k];
+}
+
+__global__ void k_u8_to_u32(const uint8_t *__restrict__ a, uint64_t n, uint32_t *__restrict__ b) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+
+__global__ void k_scatter_kept(const Rec *__restrict__ flat, const uint8_t *__restrict__ keep,
+                               const uint32_t *__restrict__ pos, uint64_t n, Rec *__restrict__ out) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && keep[i]) out[pos[i]] = flat[i];
+}
+
+__global__ void k_chunk_offsets_u64(const uint32_t *__restrict__ used, uint64_t n, uint64_t *__restrict__ out) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = used[i];
+}
+
+// redo flags of schedule entries (range variants) / query list (spatial)
+__global__ void k_redo_flags_sched(const Sched *__restrict__ S, uint32_t n, const uint8_t *__restrict__ redo,
+                                   uint32_t *__restrict__ flag) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) flag[p] = redo[S[p].qid];
+}
+
+__global__ void k_compact_sched(const Sched *__restrict__ S, uint32_t n, const uint32_t *__restrict__ flag,
+                                const uint32_t *__restrict__ pos, Sched *__restrict__ out,
+                                const uint32_t *__restrict__ qcount, uint32_t *__restrict__ cnt_out) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n && flag[p]) {
+        out[pos[p]] = S[p];
+        cnt_out[pos[p]] = qcount[S[p].qid];
+    }
+}
+
+__global__ void k_set_qoff(const Sched *__restrict__ S, uint32_t n, const uint64_t *__restrict__ off,
+                           unsigned long long base, unsigned long long *__restrict__ qoff) {
+    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) qoff[S[p].qid] = base + off[p];
+}
+
+__global__ void k_u32_to_u64(const uint32_t *__restrict__ a, uint64_t n, uint64_t *__restrict__ b) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+
+// ---------------------------------------------------------------------------
+// A11: fetch
+// ---------------------------------------------------------------------------
+__global__ void k_fetch_chunked(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                                const uint32_t *__restrict__ used, const uint64_t *__restrict__ off, uint64_t first,
+                                uint64_t count, uint32_t *qid, uint32_t *eid, float *tin, float *tout) {
+    uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (c >= nchunks) return;
+    uint32_t u = used[c];
+    uint64_t o = off[c];
+    if (o + u <= first || o >= first + count) return;
+    for (uint32_t k = lane; k < u; k += 32) {
+        uint64_t g = o + k;
+        if (g < first || g >= first + count) continue;
+        Rec r = buf[c * CS + k];
+        uint64_t j = g - first;
+        if (qid) qid[j] = r.qid;
+        if (eid) eid[j] = r.eid;
+        if (tin) tin[j] = r.t_in;
+        if (tout) tout[j] = r.t_out;
+    }
+}
+
+__global__ void k_fetch_flat(const Rec *__restrict__ rs, const uint32_t *__restrict__ order, uint64_t first,
+                             uint64_t count, uint32_t *qid, uint32_t *eid, float *tin, float *tout) {
+    uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= count) return;
+    uint64_t g = first + j;
+    Rec r = rs[order ? order[g] : g];
+    if (qid) qid[j] = r.qid;
+    if (eid) eid[j] = r.eid;
+    if (tin) tin[j] = r.t_in;
+    if (tout) tout[j] = r.t_out;
+}
+
+__global__ void k_rec_field(const Rec *__restrict__ rs, uint64_t n, int which, const uint32_t *__restrict__ order,
+                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t src = order ? order[i] : (uint32_t)i;
+    Rec r = rs[src];
+    keys[i] = which == 0 ? r.qid : r.eid;
+    vals[i] = src;
+}
+
+inline unsigned nblk(uint64_t n, int nt = 256) { return (unsigned)((n + nt - 1) / nt); }
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+struct Timer {
+    cudaEvent_t e[6];
+    cudaStream_t s;
+    explicit Timer(cudaStream_t s_) : s(s_) {
+        for (auto &x : e) cudaEventCreate(&x);
+    }
+    ~Timer() {
+        for (auto &x : e) cudaEventDestroy(x);
+    }
+    void mark(int k) { cudaEventRecord(e[k], s); }
+    float ms(int a, int b) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e[a], e[b]);
+        return t;
+    }
+};
+
+int persistent_blocks(int bps) { return num_sms() * bps; }
+
+// build tiles + work items for schedule entries [lo, hi) of the sorted schedule
+// (the category counts in st describe the whole sorted schedule)
+uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, DBuf<Tile> &tiles,
+                    DBuf<uint32_t> &item_start, cudaStream_t s) {
+    uint32_t n = hi - lo;
+    uint32_t max_tiles = n / 32 + 5;
+    tiles = DBuf<Tile>(max_tiles, s);
+    item_start = DBuf<uint32_t>(max_tiles + 1, s);
+    TDS_CUDA(cudaMemsetAsync(item_start.p, 0, 4ull * (max_tiles + 1), s));
+    DBuf<unsigned long long> tot(1, s);
+    TDS_CUDA(cudaMemsetAsync(tot.p, 0, 8, s));
+    k_make_tiles<<<nblk((uint64_t)max_tiles * 32), 256, 0, s>>>(sched, lo, n, st, lo, hi, tiles.p, max_tiles,
+                                                                item_start.p);
+    TDS_CHECK_LAUNCH();
+    k_sum_u32<<<std::min<unsigned>(nblk(max_tiles), 1024), 256, 0, s>>>(item_start.p, max_tiles, tot.p);
+    TDS_CHECK_LAUNCH();
+    uint32_t target = (uint32_t)persistent_blocks(RANGE_BPS) * (PT / 32) * 4;
+    k_tile_chunks<<<nblk(max_tiles), 256, 0, s>>>(item_start.p, max_tiles, tot.p, st, target);
+    TDS_CHECK_LAUNCH();
+    exclusive_scan_u32(item_start.p, item_start.p, max_tiles + 1, nullptr, s);
+    k_set_total_items<<<1, 1, 0, s>>>(item_start.p, max_tiles, st);
+    TDS_CHECK_LAUNCH();
+    return max_tiles;
+}
+
+struct Ctx {
+    tds_index_s *idx;
+    int kind;
+    const float4 *Q;
+    uint64_t nq;
+    float d, T0, T1;
+    cudaStream_t s;
+};
+
+}  // namespace
+
+void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, float T0, float T1,
+            uint64_t capacity, cudaStream_t s, tds_result_s *res) {
+    tds_stats &S = res->stats;
+    memset(&S, 0, sizeof S);
+    res->n = 0;
+    res->chunked = false;
+    if (nq == 0) return;
+    if (nq >= (1ull << 31)) fail(TDS_EINVAL, "nq = %llu too large", (unsigned long long)nq);
+    Timer tm(s);
+    tm.mark(0);
+    DBuf<DevStats> dst(1, s);
+    TDS_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(DevStats), s));
+    DBuf<unsigned long long> bad(1, s);
+    TDS_CUDA(cudaMemsetAsync(bad.p, 0xff, 8, s));
+    const uint32_t n = (uint32_t)nq;
+
+    // ---- A6: sort queries by t_start; FSG keeps input order
+    DBuf<uint32_t> keys(n, s), order(n, s);
+    k_query_keys<<<nblk(n), 256, 0, s>>>(Q, nq, keys.p, order.p, bad.p);
+    TDS_CHECK_LAUNCH();
+    const bool spatial = (kind == TDS_SPATIAL);
+    if (!spatial) radix_sort_pairs(keys.p, order.p, n, 0, 32, s);
+
+    DBuf<uint32_t> qcount(n, s);
+    DBuf<uint8_t> redo(n, s);
+    TDS_CUDA(cudaMemsetAsync(qcount.p, 0, 4ull * n, s));
+    TDS_CUDA(cudaMemsetAsync(redo.p, 0, n, s));
+
+    // ---- A7: schedule ---------------------------------------------------------
+    DBuf<Sched> sched;
+    DBuf<Tile> tiles;
+    DBuf<uint32_t> item_start;
+    uint32_t ntiles = 0;
+    // spatial work list
+    FsgGrid G{};
+    DBuf<int4> qbox;
+    DBuf<uint32_t> row_start, row_q, row_alo, row_len, row_cxy;
+    DBuf<unsigned long long> slot_start;
+    uint32_t nrows = 0;
+    if (!spatial) {
+        sched = DBuf<Sched>(n, s);
+        SchedArgs a{};
+        a.Q = Q; a.order = order.p; a.nq = n; a.d = d; a.T0 = T0; a.T1 = T1;
+        a.m = idx->m; a.v = idx->v;
+        a.bin_off = idx->bin_off; a.bin_lo = idx->bin_lo; a.bin_pmhi = idx->bin_pmhi;
+        a.use_st = kind == TDS_SPATIOTEMPORAL;
+        if (a.use_st) {
+            a.st_off0 = idx->st_off[0]; a.st_off1 = idx->st_off[1]; a.st_off2 = idx->st_off[2];
+            for (int c = 0; c < 3; ++c) { a.st_o[c] = idx->ext.lo[c]; a.st_w[c] = idx->ext.w_st[c]; }
+        }
+        a.out = sched.p;
+        a.keys = keys.p;
+        a.st = dst.p;
+        k_schedule<<<nblk(n), 256, 0, s>>>(a);
+        TDS_CHECK_LAUNCH();
+        // sort S by (array selector, range start): stable by lo, then by category
+        DBuf<uint32_t> perm2(n, s);
+        {
+            std::vector<uint32_t> iota(n);
+            std::iota(iota.begin(), iota.end(), 0u);
+            TDS_CUDA(cudaMemcpyAsync(perm2.p, iota.data(), 4ull * n, cudaMemcpyHostToDevice, s));
+            radix_sort_pairs(keys.p, perm2.p, n, 0, 32, s);
+            DBuf<uint32_t> ck(n, s);
+            DBuf<Sched> tmp(n, s);
+            k_permute_sched<<<nblk(n), 256, 0, s>>>(sched.p, perm2.p, n, tmp.p);
+            TDS_CHECK_LAUNCH();
+            k_cat_keys<<<nblk(n), 256, 0, s>>>(tmp.p, n, ck.p);
+            TDS_CHECK_LAUNCH();
+            TDS_CUDA(cudaMemcpyAsync(perm2.p, iota.data(), 4ull * n, cudaMemcpyHostToDevice, s));
+            radix_sort_pairs(ck.p, perm2.p, n, 0, 3, s);
+            k_permute_sched<<<nblk(n), 256, 0, s>>>(tmp.p, perm2.p, n, sched.p);
+            TDS_CHECK_LAUNCH();
+            TDS_CUDA(cudaStreamSynchronize(s));   // iota host buffer lifetime
+        }
+        ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s);
+    } else {
+        for (int c = 0; c < 3; ++c) { G.o[c] = idx->ext.lo[c]; G.w[c] = idx->w_fsg[c]; G.g[c] = idx->grid[c]; }
+        qbox = DBuf<int4>(2ull * n, s);
+        row_start = DBuf<uint32_t>(n + 1, s);
+        DBuf<uint32_t> nr(n + 1, s);
+        TDS_CUDA(cudaMemsetAsync(nr.p + n, 0, 4, s));
+        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p);
+        TDS_CHECK_LAUNCH();
+        exclusive_scan_u32(nr.p, row_start.p, n + 1, nullptr, s);
+        TDS_CUDA(cudaMemcpyAsync(&nrows, row_start.p + n, 4, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        row_q = DBuf<uint32_t>(nrows, s);
+        row_alo = DBuf<uint32_t>(nrows, s);
+        row_len = DBuf<uint32_t>(nrows + 1, s);
+        row_cxy = DBuf<uint32_t>(nrows, s);
+        TDS_CUDA(cudaMemsetAsync(row_len.p + nrows, 0, 4, s));
+        k_fsg_rows<<<nblk(n), 256, 0, s>>>(row_start.p, n, qbox.p, G, idx->cell_off, row_q.p, row_alo.p, row_len.p,
+                                          row_cxy.p);
+        TDS_CHECK_LAUNCH();
+        DBuf<uint64_t> rl64(nrows + 1, s);
+        k_u32_to_u64<<<nblk(nrows + 1), 256, 0, s>>>(row_len.p, nrows + 1, rl64.p);
+        TDS_CHECK_LAUNCH();
+        slot_start = DBuf<unsigned long long>(nrows + 1, s);
+        exclusive_scan_u64(rl64.p, (uint64_t *)slot_start.p, nrows + 1, (uint64_t *)&dst.p->pair_tests, s);
+    }
+    // pair tests bound the result count: size the pass buffer
+    DevStats hs;
+    TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+    unsigned long long hbad = 0;
+    TDS_CUDA(cudaMemcpyAsync(&hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaStreamSynchronize(s));
+    if (hbad != ~0ull) fail(TDS_EDATA, "query segment %llu has a non-finite value or t_end <= t_start", hbad);
+    tm.mark(1);
+    S.pair_tests = hs.pair_tests;
+    S.fallback_queries = hs.fallback;
+    S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
+
+    uint64_t cap = capacity;
+    if (cap == 0) {
+        size_t fr = 0, tot = 0;
+        TDS_CUDA(cudaMemGetInfo(&fr, &tot));
+        uint64_t budget = (uint64_t)(fr * 0.35) / sizeof(Rec);
+        cap = std::min<uint64_t>(hs.pair_tests + 64, budget);
+        cap = std::max<uint64_t>(cap, 1024);
+    }
+    cap = std::min<uint64_t>(cap, (1ull << 40));
+    const int bps = spatial ? SPATIAL_BPS : RANGE_BPS;
+    const uint64_t nwarps = (uint64_t)persistent_blocks(bps) * (PT / 32);
+    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(32, cap / (16 * nwarps)));
+    CS = (CS + 31) / 32 * 32;
+    const uint64_t nchunks = (cap + CS - 1) / CS;
+    DBuf<Rec> buf(cap, s);
+    DBuf<uint32_t> chunk_used(nchunks, s);
+    TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
+
+    OutArgs o{};
+    o.buf = buf.p; o.cap = cap; o.CS = CS; o.chunk_used = chunk_used.p;
+    o.redo = redo.p; o.qcount = qcount.p; o.st = dst.p;
+
+    // ---- A8-A10: pass 1 --------------------------------------------------------
+    tm.mark(2);
+    if (!spatial) {
+        RangeArgs a{};
+        a.Q = Q; a.rec = idx->rec; a.perm = idx->perm;
+        for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
+        a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
+        a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
+        k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+        TDS_CHECK_LAUNCH();
+    } else if (nrows > 0) {
+        SpatialArgs a{};
+        a.Q = Q; a.rec = idx->rec; a.perm = idx->perm; a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+        a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
+        a.slot_start = slot_start.p; a.nrows = nrows; a.G = G; a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
+        k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
+        TDS_CHECK_LAUNCH();
+    }
+    tm.mark(3);
+    TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaStreamSynchronize(s));
+    S.passes = 1;
+    S.refined_pairs = hs.refined;
+    S.pairs_executed = hs.executed;
+
+    DBuf<uint64_t> chunk_off(nchunks, s);
+    k_chunk_offsets_u64<<<nblk(nchunks), 256, 0, s>>>(chunk_used.p, nchunks, chunk_off.p);
+    TDS_CHECK_LAUNCH();
+    exclusive_scan_u64(chunk_off.p, chunk_off.p, nchunks, nullptr, s);
+
+    if (hs.dropped == 0) {
+        res->chunked = true;
+        res->buf = buf.release();
+        res->cap = cap;
+        res->CS = CS;
+        res->nchunks = nchunks;
+        res->chunk_used = chunk_used.release();
+        res->chunk_off = chunk_off.release();
+        res->n = hs.hits;
+        tm.mark(4);
+        TDS_CUDA(cudaEventSynchronize(tm.e[4]));
+        S.n_results = res->n;
+        S.ms_schedule = tm.ms(0, 1);
+        S.ms_pairs = tm.ms(2, 3);
+        S.ms_total = tm.ms(0, 4);
+        return;
+    }
+
+    // ---- overflow: keep complete queries, re-plan the others exactly ------------
+    const uint64_t stored = std::min<unsigned long long>(hs.reserved, cap);
+    uint64_t nflat = hs.hits - hs.dropped;          // records physically in the buffer
+    (void)stored;
+    DBuf<Rec> flat(nflat, s);
+    DBuf<uint8_t> keep(nflat, s);
+    k_keep_flags<<<nblk(nchunks * 32), 256, 0, s>>>(buf.p, CS, nchunks, chunk_used.p, chunk_off.p, redo.p, flat.p,
+                                                  keep.p, nflat);
+    TDS_CHECK_LAUNCH();
+    DBuf<uint32_t> kpos(nflat + 1, s), k32(nflat + 1, s);
+    TDS_CUDA(cudaMemsetAsync(k32.p, 0, 4ull * (nflat + 1), s));
+    k_u8_to_u32<<<nblk(nflat), 256, 0, s>>>(keep.p, nflat, k32.p);
+    TDS_CHECK_LAUNCH();
+    exclusive_scan_u32(k32.p, kpos.p, nflat + 1, nullptr, s);
+    uint32_t nkept = 0;
+    TDS_CUDA(cudaMemcpyAsync(&nkept, kpos.p + nflat, 4, cudaMemcpyDeviceToHost, s));
+
+    // redo list with exact counts, in schedule order (range) / input order (spatial)
+    std::vector<uint32_t> hcnt;
+    DBuf<Sched> rsched;
+    DBuf<uint32_t> rlist;              // spatial: redo query rows
+    uint32_t nredo = 0;
+    if (!spatial) {
+        DBuf<uint32_t> flag(n + 1, s), fpos(n + 1, s), cnt(n, s);
+        TDS_CUDA(cudaMemsetAsync(flag.p + n, 0, 4, s));
+        k_redo_flags_sched<<<nblk(n), 256, 0, s>>>(sched.p, n, redo.p, flag.p);
+        TDS_CHECK_LAUNCH();
+        exclusive_scan_u32(flag.p, fpos.p, n + 1, nullptr, s);
+        rsched = DBuf<Sched>(n, s);
+        k_compact_sched<<<nblk(n), 256, 0, s>>>(sched.p, n, flag.p, fpos.p, rsched.p, qcount.p, cnt.p);
+        TDS_CHECK_LAUNCH();
+        TDS_CUDA(cudaMemcpyAsync(&nredo, fpos.p + n, 4, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        hcnt.resize(nredo);
+        if (nredo) TDS_CUDA(cudaMemcpyAsync(hcnt.data(), cnt.p, 4ull * nredo, cudaMemcpyDeviceToHost, s));
+    } else {
+        std::vector<uint8_t> hr(n);
+        std::vector<uint32_t> hq(n);
+        TDS_CUDA(cudaMemcpyAsync(hr.data(), redo.p, n, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaMemcpyAsync(hq.data(), qcount.p, 4ull * n, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        std::vector<uint32_t> rl;
+        for (uint32_t k = 0; k < n; ++k)
+            if (hr[k]) { rl.push_back(k); hcnt.push_back(hq[k]); }
+        nredo = (uint32_t)rl.size();
+        rlist = DBuf<uint32_t>(nredo, s);
+        if (nredo) TDS_CUDA(cudaMemcpyAsync(rlist.p, rl.data(), 4ull * nredo, cudaMemcpyHostToDevice, s));
+    }
+    TDS_CUDA(cudaStreamSynchronize(s));
+    uint64_t redo_total = 0;
+    for (uint32_t c : hcnt) {
+        if (c > cap) fail(TDS_ECAPACITY, "one query produces %u records, more than capacity %llu", c,
+                          (unsigned long long)cap);
+        redo_total += c;
+    }
+    const uint64_t total = (uint64_t)nkept + redo_total;
+    DBuf<Rec> store(total, s);
+    k_scatter_kept<<<nblk(nflat), 256, 0, s>>>(flat.p, keep.p, kpos.p, nflat, store.p);
+    TDS_CHECK_LAUNCH();
+    flat.reset();
+    keep.reset();
+    buf.reset();
+    S.spilled = nkept;
+
+    // per-query exact offsets in redo order
+    DBuf<unsigned long long> qoff(n, s);
+    DBuf<uint32_t> qfill(n, s);
+    TDS_CUDA(cudaMemsetAsync(qfill.p, 0, 4ull * n, s));
+    {
+        std::vector<uint64_t> off(nredo);
+        uint64_t acc = nkept;
+        for (uint32_t k = 0; k < nredo; ++k) { off[k] = acc; acc += hcnt[k]; }
+        DBuf<uint64_t> doff(nredo, s);
+        if (nredo) TDS_CUDA(cudaMemcpyAsync(doff.p, off.data(), 8ull * nredo, cudaMemcpyHostToDevice, s));
+        if (!spatial) {
+            if (nredo) k_set_qoff<<<nblk(nredo), 256, 0, s>>>(rsched.p, nredo, doff.p, 0ull, qoff.p);
+        } else {
+            // spatial: scatter offsets by query row
+            std::vector<uint32_t> rl(nredo);
+            if (nredo) TDS_CUDA(cudaMemcpyAsync(rl.data(), rlist.p, 4ull * nredo, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            std::vector<unsigned long long> hq(n, 0);
+            for (uint32_t k = 0; k < nredo; ++k) hq[rl[k]] = off[k];
+            TDS_CUDA(cudaMemcpyAsync(qoff.p, hq.data(), 8ull * n, cudaMemcpyHostToDevice, s));
+        }
+        TDS_CHECK_LAUNCH();
+        TDS_CUDA(cudaStreamSynchronize(s));
+    }
+    tm.mark(4);
+    // batches: consecutive redo entries with sum(count) <= cap (paper's incremental
+    // processing of Q)
+    o.buf = store.p;
+    o.qoff = qoff.p;
+    o.qfill = qfill.p;
+    DBuf<uint32_t> qcount2(n, s);      // counts are recomputed, not needed again
+    TDS_CUDA(cudaMemsetAsync(qcount2.p, 0, 4ull * n, s));
+    o.qcount = qcount2.p;
+    uint32_t b0 = 0;
+    while (b0 < nredo) {
+        uint64_t acc = 0;
+        uint32_t b1 = b0;
+        while (b1 < nredo && acc + hcnt[b1] <= cap) acc += hcnt[b1++];
+        TDS_CUDA(cudaMemsetAsync(&dst.p->work_ctr, 0, 4, s));
+        TDS_CUDA(cudaMemsetAsync(&dst.p->total_slots, 0, 8, s));
+        if (!spatial) {
+            // category counts of the batch: re-derive by planning on the compacted list
+            DBuf<DevStats> bst(1, s);
+            TDS_CUDA(cudaMemsetAsync(bst.p, 0, sizeof(DevStats), s));
+            DBuf<uint32_t> ck(b1 - b0, s);
+            // count categories of [b0, b1)
+            std::vector<Sched> hsched(b1 - b0);
+            TDS_CUDA(cudaMemcpyAsync(hsched.data(), rsched.p + b0, sizeof(Sched) * (b1 - b0),
+                                     cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            DevStats hb{};
+            for (auto &e : hsched) hb.cat_cnt[e.sel + 1]++;
+            TDS_CUDA(cudaMemcpyAsync(bst.p, &hb, sizeof hb, cudaMemcpyHostToDevice, s));
+            DBuf<Tile> bt;
+            DBuf<uint32_t> bis;
+            uint32_t bnt = plan_items(rsched.p + b0, 0, b1 - b0, bst.p, bt, bis, s);
+            RangeArgs a{};
+            a.Q = Q; a.rec = idx->rec; a.perm = idx->perm;
+            for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
+            a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
+            a.d = d; a.T0 = T0; a.T1 = T1;
+            a.o = o;
+            a.o.st = bst.p;
+            k_pair_range<true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+            TDS_CHECK_LAUNCH();
+            TDS_CUDA(cudaStreamSynchronize(s));
+            DevStats hb2;
+            TDS_CUDA(cudaMemcpy(&hb2, bst.p, sizeof hb2, cudaMemcpyDeviceToHost));
+            S.refined_pairs += hb2.refined;
+            S.pairs_executed += hb2.executed;
+        } else {
+            uint32_t nb = b1 - b0;
+            DBuf<int4> bq(2ull * nb, s);
+            DBuf<uint32_t> bnr(nb + 1, s), brs(nb + 1, s);
+            TDS_CUDA(cudaMemsetAsync(bnr.p + nb, 0, 4, s));
+            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u32(bnr.p, brs.p, nb + 1, nullptr, s);
+            uint32_t bnrows = 0;
+            TDS_CUDA(cudaMemcpyAsync(&bnrows, brs.p + nb, 4, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            DBuf<uint32_t> rq(bnrows, s), ra(bnrows, s), rlen(bnrows + 1, s), rc(bnrows, s);
+            TDS_CUDA(cudaMemsetAsync(rlen.p + bnrows, 0, 4, s));
+            k_fsg_rows<<<nblk(nb), 256, 0, s>>>(brs.p, nb, bq.p, G, idx->cell_off, rq.p, ra.p, rlen.p, rc.p);
+            TDS_CHECK_LAUNCH();
+            DBuf<uint64_t> rl64(bnrows + 1, s);
+            DBuf<unsigned long long> ss(bnrows + 1, s);
+            k_u32_to_u64<<<nblk(bnrows + 1), 256, 0, s>>>(rlen.p, bnrows + 1, rl64.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u64(rl64.p, (uint64_t *)ss.p, bnrows + 1, nullptr, s);
+            SpatialArgs a{};
+            a.Q = Q; a.rec = idx->rec; a.perm = idx->perm; a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+            a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
+            a.nrows = bnrows; a.G = G; a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
+            if (bnrows) {
+                k_pair_spatial<true><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
+                TDS_CHECK_LAUNCH();
+            }
+            TDS_CUDA(cudaStreamSynchronize(s));
+            DevStats hb2;
+            TDS_CUDA(cudaMemcpy(&hb2, dst.p, sizeof hb2, cudaMemcpyDeviceToHost));
+            S.refined_pairs = hb2.refined;
+            S.pairs_executed = hb2.executed;
+        }
+        S.passes++;
+        b0 = b1;
+    }
+    tm.mark(5);
+    TDS_CUDA(cudaStreamSynchronize(s));
+    res->chunked = false;
+    res->store = store.release();
+    res->n = total;
+    S.n_results = total;
+    S.ms_schedule = tm.ms(0, 1);
+    S.ms_pairs = tm.ms(2, 3) + tm.ms(4, 5);
+    S.ms_compact = tm.ms(3, 4);
+    S.ms_total = tm.ms(0, 5);
+}
+
+void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint32_t *eid, float *tin, float *tout,
+           bool dst_dev, bool sorted, cudaStream_t s) {
+    if (first > r->n || count > r->n - first) fail(TDS_EINVAL, "fetch range [%llu, +%llu) outside %llu records",
+                                                   (unsigned long long)first, (unsigned long long)count,
+                                                   (unsigned long long)r->n);
+    if (count == 0) return;
+    // device staging for host destinations
+    DBuf<uint32_t> dq, de;
+    DBuf<float> di, doo;
+    uint32_t *oq = qid, *oe = eid;
+    float *oi = tin, *oo = tout;
+    if (!dst_dev) {
+        if (qid) { dq = DBuf<uint32_t>(count, s); oq = dq.p; }
+        if (eid) { de = DBuf<uint32_t>(count, s); oe = de.p; }
+        if (tin) { di = DBuf<float>(count, s); oi = di.p; }
+        if (tout) { doo = DBuf<float>(count, s); oo = doo.p; }
+    }
+    if (!sorted) {
+        if (r->chunked) {
+            k_fetch_chunked<<<nblk(r->nchunks * 32), 256, 0, s>>>(r->buf, r->CS, r->nchunks, r->chunk_used,
+                                                                  r->chunk_off, first, count, oq, oe, oi, oo);
+        } else {
+            k_fetch_flat<<<nblk(count), 256, 0, s>>>(r->store, nullptr, first, count, oq, oe, oi, oo);
+        }
+        TDS_CHECK_LAUNCH();
+    } else {
+        // flatten, then stable radix sort by entry id, then by query id
+        const uint64_t n = r->n;
+        DBuf<Rec> flat;
+        const Rec *rs = r->store;
+        if (r->chunked) {
+            flat = DBuf<Rec>(n, s);
+            k_flatten<<<nblk(r->nchunks * 32), 256, 0, s>>>(r->buf, r->CS, r->nchunks, r->chunk_used, r->chunk_off,
+                                                            flat.p);
+            TDS_CHECK_LAUNCH();
+            rs = flat.p;
+        }
+        DBuf<uint32_t> k1(n, s), ord(n, s), k2(n, s), ord2(n, s);
+        k_rec_field<<<nblk(n), 256, 0, s>>>(rs, n, 1, nullptr, k1.p, ord.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(k1.p, ord.p, n, 0, 32, s);
+        k_rec_field<<<nblk(n), 256, 0, s>>>(rs, n, 0, ord.p, k2.p, ord2.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(k2.p, ord2.p, n, 0, 32, s);
+        k_fetch_flat<<<nblk(count), 256, 0, s>>>(rs, ord2.p, first, count, oq, oe, oi, oo);
+        TDS_CHECK_LAUNCH();
+        TDS_CUDA(cudaStreamSynchronize(s));
+    }
+    if (!dst_dev) {
+        if (qid) TDS_CUDA(cudaMemcpyAsync(qid, oq, 4 * count, cudaMemcpyDeviceToHost, s));
+        if (eid) TDS_CUDA(cudaMemcpyAsync(eid, oe, 4 * count, cudaMemcpyDeviceToHost, s));
+        if (tin) TDS_CUDA(cudaMemcpyAsync(tin, oi, 4 * count, cudaMemcpyDeviceToHost, s));
+        if (tout) TDS_CUDA(cudaMemcpyAsync(tout, oo, 4 * count, cudaMemcpyDeviceToHost, s));
+    }
+    TDS_CUDA(cudaStreamSynchronize(s));
+}
+
+void free_result(tds_result_s *r) {
+    cudaStream_t s = 0;
+    if (r->buf) dfree(r->buf, s);
+    if (r->chunk_used) dfree(r->chunk_used, s);
+    if (r->chunk_off) dfree(r->chunk_off, s);
+    if (r->store) dfree(r->store, s);
+    r->buf = nullptr; r->chunk_used = nullptr; r->chunk_off = nullptr; r->store = nullptr;
+    cudaStreamSynchronize(s);
+}
+
+}  // namespace tds

@@ -1,0 +1,243 @@
+// sort.cu — device primitives hand-written for sm_100a: exclusive scan
+// (reduce-then-scan) and a stable LSD radix sort of (uint32 key, uint32 value)
+// pairs.  Used by the index build (t_start sort P:569-571, subbin / cell
+// grouping P:347-361) and by query preparation (sort Q by t_start,
+// P:681-682; sort S by the array selector).
+#include "tds_internal.cuh"
+
+namespace tds {
+
+namespace {
+
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;   // 4096 elements per block
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix, writes the block total to *total.
+template <class T, int NT>
+__device__ __forceinline__ T block_excl_scan(T x, T *total) {
+    __shared__ T wsum[NT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T inc = warp_incl_scan(x);
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        T v = (lane < NT / 32) ? wsum[lane] : T(0);
+        T vi = warp_incl_scan(v);
+        if (lane < NT / 32) wsum[lane] = vi - v;
+        if (lane == NT / 32 - 1) *total = vi;
+    }
+    __syncthreads();
+    T r = inc - x + wsum[w];
+    __syncthreads();
+    return r;
+}
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T *__restrict__ in, uint64_t n,
+                                                              T *__restrict__ partial) {
+    uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        uint64_t k = base + (uint64_t)i * SCAN_THREADS + threadIdx.x;
+        if (k < n) s += in[k];
+    }
+    __shared__ T tot;
+    block_excl_scan<T, SCAN_THREADS>(s, &tot);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of partial[0..nb) in place, total -> *d_total
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(T *partial, uint64_t nb, T *d_total) {
+    __shared__ T tot;
+    T carry = 0;
+    for (uint64_t b0 = 0; b0 < nb; b0 += SCAN_THREADS) {
+        uint64_t k = b0 + threadIdx.x;
+        T x = (k < nb) ? partial[k] : T(0);
+        T e = block_excl_scan<T, SCAN_THREADS>(x, &tot);
+        if (k < nb) partial[k] = carry + e;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && d_total) *d_total = carry;
+}
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const T *__restrict__ in, T *out, uint64_t n,
+                                                             const T *__restrict__ partial) {
+    __shared__ T buf[SCAN_TILE];
+    __shared__ T tot;
+    uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {        // coalesced load (striped)
+        int j = i * SCAN_THREADS + threadIdx.x;
+        uint64_t k = base + j;
+        buf[j] = (k < n) ? in[k] : T(0);
+    }
+    __syncthreads();
+    T v[SCAN_ITEMS];
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {        // blocked: thread owns 8 consecutive
+        v[i] = buf[threadIdx.x * SCAN_ITEMS + i];
+        s += v[i];
+    }
+    T e = block_excl_scan<T, SCAN_THREADS>(s, &tot) + partial[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        buf[threadIdx.x * SCAN_ITEMS + i] = e;
+        e += v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int j = i * SCAN_THREADS + threadIdx.x;
+        uint64_t k = base + j;
+        if (k < n) out[k] = buf[j];
+    }
+}
+
+template <class T>
+void exclusive_scan_impl(const T *in, T *out, uint64_t n, T *d_total, cudaStream_t s) {
+    if (n == 0) {
+        if (d_total) TDS_CUDA(cudaMemsetAsync(d_total, 0, sizeof(T), s));
+        return;
+    }
+    uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DBuf<T> partial(nb, s);
+    k_scan_reduce<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, partial.p);
+    TDS_CHECK_LAUNCH();
+    k_scan_partials<T><<<1, SCAN_THREADS, 0, s>>>(partial.p, nb, d_total);
+    TDS_CHECK_LAUNCH();
+    k_scan_apply<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, partial.p);
+    TDS_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// radix sort
+// ---------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ROUNDS = 8;                        // keys per thread
+constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;     // 2048 keys per tile
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t *__restrict__ keys, uint64_t n,
+                                                        int shift, uint32_t mask, uint32_t *__restrict__ hist,
+                                                        uint32_t ntiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        uint64_t k = base + (uint64_t)r * RS_THREADS + threadIdx.x;
+        if (k < n) atomicAdd(&h[(keys[k] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t *__restrict__ kin,
+                                                           const uint32_t *__restrict__ vin,
+                                                           uint32_t *__restrict__ kout,
+                                                           uint32_t *__restrict__ vout, uint64_t n, int shift,
+                                                           uint32_t mask, const uint32_t *__restrict__ offs,
+                                                           uint32_t ntiles) {
+    __shared__ uint32_t cnt[RS_WARPS][256];
+    __shared__ uint32_t base[256];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+    base[threadIdx.x] = offs[(uint64_t)threadIdx.x * ntiles + blockIdx.x];
+    __syncthreads();
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t key[RS_ROUNDS], val[RS_ROUNDS], rank[RS_ROUNDS];
+    int dig[RS_ROUNDS];
+    uint64_t tbase = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)w * (32 * RS_ROUNDS);
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        uint64_t k = tbase + (uint64_t)r * 32 + lane;
+        bool valid = k < n;
+        key[r] = valid ? kin[k] : 0u;
+        val[r] = valid ? vin[k] : 0u;
+        int d = valid ? (int)((key[r] >> shift) & mask) : 256;
+        dig[r] = d;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t lt = __popc(peers & lt_mask);
+        uint32_t c = (d < 256) ? cnt[w][d] : 0u;
+        rank[r] = c + lt;
+        __syncwarp();
+        if (d < 256 && lt == 0) cnt[w][d] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // exclusive prefix over warps, per digit (thread = digit)
+        uint32_t run = 0;
+        const int d = threadIdx.x;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ++ww) {
+            uint32_t t = cnt[ww][d];
+            cnt[ww][d] = run + base[d];
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        if (dig[r] < 256) {
+            uint32_t pos = cnt[w][dig[r]] + rank[r];
+            kout[pos] = key[r];
+            vout[pos] = val[r];
+        }
+    }
+}
+
+}  // namespace
+
+void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *d_total, cudaStream_t s) {
+    exclusive_scan_impl<uint32_t>(in, out, n, d_total, s);
+}
+
+void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *d_total, cudaStream_t s) {
+    exclusive_scan_impl<uint64_t>(in, out, n, d_total, s);
+}
+
+void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit, cudaStream_t s) {
+    if (n <= 1 || end_bit <= begin_bit) return;
+    if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
+    uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    DBuf<uint32_t> k2(n, s), v2(n, s), hist((uint64_t)256 * ntiles, s);
+    uint32_t *ka = keys, *va = vals, *kb = k2.p, *vb = v2.p;
+    int passes = 0;
+    for (int shift = begin_bit; shift < end_bit; shift += 8, ++passes) {
+        int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+        uint32_t mask = (1u << nb) - 1u;
+        k_rs_hist<<<ntiles, RS_THREADS, 0, s>>>(ka, n, shift, mask, hist.p, ntiles);
+        TDS_CHECK_LAUNCH();
+        exclusive_scan_u32(hist.p, hist.p, (uint64_t)256 * ntiles, nullptr, s);
+        k_rs_scatter<<<ntiles, RS_THREADS, 0, s>>>(ka, va, kb, vb, n, shift, mask, hist.p, ntiles);
+        TDS_CHECK_LAUNCH();
+        uint32_t *t;
+        t = ka; ka = kb; kb = t;
+        t = va; va = vb; vb = t;
+    }
+    if (passes & 1) {
+        TDS_CUDA(cudaMemcpyAsync(keys, ka, n * 4, cudaMemcpyDeviceToDevice, s));
+        TDS_CUDA(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+}  // namespace tds

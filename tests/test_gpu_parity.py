@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Marked gpu: run on a B200 via gpurun."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import check, keys
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("temporal", "spatiotemporal", "spatial")
+
+
+@pytest.fixture(scope="module")
+def tds():
+    import torch
+    import paper_1410_2698_b200 as t
+    t.load_library()
+    assert torch.cuda.is_available()
+    return t
+
+
+def _cuda(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _run(idx, Q, d, kind, window=(-math.inf, math.inf), capacity=0):
+    r = idx.search(_cuda(Q), d, window=window, kind=kind, capacity=capacity)
+    got = r.fetch(sorted=True, device=False)
+    st = r.stats()
+    r.close()
+    return got, st
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    w = synth.tiny()
+    return w, oracle.search(w.D, w.Q, w.d)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_tiny_default(tds, tiny, kind):
+    w, ref = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    got, st = _run(idx, w.Q, w.d, kind)
+    rep = check(got, ref, w.D, w.Q, w.d, label=kind)
+    assert rep["pairs"] > 50
+    assert st["n_results"] == len(got[0])
+
+
+@pytest.mark.parametrize("m", [1, 3, 10, 100])
+@pytest.mark.parametrize("v", [1, 2, 3])
+def test_tiny_param_sweep_temporal_st(tds, tiny, m, v):
+    w, ref = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=m, v=v)
+    for kind in ("temporal", "spatiotemporal"):
+        got, _ = _run(idx, w.Q, w.d, kind)
+        check(got, ref, w.D, w.Q, w.d, label=f"{kind} m={m} v={v}")
+
+
+@pytest.mark.parametrize("g", [1, 4, 10, 33])
+def test_tiny_grid_sweep_spatial(tds, tiny, g):
+    w, ref = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.SPATIAL, m=10, grid=(g, g, max(1, g // 2)))
+    got, _ = _run(idx, w.Q, w.d, "spatial")
+    check(got, ref, w.D, w.Q, w.d, label=f"spatial g={g}")
+
+
+@pytest.mark.parametrize("cap", [1, 7, 100, 1000])
+@pytest.mark.parametrize("kind", KINDS)
+def test_tiny_forced_capacity(tds, tiny, cap, kind):
+    """Overflow re-launch: results identical whatever the buffer size."""
+    w, ref = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    if cap == 1:
+        # some query has more than one record -> one query alone exceeds the capacity
+        with pytest.raises(tds.TdsError) as ei:
+            _run(idx, w.Q, w.d, kind, capacity=cap)
+        assert ei.value.status == "TDS_ECAPACITY"
+        return
+    got, st = _run(idx, w.Q, w.d, kind, capacity=cap)
+    check(got, ref, w.D, w.Q, w.d, label=f"{kind} cap={cap}")
+    if cap < len(got[0]):
+        assert st["passes"] > 1
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("window", [(8.0, 12.0), (0.0, 3.5), (13.2, 13.2000005), (30.0, 40.0)])
+def test_tiny_window(tds, tiny, kind, window):
+    w, _ = tiny
+    ref = oracle.search(w.D, w.Q, w.d, window=window)
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    got, _ = _run(idx, w.Q, w.d, kind, window=window)
+    check(got, ref, w.D, w.Q, w.d, window=window, label=f"{kind} {window}")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("d", [1e-3, 0.3, 7.0, 50.0])
+def test_tiny_d_sweep(tds, tiny, kind, d):
+    w, _ = tiny
+    ref = oracle.search(w.D, w.Q, d)
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=1, grid=w.grid)
+    got, _ = _run(idx, w.Q, d, kind)
+    check(got, ref, w.D, w.Q, d, label=f"{kind} d={d}")
+
+
+def test_edge_cases(tds, tiny):
+    w, _ = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    # empty query set
+    r = idx.search(_cuda(np.zeros((0, 8), np.float32)), 1.0)
+    assert r.count == 0
+    # queries entirely outside the data in time and space
+    Q = w.Q.copy()
+    Q[:, 3] += 1000
+    Q[:, 7] += 1000
+    for kind in KINDS:
+        assert idx.search(_cuda(Q), w.d, kind=kind).count == 0
+    # stationary queries and a query identical to an entry (self hit over its span)
+    Q = np.concatenate([w.D[:7], w.D[:3]]).copy()
+    Q[7:, 4:7] = Q[7:, 0:3]
+    ref = oracle.search(w.D, Q, 0.5)
+    for kind in KINDS:
+        got, _ = _run(idx, Q, 0.5, kind)
+        check(got, ref, w.D, Q, 0.5, label=f"edge {kind}")
+    # error paths
+    bad = w.Q.copy()
+    bad[5, 7] = bad[5, 3]
+    with pytest.raises(tds.TdsError) as ei:
+        idx.search(_cuda(bad), 1.0)
+    assert ei.value.status == "TDS_EDATA"
+    with pytest.raises(tds.TdsError) as ei:
+        idx.search(_cuda(w.Q), 0.0)
+    assert ei.value.status == "TDS_EINVAL"
+    with pytest.raises(tds.TdsError) as ei:
+        tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=10, v=10_000)
+    assert ei.value.status == "TDS_EINVAL"
+    badD = w.D.copy()
+    badD[17, 2] = np.nan
+    with pytest.raises(tds.TdsError) as ei:
+        tds.Index(_cuda(badD), kinds=tds.TEMPORAL, m=10)
+    assert ei.value.status == "TDS_EDATA" and "17" in str(ei.value)
+
+
+def test_host_inputs_and_host_fetch(tds, tiny):
+    """The C-ABI accepts host buffers (e2e path)."""
+    w, ref = tiny
+    idx = tds.Index(w.D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    r = idx.search(w.Q, w.d, kind="temporal")
+    got = r.fetch(sorted=True, device=False)
+    check(got, ref, w.D, w.Q, w.d, label="host")
+
+
+def test_index_build_matches_paper_structures(tds, tiny):
+    """GPU bins / X-Y-Z / FSG arrays equal oracle/index_ref on the same data."""
+    from oracle import index_ref as ir
+    w, _ = tiny
+    m, v, grid = 7, 2, (4, 3, 5)
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=m, v=v, grid=grid)
+    Ds, perm = ir.temporal_sort(w.D)
+    assert np.array_equal(idx.export("perm"), perm)
+    b = ir.temporal_bins(Ds, m)
+    off = idx.export("bin_off").astype(np.int64)
+    for j in range(m):
+        if b["B_first"][j] >= 0:
+            assert off[j] == b["B_first"][j] and off[j + 1] - 1 == b["B_last"][j]
+            assert max(b["B_start"][j] + b["b"], idx.export("bin_hi")[j]) == pytest.approx(b["B_end"][j])
+        else:
+            assert off[j] == off[j + 1]
+    ext = idx.export("extents")
+    lo, hi = ext[2:5], ext[5:8]
+    wst = ext[11:14]
+    arrays, ranges = ir.st_arrays(Ds, b["bin_of"], m, v, lo, wst)
+    for c, name in enumerate(("st_x", "st_y", "st_z")):
+        assert np.array_equal(idx.export(name), arrays[c])
+        o = idx.export(["st_off_x", "st_off_y", "st_off_z"][c])
+        for (i, j), rg in ranges[c].items():
+            a0, a1 = o[j * m + i], o[j * m + i + 1]
+            assert (rg is None and a0 == a1) or (rg is not None and (a0, a1 - 1) == rg)
+    wf = (hi - lo) / np.array(grid, np.float32)
+    G, A = ir.fsg_build(Ds, grid, lo, wf)
+    cell_off = idx.export("fsg_cell_off")
+    A_gpu = idx.export("fsg_A")
+    assert np.array_equal(A_gpu, A)
+    for h, a0, a1 in G:
+        assert cell_off[h] == a0 and cell_off[h + 1] == a1 + 1
+
+
+@pytest.fixture(scope="module")
+def r1m():
+    w = synth.random_1m()
+    rng = np.random.default_rng(11)
+    sel = np.sort(rng.choice(w.Q.shape[0], 600, replace=False))
+    return w, sel
+
+
+@pytest.mark.parametrize("d", [5.0, 50.0])
+def test_random_1m_subsample(tds, r1m, d):
+    """Random-1M-shaped at full size, the bench's launch configuration; oracle on
+    a query subsample, all three variants cross-checked on the full query set."""
+    w, sel = r1m
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    full = {}
+    for kind in KINDS:
+        got, st = _run(idx, w.Q, d, kind)
+        full[kind] = (keys(got[0], got[1]), got)
+    ref = oracle.search(w.D, w.Q, d, qsel=sel)
+    m = np.isin(full["temporal"][1][0], sel)
+    for kind in KINDS:
+        g = full[kind][1]
+        mk = np.isin(g[0], sel)
+        check(tuple(x[mk] for x in g), ref, w.D, w.Q, d, label=f"r1m {kind} d={d}")
+    # full-set cross-variant equality (all variants are filters of the same set)
+    base = np.sort(full["temporal"][0])
+    for kind in ("spatiotemporal", "spatial"):
+        assert np.array_equal(np.sort(full[kind][0]), base), kind
+    assert m.sum() > 0
+
+
+@pytest.mark.parametrize("name,kinds", [("random-dense-1m", ("spatiotemporal", "temporal")),
+                                        ("merger-small", KINDS)])
+def test_dense_and_merger_subsample(tds, name, kinds):
+    if name == "merger-small":
+        w = synth.merger(n_per_disk=8192)
+        d = 1.0
+    else:
+        w = synth.make_workload(name)
+        d = 0.01
+    rng = np.random.default_rng(5)
+    sel = np.sort(rng.choice(w.Q.shape[0], 300, replace=False))
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins if name != "random-dense-1m" else 2,
+                    grid=w.grid)
+    ref = oracle.search(w.D, w.Q, d, qsel=sel)
+    sets = []
+    for kind in kinds:
+        got, _ = _run(idx, w.Q, d, kind)
+        mk = np.isin(got[0], sel)
+        check(tuple(x[mk] for x in got), ref, w.D, w.Q, d, label=f"{name} {kind}")
+        sets.append(np.sort(keys(got[0], got[1])))
+    for s2 in sets[1:]:
+        assert np.array_equal(s2, sets[0])
