@@ -1,0 +1,405 @@
+"""Benchmark of the B200 distance threshold search (driver contract in DESIGN.md "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config random-1m] [--d 50]
+    python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
+
+One step = one pass of the whole hot path over the workload, device-resident
+inputs: tds_build_index (validate, t_start radix sort, bins, subbin arrays,
+FSG) + for each index variant (GPUTemporal, GPUSpatioTemporal, GPUSpatial)
+tds_search + tds_fetch_results into device buffers.  ``value`` counts query
+segments answered per second over all ranks (3 x |Q| per step per rank: each
+query is answered once per variant).  Multi-GPU: one process per GPU, every
+rank holds D and answers its own query trajectories (weak scaling; results
+stay sharded, no data-path collective); timing is max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "query segments/s & segment-pair tests/s vs HBM roofline at 1/2/4/8 B200"
+VARIANTS = ("temporal", "spatiotemporal", "spatial")
+# algorithmic work of one pair test: the certified fp32 filter of DESIGN.md
+# ("Pair test numerics"): 43 FP32 instructions, 16 of them FFMA -> 59 flops
+FLOPS_PER_PAIR = 59
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(peaks, n_sms=148):
+    # 128 FP32 lanes per SM, FFMA = 2 flops, at the maximum SM clock
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    return n_sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled in the background."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark(self, which):
+        if which == 0:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        inside = [r for t, r in self.rows if self.t0 - 0.06 <= t <= self.t1 + 0.06] or \
+                 [r for t, r in self.rows if t >= self.t0 - 0.5][:3]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in inside:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except Exception:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def make_workload(args, rank):
+    import synth
+    kw = {}
+    if args.config in ("random-1m", "random-dense", "random-dense-1m", "merger"):
+        kw["offset"] = rank
+    w = synth.make_workload(args.config, **kw)
+    if args.d is not None:
+        w.d = args.d
+    if args.m is not None:
+        w.m_bins = args.m
+    if args.v is not None:
+        w.v_subbins = args.v
+    if args.grid is not None:
+        w.grid = (args.grid,) * 3
+    return w
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle (all-pairs, fp64)
+# ---------------------------------------------------------------------------
+def oracle_rate(w, seconds, seed=0, max_q=None):
+    """Time the oracle as it stands on a bounded query sample of the workload."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    nq = w.Q.shape[0]
+    cal = np.sort(rng.choice(nq, min(8, nq), replace=False))
+    t = time.perf_counter()
+    oracle.search(w.D, w.Q, w.d, qsel=cal)
+    dt = max(time.perf_counter() - t, 1e-6)
+    n = int(min(nq, max(8, seconds * len(cal) / dt)))
+    if max_q:
+        n = min(n, max_q)
+    sel = np.sort(rng.choice(nq, n, replace=False))
+    t = time.perf_counter()
+    r = oracle.search(w.D, w.Q, w.d, qsel=sel)
+    dt = time.perf_counter() - t
+    return n, dt, int(r["hit"].sum()), oracle.max_threads()
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    w = make_workload(args, 0)
+    # each step: a bounded query sample (~step_seconds of CPU work)
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    import oracle
+    oracle.build()
+    n, dt, hits, cores = oracle_rate(w, per_step)
+    rng = np.random.default_rng(1)
+    times = []
+    for k in range(args.warmup + args.steps):
+        sel = np.sort(rng.choice(w.Q.shape[0], n, replace=False))
+        t = time.perf_counter()
+        oracle.search(w.D, w.Q, w.d, qsel=sel)
+        el = time.perf_counter() - t
+        if k >= args.warmup:
+            times.append(el)
+    tot = sum(times)
+    value = n * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "query segments/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args, w, ws),
+        "cpu_baseline": {"value": value, "unit": "query segments/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{n} random queries of {w.Q.shape[0]} per step, all-pairs fp64 against "
+                                   f"all {w.D.shape[0]} entries"},
+        "e2e": {"value": value, "unit": "query segments/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pair_tests_per_s": n * w.D.shape[0] * len(times) / tot,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, w, ws):
+    return {"workload": f"{w.name}-shaped", "n_entries": int(w.D.shape[0]), "n_queries_per_rank": int(w.Q.shape[0]),
+            "d": w.d, "m_bins": w.m_bins, "v_subbins": w.v_subbins, "grid": list(w.grid),
+            "variants": list(args.variants), "parallelism": f"query-sharded x{ws}, index replicated",
+            "l2": "flushed between steps (256 MiB write); timed steps bracketed by barrier + synchronize",
+            "note": w.note}
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+def run_tds(args, ws, rank, local):
+    import torch
+    import paper_1410_2698_b200 as tds
+    tds.load_library()
+    dev = torch.device("cuda", local)
+    w = make_workload(args, rank)
+    Dh = torch.from_numpy(w.D).pin_memory()
+    Qh = torch.from_numpy(w.Q).pin_memory()
+    D = Dh.to(dev)
+    Q = Qh.to(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def step(collect=None, host=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 + 2 * len(args.variants))]
+        ev[0].record(stream)
+        idx = tds.Index(Dh if host else D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+        ev[1].record(stream)
+        per = {}
+        d2h = 0
+        for j, kind in enumerate(args.variants):
+            r = idx.search(Qh if host else Q, w.d, kind=kind, capacity=args.capacity)
+            ev[2 + 2 * j].record(stream)
+            out = r.fetch(device=not host)
+            ev[3 + 2 * j].record(stream)
+            st = r.stats()
+            per[kind] = st
+            d2h += 16 * r.count
+            r.close()
+        idx.close()
+        if collect is not None:
+            collect.append((ev, per, d2h))
+        return per
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # timed region: K steps, L2 flushed before each (outside the events)
+    launches0 = tds.kernel_launches()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    recs = []
+    step_ms = []
+    sampler.mark(0)
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(recs)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        step_ms.append(e0.elapsed_time(e1))
+    sampler.mark(1)
+    clocks = sampler.stop()
+    launches = tds.kernel_launches() - launches0
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    nq = w.Q.shape[0]
+    nvar = len(args.variants)
+    value = ws * nvar * nq * args.steps / (total_ms / 1e3)
+    # per-phase breakdown (medians over the timed steps)
+    build_ms = statistics.median(ev[0].elapsed_time(ev[1]) for ev, _, _ in recs)
+    per_kind = {}
+    for j, kind in enumerate(args.variants):
+        pt = [p[kind]["pair_tests"] for _, p, _ in recs]
+        pm = [p[kind]["ms_pairs"] for _, p, _ in recs]
+        per_kind[kind] = {
+            "search_ms": statistics.median(ev[1 if j == 0 else 1 + 2 * j].elapsed_time(ev[2 + 2 * j])
+                                           for ev, _, _ in recs),
+            "fetch_ms": statistics.median(ev[2 + 2 * j].elapsed_time(ev[3 + 2 * j]) for ev, _, _ in recs),
+            "pair_kernel_ms": statistics.median(pm),
+            "pair_tests": int(pt[0]),
+            "pairs_executed": int(recs[0][1][kind]["pairs_executed"]),
+            "refined_pairs": int(recs[0][1][kind]["refined_pairs"]),
+            "results": int(recs[0][1][kind]["n_results"]),
+            "passes": int(recs[0][1][kind]["passes"]),
+            "fallback_queries": int(recs[0][1][kind]["fallback_queries"]),
+            "pair_tests_per_s": pt[0] / (statistics.median(pm) / 1e3) if statistics.median(pm) > 0 else None,
+        }
+    pair_tests_step = sum(v["pair_tests"] for v in per_kind.values())
+    peaks = load_peaks()
+    # roofline of the dominant kernel: the pair kernel with the largest share
+    dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
+    dk = per_kind[dom]
+    achieved = FLOPS_PER_PAIR * dk["pair_tests"] / (dk["pair_kernel_ms"] / 1e3) / 1e12
+    peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
+    roof = {"bound": "alu", "kernel": f"k_pair_{'spatial' if dom == 'spatial' else 'range'} ({dom})",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None,
+            "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
+                           "algorithmic 59 flops per scheduled pair test",
+            "share_of_step": dk["pair_kernel_ms"] / statistics.median(step_ms)}
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(max(1, args.warmup // 2)):
+            step(host=True)
+        torch.cuda.synchronize(dev)
+        er = []
+        e2e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            step(er, host=True)
+            torch.cuda.synchronize(dev)
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            barrier()
+        tot = sum(e2e_ms)
+        if dist is not None:
+            t = torch.tensor([tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        e2e = {"value": ws * nvar * nq * args.steps / (tot / 1e3), "unit": "query segments/s",
+               "h2d_bytes_per_step": int(w.D.nbytes + nvar * w.Q.nbytes),
+               "d2h_bytes_per_step": int(statistics.median(x[2] for x in er)),
+               "timing": "host wall clock around each step, synchronize on both sides, max over ranks"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        n, dt, hits, cores = oracle_rate(w, args.cpu_seconds)
+        cpu = {"value": n / dt, "unit": "query segments/s", "cores": cores, "kind": "oracle",
+               "sample": f"{n} random queries of {nq}, all-pairs fp64 vs all {w.D.shape[0]} entries, "
+                         f"one answer per query ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "query segments/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": config_dict(args, w, ws),
+            "pair_tests_per_s": ws * pair_tests_step * args.steps / (total_ms / 1e3),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+            "breakdown": {"build_index_ms": build_ms, "variants": per_kind,
+                          "step_ms_median": statistics.median(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="tds", choices=["tds", "reference"])
+    ap.add_argument("--config", default="random-1m")
+    ap.add_argument("--d", type=float, default=None)
+    ap.add_argument("--m", type=int, default=None)
+    ap.add_argument("--v", type=int, default=None)
+    ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--variants", default="all")
+    ap.add_argument("--capacity", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    args.variants = VARIANTS if args.variants == "all" else tuple(args.variants.split(","))
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    run_tds(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

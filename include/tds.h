@@ -179,6 +179,10 @@ int tds_index_export(tds_index idx, int what, void *dst, uint64_t cap_bytes, uin
 int tds_index_info(tds_index idx, uint64_t *n, int32_t *m, int32_t *v, int32_t *grid3,
                    uint32_t *kinds);
 
+/* tds_kernel_launches — number of CUDA kernels this process has launched through
+ * the library so far (a monotone counter; benchmarks difference it). */
+uint64_t tds_kernel_launches(void);
+
 /* tds_version — library build string. */
 const char *tds_version(void);
 

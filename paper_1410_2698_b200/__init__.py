@@ -34,7 +34,7 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 # every symbol include/tds.h declares
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
-               "tds_version"]
+               "tds_version", "tds_kernel_launches"]
 
 
 class TdsError(RuntimeError):
@@ -81,6 +81,7 @@ def load_library(path: str = LIB_PATH):
     lib.tds_index_free.restype = None
     lib.tds_last_error.restype = ctypes.c_char_p
     lib.tds_version.restype = ctypes.c_char_p
+    lib.tds_kernel_launches.restype = ctypes.c_uint64
     lib.tds_index_export.argtypes = [vp, i32, vp, u64, ctypes.POINTER(u64)]
     lib.tds_index_info.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
@@ -231,6 +232,11 @@ class Result:
             self.close()
         except Exception:
             pass
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library in this process (monotone counter)."""
+    return int(load_library().tds_kernel_launches())
 
 
 def version() -> str:

@@ -3,12 +3,16 @@
 #include <cstdarg>
 #include <cstdio>
 #include <new>
+#include <atomic>
 
 #include "tds_internal.cuh"
 
 namespace tds {
 
 static thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(int code, const char *fmt, ...) {
     char buf[1024];
@@ -118,6 +122,8 @@ extern "C" {
 const char *tds_last_error(void) { return tds::last_error(); }
 
 const char *tds_version(void) { return "tds-b200 0.1 (sm_100a)"; }
+
+uint64_t tds_kernel_launches(void) { return tds::g_launches.load(); }
 
 int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *params, void *stream,
                     tds_index *out) {

@@ -39,7 +39,12 @@ const char *last_error();
         }                                                                           \
     } while (0)
 
-#define TDS_CHECK_LAUNCH() TDS_CUDA(cudaGetLastError())
+void count_launch();
+#define TDS_CHECK_LAUNCH()                 \
+    do {                                   \
+        ::tds::count_launch();             \
+        TDS_CUDA(cudaGetLastError());      \
+    } while (0)
 
 [[noreturn]] void fail(int code, const char *fmt, ...);
 
