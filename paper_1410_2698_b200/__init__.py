@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtds.so")
+LIB_PATH = os.environ.get("TDS_LIB", os.path.join(_HERE, "libtds.so"))
 
 TEMPORAL, SPATIAL, SPATIOTEMPORAL, ALL = 1, 2, 4, 7
 KINDS = {"temporal": TEMPORAL, "spatial": SPATIAL, "spatiotemporal": SPATIOTEMPORAL}

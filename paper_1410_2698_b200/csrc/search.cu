@@ -23,8 +23,14 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PT = 256;                  // threads per block of the pair kernels
-constexpr int RANGE_BPS = 3;             // resident blocks per SM (range kernel)
-constexpr int SPATIAL_BPS = 3;
+#ifndef TDS_RANGE_BPS
+#define TDS_RANGE_BPS 2
+#endif
+#ifndef TDS_SPATIAL_BPS
+#define TDS_SPATIAL_BPS 3
+#endif
+constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
+constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int UNROLL = 4;                // candidates per inner step (range kernel)
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
@@ -117,9 +123,48 @@ __device__ __forceinline__ bool filter32(const QConst &q, float4 ea, float4 eb, 
     return (a < b) & (h <= thr * thr);
 }
 
+// candidate-side terms of the filter, computed once per loaded candidate and
+// reused for every query of the group
+struct ECand {
+    float px, py, pz, t0;
+    float vx, vy, vz, t1;
+    float ext;
+};
+
+__device__ __forceinline__ ECand make_ecand(float4 a, float4 b) {
+    ECand e;
+    float dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
+    float r = rcp_approx(b.w - a.w);
+    e.px = a.x; e.py = a.y; e.pz = a.z; e.t0 = a.w;
+    e.vx = dx * r; e.vy = dy * r; e.vz = dz * r; e.t1 = b.w;
+    e.ext = fabsf(dx) + fabsf(dy) + fabsf(dz);
+    return e;
+}
+
+// the per-pair part of filter32 (same arithmetic, same certified margin);
+// q0 = (p0, t0), q1 = (v, ext) of the query, [t0c, t1c] its window-clipped span
+__device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
+    float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    float aq = a - q0.w, ae = a - e.t0;
+    float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
+    float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
+    float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
+    float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
+    float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
+    float L = b - a;
+    float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);
+    float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    float thr = fmaf(KU, M, d);
+    return (a < b) & (h <= thr * thr);
+}
+
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
 // the sublevel interval of the convex quadratic ||Pq(t)-Pe(t)||^2 <= d^2 on [a,b].
-__device__ __noinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 eb, double d, double T0, double T1,
+__device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 eb, double d, double T0, double T1,
                                     float &t_in, float &t_out) {
     double t0q = qa.w, t1q = qb.w, t0e = ea.w, t1e = eb.w;
     double a = fmax(fmax(t0q, t0e), T0);
@@ -173,17 +218,28 @@ struct OutArgs {
     DevStats *st;
 };
 
-struct Appender {                    // per-warp (uniform) chunk state
-    unsigned long long base;
-    uint32_t used, size;
-    bool full;
-    __device__ void init() { base = 0; used = 0; size = 0; full = false; }
+// Per-warp shared state (warp-uniform; lane 0 writes, every lane reads):
+// the result chunk being filled and the queue of pairs awaiting fp64 evaluation.
+struct WarpState {
+    unsigned long long ap_base;
+    uint32_t ap_used, ap_size, ap_full;
+    uint32_t refined, hits;
+    uint32_t rq[64], rj[64];         // refine queue: query row, sorted entry position
 };
 
-// warp-wide: every lane calls with its own hit flag / record; EXACT places the
-// record at the query's planned offset instead.
+__device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
+    if (lane == 0) {
+        W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0;
+    }
+    __syncwarp();
+}
+
+// warp-wide: every lane calls with its own hit flag / record.  Pass 1 appends
+// into chunks of CS slots reserved with one atomic per chunk (warp-aggregated,
+// no per-record global atomics); EXACT (re-plan passes) writes the record at
+// its query's planned offset.
 template <bool EXACT>
-__device__ __forceinline__ void append(const OutArgs &o, Appender &ap, bool hit, const Rec &r, int lane) {
+__device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit, const Rec &r, int lane) {
     const unsigned hm = __ballot_sync(FULL, hit);
     if (!hm) return;
     if (EXACT) {
@@ -196,38 +252,100 @@ __device__ __forceinline__ void append(const OutArgs &o, Appender &ap, bool hit,
         return;
     }
     const uint32_t k = __popc(hm);
-    if (!ap.full && ap.used + k > ap.size) {
-        if (ap.size && lane == 0) o.chunk_used[ap.base / o.CS] = ap.used;
+    unsigned long long base = W.ap_base;
+    uint32_t used = W.ap_used, size = W.ap_size, full = W.ap_full;
+    if (!full && used + k > size) {
+        if (size && lane == 0) o.chunk_used[base / o.CS] = used;
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(&o.st->reserved, (unsigned long long)o.CS);
         nb = __shfl_sync(FULL, nb, 0);
         if (nb >= o.cap) {
-            ap.full = true;
-            ap.size = 0;
-            ap.used = 0;
+            full = 1; size = 0; used = 0;
         } else {
-            ap.base = nb;
-            ap.used = 0;
+            base = nb;
+            used = 0;
             unsigned long long room = o.cap - nb;
-            ap.size = room < o.CS ? (uint32_t)room : o.CS;
+            size = room < o.CS ? (uint32_t)room : o.CS;
         }
     }
     const uint32_t rk = __popc(hm & ((1u << lane) - 1u));
     if (hit) {
-        if (!ap.full && ap.used + rk < ap.size) {
-            reinterpret_cast<uint4 *>(o.buf)[ap.base + ap.used + rk] =
+        if (!full && used + rk < size) {
+            reinterpret_cast<uint4 *>(o.buf)[base + used + rk] =
                 make_uint4(r.qid, r.eid, __float_as_uint(r.t_in), __float_as_uint(r.t_out));
         } else {
             o.redo[r.qid] = 1;
             atomicAdd(&o.st->dropped, 1ull);
         }
     }
-    if (!ap.full) ap.used = min(ap.used + k, ap.size);
+    if (!full) used = min(used + k, size);
+    __syncwarp();
+    if (lane == 0) { W.ap_base = base; W.ap_used = used; W.ap_size = size; W.ap_full = full; }
+    __syncwarp();
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void close_chunk(const OutArgs &o, Appender &ap, int lane) {
-    if (!EXACT && !ap.full && ap.size && lane == 0) o.chunk_used[ap.base / o.CS] = ap.used;
+__device__ __forceinline__ void warp_state_finish(const OutArgs &o, WarpState &W, int lane) {
+    __syncwarp();
+    if (lane == 0) {
+        if (!EXACT && !W.ap_full && W.ap_size) o.chunk_used[W.ap_base / o.CS] = W.ap_used;
+        if (W.refined) atomicAdd(&o.st->refined, (unsigned long long)W.refined);
+        if (W.hits) atomicAdd(&o.st->hits, (unsigned long long)W.hits);
+    }
+}
+
+struct PairCtx {                     // what the fp64 path needs
+    const float4 *Q;                 // queries (original rows)
+    const float4 *rec;               // sorted entries
+    const uint32_t *perm;            // sorted position -> entry row
+    float d, T0, T1;
+    OutArgs o;
+};
+
+// Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
+template <bool EXACT>
+__device__ __noinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n) {
+    const int lane = threadIdx.x & 31;
+    const bool v = (uint32_t)lane < n;
+    const uint32_t q = v ? W->rq[lane] : 0u, j = v ? W->rj[lane] : 0u;
+    float tin = 0.f, tout = 0.f;
+    bool hit = false;
+    if (v)
+        hit = pair64(__ldg(C->Q + 2 * (uint64_t)q), __ldg(C->Q + 2 * (uint64_t)q + 1), __ldg(C->rec + 2 * (uint64_t)j),
+                     __ldg(C->rec + 2 * (uint64_t)j + 1), (double)C->d, (double)C->T0, (double)C->T1, tin, tout);
+    const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
+    Rec r{q, eid, tin, tout};
+    append<EXACT>(C->o, *W, hit, r, lane);
+    const unsigned hm = __ballot_sync(FULL, hit);
+    if (hit) {   // per-query counts, aggregated over the lanes of the same query
+        const unsigned peers = __match_any_sync(hm, q);
+        if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&C->o.qcount[q], (uint32_t)__popc(peers));
+    }
+    __syncwarp();
+    if (lane == 0) { W->refined += n; W->hits += __popc(hm); }
+    __syncwarp();
+}
+
+// warp-wide: queue the pairs whose fp32 filter passed; flush 32 at a time
+template <bool EXACT>
+__device__ __forceinline__ void push_refine(const PairCtx *C, WarpState &W, uint32_t &qn, bool maybe, uint32_t qid,
+                                            uint32_t j, int lane) {
+    const unsigned mb = __ballot_sync(FULL, maybe);
+    if (!mb) return;
+    const uint32_t pos = qn + __popc(mb & ((1u << lane) - 1u));
+    if (maybe) { W.rq[pos] = qid; W.rj[pos] = j; }
+    qn += __popc(mb);
+    __syncwarp();
+    if (qn >= 32) {
+        flush_refine<EXACT>(C, &W, 32);
+        const uint32_t rest = qn - 32;
+        uint32_t t1 = 0, t2 = 0;
+        if ((uint32_t)lane < rest) { t1 = W.rq[32 + lane]; t2 = W.rj[32 + lane]; }
+        __syncwarp();
+        if ((uint32_t)lane < rest) { W.rq[lane] = t1; W.rj[lane] = t2; }
+        __syncwarp();
+        qn = rest;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -430,28 +548,39 @@ __global__ void k_set_total_items(const uint32_t *item_start, uint32_t ntiles, D
 // A8: pair kernel for GPUTemporal / GPUSpatioTemporal (Alg. 2 / Alg. 3)
 // ---------------------------------------------------------------------------
 struct RangeArgs {
-    const float4 *Q;                 // queries (original rows)
-    const float4 *rec;               // sorted entries
-    const uint32_t *perm;
+    PairCtx pc;                      // Q, rec, perm, d, window, output
     const uint32_t *arr[3];          // X, Y, Z
     const Sched *sched;
     const Tile *tiles;
     const uint32_t *item_start;      // [ntiles+1]
     uint32_t ntiles;
-    float d, T0, T1;
-    OutArgs o;
 };
 
+struct __align__(16) RangeWarpSmem {
+    float4 q[32][3];                 // group query constants: (p0,t0) (v,ext) (t0c,t1c,lo,hi)
+    WarpState ws;
+};
+
+// Mapping: a work item is a group of <= 32
+// consecutive schedule entries (one category) and a chunk of the union of their
+// candidate ranges.  Lane g owns query g of the group (its constants are staged
+// in shared memory); the warp then walks the chunk 32 candidates at a time with
+// lane = candidate.  A ballot over the owners gives the queries whose range
+// meets the current 32 candidates, so each loaded candidate is tested against
+// every query that needs it and gaps between ranges are skipped.  Pairs that
+// pass the fp32 filter are queued and evaluated 32 at a time in fp64.
 template <bool EXACT>
-__global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(RangeArgs A) {
+__global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_constant__ RangeArgs A) {
+    __shared__ RangeWarpSmem sm[PT / 32];
     const int lane = threadIdx.x & 31;
-    DevStats *st = A.o.st;
+    RangeWarpSmem &W = sm[threadIdx.x >> 5];
+    DevStats *st = A.pc.o.st;
     const uint32_t total = st->total_items;
     const uint32_t CH = st->ch;
-    const double d64 = (double)A.d, T064 = (double)A.T0, T164 = (double)A.T1;
-    Appender ap;
-    ap.init();
-    unsigned long long exec = 0, refined = 0, hits = 0;
+    const float d = A.pc.d;
+    warp_state_init(W.ws, lane);
+    uint32_t qn = 0;
+    unsigned long long exec = 0;
     while (true) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
@@ -466,73 +595,69 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(RangeArgs A) {
         const uint32_t chunk = item - A.item_start[lo];
         const uint32_t c_lo = T.ulo + chunk * CH;
         const uint32_t c_hi = min(c_lo + CH, T.uhi);
+        // ---- owner side: lane g stages query g of the group
         const uint32_t p = T.tb + lane;
         const bool active = p < T.te;
         Sched S{0, 0, 0, 3};
         if (active) S = A.sched[p];
-        uint32_t llo = max(S.lo, c_lo), lhi = min(S.hi, c_hi);
-        if (!active || llo >= lhi) { llo = 0xffffffffu; lhi = 0; }
-        float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
-        if (active) { qa = A.Q[2 * (uint64_t)S.qid]; qb = A.Q[2 * (uint64_t)S.qid + 1]; }
-        const QConst q = make_qconst(qa, qb, A.T0, A.T1);
-        uint32_t wlo = llo, whi = lhi;
+        uint32_t my_lo = max(S.lo, c_lo), my_hi = min(S.hi, c_hi);
+        if (!active || my_lo >= my_hi) { my_lo = 0xffffffffu; my_hi = 0; }
+        {
+            float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
+            if (active) { qa = __ldg(A.pc.Q + 2 * (uint64_t)S.qid); qb = __ldg(A.pc.Q + 2 * (uint64_t)S.qid + 1); }
+            const QConst qc = make_qconst(qa, qb, A.pc.T0, A.pc.T1);
+            __syncwarp();
+            W.q[lane][0] = make_float4(qc.px, qc.py, qc.pz, qc.t0);
+            W.q[lane][1] = make_float4(qc.vx, qc.vy, qc.vz, qc.ext);
+            W.q[lane][2] = make_float4(qc.t0c, qc.t1c, __uint_as_float(my_lo), __uint_as_float(my_hi));
+            __syncwarp();
+        }
+        uint32_t wlo = my_lo, whi = my_hi;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             wlo = min(wlo, __shfl_xor_sync(FULL, wlo, o));
             whi = max(whi, __shfl_xor_sync(FULL, whi, o));
         }
-        if (wlo >= whi) continue;
-        exec += (unsigned long long)(whi - wlo) * __popc(__ballot_sync(FULL, active));
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
-        uint32_t myhits = 0;
-        for (uint32_t i = wlo; i < whi; i += UNROLL) {
-            uint32_t jj[UNROLL];
-            float4 ea[UNROLL], eb[UNROLL];
-            bool mb[UNROLL];
-            bool any = false;
+        uint32_t base = wlo;
+        while (base < whi) {
+            const uint32_t cend = min(base + 32, whi);
+            unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
+            if (!mask) {                       // skip the gap to the next range start
+                uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                uint32_t ii = i + u;
-                bool v = ii < whi;
-                uint32_t j = v ? (arr ? __ldg(arr + ii) : ii) : 0u;
-                jj[u] = j;
-                ea[u] = __ldg(A.rec + 2 * (uint64_t)j);
-                eb[u] = __ldg(A.rec + 2 * (uint64_t)j + 1);
-                mb[u] = v && ii >= llo && ii < lhi && filter32(q, ea[u], eb[u], A.d);
-                any |= mb[u];
+                for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
+                base = nxt;
+                continue;
             }
-            if (__any_sync(FULL, any)) {
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    if (!__any_sync(FULL, mb[u])) continue;
-                    float tin = 0.f, tout = 0.f;
-                    bool hit = false;
-                    if (mb[u]) {
-                        ++refined;
-                        hit = pair64(qa, qb, ea[u], eb[u], d64, T064, T164, tin, tout);
-                    }
-                    uint32_t eid = 0;
-                    if (__any_sync(FULL, hit)) eid = __ldg(A.perm + jj[u]);
-                    myhits += hit;
-                    Rec r{S.qid, eid, tin, tout};
-                    append<EXACT>(A.o, ap, hit, r, lane);
-                }
+            // ---- worker side: lane = candidate
+            const uint32_t cand = base + lane;
+            const bool v = cand < cend;
+            uint32_t j = 0;
+            float4 ea = make_float4(0.f, 0.f, 0.f, 0.f), eb = make_float4(0.f, 0.f, 0.f, 1.f);
+            if (v) {
+                j = arr ? __ldg(arr + cand) : cand;
+                ea = __ldg(A.pc.rec + 2 * (uint64_t)j);
+                eb = __ldg(A.pc.rec + 2 * (uint64_t)j + 1);
             }
+            const ECand e = make_ecand(ea, eb);
+            exec += 32ull * __popc(mask);
+            while (mask) {
+                const int g = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
+                const bool inr = v && cand >= __float_as_uint(q2.z) && cand < __float_as_uint(q2.w);
+                const bool maybe = inr && filter_pair(q0, q1, q2.x, q2.y, e, d);
+                if (!__any_sync(FULL, maybe)) continue;
+                const uint32_t qid = __shfl_sync(FULL, S.qid, g);
+                push_refine<EXACT>(&A.pc, W.ws, qn, maybe, qid, j, lane);
+            }
+            base = cend;
         }
-        if (myhits) atomicAdd(&A.o.qcount[S.qid], myhits);
-        hits += myhits;
     }
-    close_chunk<EXACT>(A.o, ap, lane);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        refined += __shfl_xor_sync(FULL, refined, o);
-        hits += __shfl_xor_sync(FULL, hits, o);
-    }
-    if (lane == 0) {
-        if (exec) atomicAdd(&st->executed, exec);
-        if (refined) atomicAdd(&st->refined, refined);
-        if (hits) atomicAdd(&st->hits, hits);
-    }
+    if (qn) flush_refine<EXACT>(&A.pc, &W.ws, qn);
+    warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
+    if (lane == 0 && exec) atomicAdd(&st->executed, exec);
 }
 
 // ---------------------------------------------------------------------------
@@ -589,9 +714,7 @@ __global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, c
 }
 
 struct SpatialArgs {
-    const float4 *Q;
-    const float4 *rec;
-    const uint32_t *perm;
+    PairCtx pc;
     const uint32_t *A;               // lookup array
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
@@ -599,8 +722,6 @@ struct SpatialArgs {
     const unsigned long long *slot_start;   // [nrows + 1]
     uint32_t nrows;
     FsgGrid G;
-    float d, T0, T1;
-    OutArgs o;
 };
 
 __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint32_t lo, uint32_t hi,
@@ -613,19 +734,21 @@ __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint3
     return lo;
 }
 
+// lane = candidate slot of the flattened (query, cell row) work list; warps grab
+// 32 x SP_PER_LANE consecutive slots at a time (dynamic load balance).
 template <bool EXACT>
-__global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(SpatialArgs A) {
+__global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_constant__ SpatialArgs A) {
+    __shared__ WarpState sm[PT / 32];
     const int lane = threadIdx.x & 31;
-    DevStats *st = A.o.st;
+    WarpState &W = sm[threadIdx.x >> 5];
+    DevStats *st = A.pc.o.st;
     const unsigned long long total = A.slot_start[A.nrows];
-    const double d64 = (double)A.d, T064 = (double)A.T0, T164 = (double)A.T1;
-    Appender ap;
-    ap.init();
-    unsigned long long refined = 0, hits = 0, exec = 0;
+    warp_state_init(W, lane);
+    uint32_t qn = 0;
+    unsigned long long exec = 0;
     uint32_t cur_p = 0xffffffffu;
     uint32_t cur_qrow = 0;
-    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
-    QConst q = make_qconst(qa, qb, A.T0, A.T1);
+    QConst q = make_qconst(make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 1.f), A.pc.T0, A.pc.T1);
     int4 qlo = make_int4(0, 0, 0, 0);
     constexpr unsigned long long GRAB = 32ull * SP_PER_LANE;
     while (true) {
@@ -634,7 +757,6 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(SpatialArgs A)
         B = __shfl_sync(FULL, B, 0);
         if (B >= total) break;
         const unsigned long long Bend = min(B + GRAB, total);
-        // rows of the first and last slot of the grab (lanes 0 / 1), then per-lane search
         uint32_t rr = 0;
         if (lane < 2) rr = find_row(A.slot_start, 0, A.nrows, lane == 0 ? B : Bend - 1);
         const uint32_t rlo = __shfl_sync(FULL, rr, 0), rhi = __shfl_sync(FULL, rr, 1) + 1;
@@ -642,25 +764,22 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(SpatialArgs A)
         exec += Bend - B;
         for (int u = 0; u < SP_PER_LANE; ++u) {
             const unsigned long long s = B + (unsigned long long)u * 32 + lane;
-            const bool v = s < Bend;
-            bool mb = false;
-            uint32_t e = 0, i = 0;
-            float4 ea = make_float4(0.f, 0.f, 0.f, 0.f), eb = make_float4(0.f, 0.f, 0.f, 1.f);
-            if (v) {
+            bool maybe = false;
+            uint32_t e = 0;
+            if (s < Bend) {
                 const uint32_t r = find_row(A.slot_start, rprev, rhi, s);
                 rprev = r;
                 const uint32_t pl = A.row_q[r];
-                i = A.row_alo[r] + (uint32_t)(s - A.slot_start[r]);
+                const uint32_t i = A.row_alo[r] + (uint32_t)(s - A.slot_start[r]);
                 e = __ldg(A.A + i);
-                ea = __ldg(A.rec + 2 * (uint64_t)e);
-                eb = __ldg(A.rec + 2 * (uint64_t)e + 1);
+                const float4 ea = __ldg(A.pc.rec + 2 * (uint64_t)e);
+                const float4 eb = __ldg(A.pc.rec + 2 * (uint64_t)e + 1);
                 if (pl != cur_p) {
                     cur_p = pl;
                     qlo = A.qbox[2 * pl];
                     cur_qrow = (uint32_t)qlo.w;
-                    qa = A.Q[2 * (uint64_t)cur_qrow];
-                    qb = A.Q[2 * (uint64_t)cur_qrow + 1];
-                    q = make_qconst(qa, qb, A.T0, A.T1);
+                    q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow), __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1),
+                                    A.pc.T0, A.pc.T1);
                 }
                 // duplicate avoidance: test (q, e) only in the first cell (index-space min
                 // corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
@@ -674,38 +793,14 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(SpatialArgs A)
                     const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
                     first = __ldg(A.cell_off + h) <= i && i < __ldg(A.cell_off + h + 1);
                 }
-                mb = first && filter32(q, ea, eb, A.d);
+                maybe = first && filter32(q, ea, eb, A.pc.d);
             }
-            if (!__any_sync(FULL, mb)) continue;
-            float tin = 0.f, tout = 0.f;
-            bool hit = false;
-            if (mb) {
-                ++refined;
-                hit = pair64(qa, qb, ea, eb, d64, T064, T164, tin, tout);
-            }
-            uint32_t eid = hit ? __ldg(A.perm + e) : 0u;
-            Rec rec{cur_qrow, eid, tin, tout};
-            append<EXACT>(A.o, ap, hit, rec, lane);
-            const unsigned hm = __ballot_sync(FULL, hit);
-            if (hit) {
-                // per-query counts, aggregated over lanes of the same query
-                unsigned peers = __match_any_sync(hm, cur_qrow);
-                if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&A.o.qcount[cur_qrow], __popc(peers));
-                ++hits;
-            }
+            push_refine<EXACT>(&A.pc, W, qn, maybe, cur_qrow, e, lane);
         }
     }
-    close_chunk<EXACT>(A.o, ap, lane);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        refined += __shfl_xor_sync(FULL, refined, o);
-        hits += __shfl_xor_sync(FULL, hits, o);
-    }
-    if (lane == 0) {
-        if (refined) atomicAdd(&st->refined, refined);
-        if (hits) atomicAdd(&st->hits, hits);
-        if (exec) atomicAdd(&st->executed, exec);
-    }
+    if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
+    warp_state_finish<EXACT>(A.pc.o, W, lane);
+    if (lane == 0 && exec) atomicAdd(&st->executed, exec);
 }
 
 // ---------------------------------------------------------------------------
@@ -1029,17 +1124,17 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     tm.mark(2);
     if (!spatial) {
         RangeArgs a{};
-        a.Q = Q; a.rec = idx->rec; a.perm = idx->perm;
+        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
         for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
-        a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
         k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
     } else if (nrows > 0) {
         SpatialArgs a{};
-        a.Q = Q; a.rec = idx->rec; a.perm = idx->perm; a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
+        a.A = idx->fsg_A; a.cell_off = idx->cell_off;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
-        a.slot_start = slot_start.p; a.nrows = nrows; a.G = G; a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
+        a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
         k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
     }
@@ -1194,12 +1289,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             DBuf<uint32_t> bis;
             uint32_t bnt = plan_items(rsched.p + b0, 0, b1 - b0, bst.p, bt, bis, s);
             RangeArgs a{};
-            a.Q = Q; a.rec = idx->rec; a.perm = idx->perm;
+            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
+            a.pc.o.st = bst.p;
             for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
             a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
-            a.d = d; a.T0 = T0; a.T1 = T1;
-            a.o = o;
-            a.o.st = bst.p;
             k_pair_range<true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
             TDS_CHECK_LAUNCH();
             TDS_CUDA(cudaStreamSynchronize(s));
@@ -1228,9 +1321,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             TDS_CHECK_LAUNCH();
             exclusive_scan_u64(rl64.p, (uint64_t *)ss.p, bnrows + 1, nullptr, s);
             SpatialArgs a{};
-            a.Q = Q; a.rec = idx->rec; a.perm = idx->perm; a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
+            a.A = idx->fsg_A; a.cell_off = idx->cell_off;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
-            a.nrows = bnrows; a.G = G; a.d = d; a.T0 = T0; a.T1 = T1; a.o = o;
+            a.nrows = bnrows; a.G = G;
             if (bnrows) {
                 k_pair_spatial<true><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
                 TDS_CHECK_LAUNCH();
