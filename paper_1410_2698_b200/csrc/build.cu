@@ -54,7 +54,7 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
             mx[c] = fmaxf(mx[c], fabsf(__fsub_rn(p1[c], p0[c])));
         }
     }
-    // warp reduce then one atomic per warp
+    // warp reduce, then block reduce through shared memory, then one set of atomics per block
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
@@ -66,15 +66,19 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
             mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
         }
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomic_min_key(&red[0], tmin);
-        atomic_max_key(&red[1], tmax);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            atomic_min_key(&red[2 + c], lo[c]);
-            atomic_max_key(&red[5 + c], hi[c]);
-            atomic_max_key(&red[8 + c], mx[c]);
-        }
+    __shared__ float sred[NT / 32][11];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sred[w][0] = tmin; sred[w][1] = tmax;
+        for (int c = 0; c < 3; ++c) { sred[w][2 + c] = lo[c]; sred[w][5 + c] = hi[c]; sred[w][8 + c] = mx[c]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 11) {
+        const int k = threadIdx.x;
+        const bool is_min = (k == 0) || (k >= 2 && k <= 4);
+        float v = sred[0][k];
+        for (int ww = 1; ww < NT / 32; ++ww) v = is_min ? fminf(v, sred[ww][k]) : fmaxf(v, sred[ww][k]);
+        if (is_min) atomic_min_key(&red[k], v); else atomic_max_key(&red[k], v);
     }
 }
 

@@ -375,7 +375,9 @@ struct SchedArgs {
     float st_o[3], st_w[3];
     int use_st;
     Sched *out;
-    uint32_t *keys;                  // sort keys (category-major, then lo) or null
+    uint32_t *keys;                  // sort keys: category << lo_bits | lo
+    uint32_t *vals;                  // identity (sort payload)
+    int lo_bits;
     DevStats *st;
 };
 
@@ -402,7 +404,7 @@ __global__ void k_schedule(SchedArgs A) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long work = 0, fb = 0;
     if (p < A.nq) {
-        uint32_t k = A.order[p];
+        uint32_t k = A.order ? A.order[p] : p;
         float4 a = A.Q[2 * (uint64_t)k], b = A.Q[2 * (uint64_t)k + 1];
         float t0c = fmaxf(a.w, A.T0), t1c = fminf(b.w, A.T1);
         Sched S{k, 0u, 0u, 3};
@@ -443,7 +445,8 @@ __global__ void k_schedule(SchedArgs A) {
             }
         }
         A.out[p] = S;
-        if (A.keys) A.keys[p] = S.lo;
+        A.keys[p] = ((uint32_t)(S.sel + 1) << A.lo_bits) | S.lo;
+        A.vals[p] = p;
         atomicAdd(&A.st->cat_cnt[S.sel + 1], 1u);
     }
 #pragma unroll
@@ -619,9 +622,11 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             whi = max(whi, __shfl_xor_sync(FULL, whi, o));
         }
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
+        // windows of 64 candidates: lane handles cand and cand + 32 (two independent
+        // filter chains per query load)
         uint32_t base = wlo;
         while (base < whi) {
-            const uint32_t cend = min(base + 32, whi);
+            const uint32_t cend = min(base + 64, whi);
             unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
             if (!mask) {                       // skip the gap to the next range start
                 uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
@@ -631,26 +636,34 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 continue;
             }
             // ---- worker side: lane = candidate
-            const uint32_t cand = base + lane;
-            const bool v = cand < cend;
-            uint32_t j = 0;
-            float4 ea = make_float4(0.f, 0.f, 0.f, 0.f), eb = make_float4(0.f, 0.f, 0.f, 1.f);
-            if (v) {
-                j = arr ? __ldg(arr + cand) : cand;
-                ea = __ldg(A.pc.rec + 2 * (uint64_t)j);
-                eb = __ldg(A.pc.rec + 2 * (uint64_t)j + 1);
+            const uint32_t c0 = base + lane, c1 = c0 + 32;
+            const bool v0 = c0 < cend, v1 = c1 < cend;
+            uint32_t j0 = 0, j1 = 0;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), b0 = make_float4(0.f, 0.f, 0.f, 1.f);
+            float4 a1 = a0, b1 = b0;
+            if (v0) {
+                j0 = arr ? __ldg(arr + c0) : c0;
+                a0 = __ldg(A.pc.rec + 2 * (uint64_t)j0);
+                b0 = __ldg(A.pc.rec + 2 * (uint64_t)j0 + 1);
             }
-            const ECand e = make_ecand(ea, eb);
-            exec += 32ull * __popc(mask);
+            if (v1) {
+                j1 = arr ? __ldg(arr + c1) : c1;
+                a1 = __ldg(A.pc.rec + 2 * (uint64_t)j1);
+                b1 = __ldg(A.pc.rec + 2 * (uint64_t)j1 + 1);
+            }
+            const ECand e0 = make_ecand(a0, b0), e1 = make_ecand(a1, b1);
+            exec += (unsigned long long)(cend - base) * __popc(mask);
             while (mask) {
                 const int g = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                const bool inr = v && cand >= __float_as_uint(q2.z) && cand < __float_as_uint(q2.w);
-                const bool maybe = inr && filter_pair(q0, q1, q2.x, q2.y, e, d);
-                if (!__any_sync(FULL, maybe)) continue;
+                const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
+                const bool m0 = v0 && c0 >= glo && c0 < ghi && filter_pair(q0, q1, q2.x, q2.y, e0, d);
+                const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
+                if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                push_refine<EXACT>(&A.pc, W.ws, qn, maybe, qid, j, lane);
+                push_refine<EXACT>(&A.pc, W.ws, qn, m0, qid, j0, lane);
+                push_refine<EXACT>(&A.pc, W.ws, qn, m1, qid, j1, lane);
             }
             base = cend;
         }
@@ -1002,12 +1015,13 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     TDS_CUDA(cudaMemsetAsync(bad.p, 0xff, 8, s));
     const uint32_t n = (uint32_t)nq;
 
-    // ---- A6: sort queries by t_start; FSG keeps input order
+    // ---- A6: validate queries; GPUTemporal / GPUSpatioTemporal order them by
+    // (selector, range start) below, which subsumes the t_start sort of P:681-682
+    // (range starts are monotone in t_start); FSG keeps input order
     DBuf<uint32_t> keys(n, s), order(n, s);
     k_query_keys<<<nblk(n), 256, 0, s>>>(Q, nq, keys.p, order.p, bad.p);
     TDS_CHECK_LAUNCH();
     const bool spatial = (kind == TDS_SPATIAL);
-    if (!spatial) radix_sort_pairs(keys.p, order.p, n, 0, 32, s);
 
     DBuf<uint32_t> qcount(n, s);
     DBuf<uint8_t> redo(n, s);
@@ -1028,7 +1042,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     if (!spatial) {
         sched = DBuf<Sched>(n, s);
         SchedArgs a{};
-        a.Q = Q; a.order = order.p; a.nq = n; a.d = d; a.T0 = T0; a.T1 = T1;
+        a.Q = Q; a.order = nullptr; a.nq = n; a.d = d; a.T0 = T0; a.T1 = T1;
         a.m = idx->m; a.v = idx->v;
         a.bin_off = idx->bin_off; a.bin_lo = idx->bin_lo; a.bin_pmhi = idx->bin_pmhi;
         a.use_st = kind == TDS_SPATIOTEMPORAL;
@@ -1038,27 +1052,25 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         }
         a.out = sched.p;
         a.keys = keys.p;
+        a.vals = order.p;
+        uint64_t lo_max = idx->n;
+        if (a.use_st)
+            for (int c = 0; c < 3; ++c) lo_max = std::max<uint64_t>(lo_max, idx->st_len[c]);
+        int lo_bits = 1;
+        while ((1ull << lo_bits) <= lo_max) ++lo_bits;
+        if (lo_bits > 29) fail(TDS_EINVAL, "index too large for the 32-bit schedule key (%llu)",
+                               (unsigned long long)lo_max);
+        a.lo_bits = lo_bits;
         a.st = dst.p;
         k_schedule<<<nblk(n), 256, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
-        // sort S by (array selector, range start): stable by lo, then by category
-        DBuf<uint32_t> perm2(n, s);
+        // sort S by (array selector, range start): one stable radix sort
+        radix_sort_pairs(keys.p, order.p, n, 0, lo_bits + 3, s);
         {
-            std::vector<uint32_t> iota(n);
-            std::iota(iota.begin(), iota.end(), 0u);
-            TDS_CUDA(cudaMemcpyAsync(perm2.p, iota.data(), 4ull * n, cudaMemcpyHostToDevice, s));
-            radix_sort_pairs(keys.p, perm2.p, n, 0, 32, s);
-            DBuf<uint32_t> ck(n, s);
             DBuf<Sched> tmp(n, s);
-            k_permute_sched<<<nblk(n), 256, 0, s>>>(sched.p, perm2.p, n, tmp.p);
+            k_permute_sched<<<nblk(n), 256, 0, s>>>(sched.p, order.p, n, tmp.p);
             TDS_CHECK_LAUNCH();
-            k_cat_keys<<<nblk(n), 256, 0, s>>>(tmp.p, n, ck.p);
-            TDS_CHECK_LAUNCH();
-            TDS_CUDA(cudaMemcpyAsync(perm2.p, iota.data(), 4ull * n, cudaMemcpyHostToDevice, s));
-            radix_sort_pairs(ck.p, perm2.p, n, 0, 3, s);
-            k_permute_sched<<<nblk(n), 256, 0, s>>>(tmp.p, perm2.p, n, sched.p);
-            TDS_CHECK_LAUNCH();
-            TDS_CUDA(cudaStreamSynchronize(s));   // iota host buffer lifetime
+            std::swap(sched.p, tmp.p);
         }
         ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s);
     } else {

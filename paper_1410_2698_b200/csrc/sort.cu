@@ -3,6 +3,8 @@
 // pairs.  Used by the index build (t_start sort P:569-571, subbin / cell
 // grouping P:347-361) and by query preparation (sort Q by t_start,
 // P:681-682; sort S by the array selector).
+#include <algorithm>
+
 #include "tds_internal.cuh"
 
 namespace tds {
@@ -111,22 +113,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const T *__restrict
     }
 }
 
-template <class T>
-void exclusive_scan_impl(const T *in, T *out, uint64_t n, T *d_total, cudaStream_t s) {
-    if (n == 0) {
-        if (d_total) TDS_CUDA(cudaMemsetAsync(d_total, 0, sizeof(T), s));
-        return;
-    }
-    uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    DBuf<T> partial(nb, s);
-    k_scan_reduce<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, partial.p);
-    TDS_CHECK_LAUNCH();
-    k_scan_partials<T><<<1, SCAN_THREADS, 0, s>>>(partial.p, nb, d_total);
-    TDS_CHECK_LAUNCH();
-    k_scan_apply<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, partial.p);
-    TDS_CHECK_LAUNCH();
-}
-
 // ---------------------------------------------------------------------------
 // radix sort
 // ---------------------------------------------------------------------------
@@ -205,6 +191,233 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t *__res
     }
 }
 
+// ---------------------------------------------------------------------------
+// single-pass chained scan (decoupled look-back): one launch per scan
+// status word per tile: flag (2 high bits: 1 = aggregate, 2 = inclusive prefix)
+// | 62-bit value
+// ---------------------------------------------------------------------------
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// warp 0 of the block: exclusive prefix of tile t from its predecessors
+__device__ __forceinline__ unsigned long long lookback(unsigned long long *status, long long t) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long prefix = 0;
+    long long k = t - 1;
+    while (k >= 0) {
+        long long idx = k - lane;
+        unsigned long long s = ST_INC;            // beyond tile 0: inclusive 0
+        if (idx >= 0) {
+            do { s = ld_volatile(status + idx); } while ((s >> 62) == 0);
+        }
+        unsigned inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        unsigned long long v = s & ST_VAL;
+        int stop = inc ? __ffs(inc) - 1 : 31;
+        unsigned long long part = (lane <= stop) ? v : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += part;
+        if (inc) break;
+        k -= 32;
+    }
+    return prefix;
+}
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chained(const T *__restrict__ in, T *out, uint64_t n,
+                                                               unsigned long long *status, unsigned *tile_ctr,
+                                                               T *d_total, uint64_t ntiles) {
+    __shared__ T buf[SCAN_TILE];
+    __shared__ T tot;
+    __shared__ unsigned long long s_prefix;
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint64_t t = s_tile;
+    const uint64_t base = t * SCAN_TILE;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int j = i * SCAN_THREADS + threadIdx.x;
+        uint64_t k = base + j;
+        buf[j] = (k < n) ? in[k] : T(0);
+    }
+    __syncthreads();
+    T v[SCAN_ITEMS];
+    T sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        v[i] = buf[threadIdx.x * SCAN_ITEMS + i];
+        sum += v[i];
+    }
+    T e = block_excl_scan<T, SCAN_THREADS>(sum, &tot);
+    if (threadIdx.x < 32) {
+        if (t == 0) {
+            if (threadIdx.x == 0) {
+                atomicExch(status, ST_INC | (unsigned long long)tot);
+                s_prefix = 0;
+            }
+        } else {
+            if (threadIdx.x == 0) atomicExch(status + t, ST_AGG | (unsigned long long)tot);
+            unsigned long long pre = lookback(status, (long long)t);
+            if (threadIdx.x == 0) {
+                atomicExch(status + t, ST_INC | (pre + (unsigned long long)tot));
+                s_prefix = pre;
+            }
+        }
+    }
+    __syncthreads();
+    e += (T)s_prefix;
+    if (t == ntiles - 1 && threadIdx.x == 0 && d_total) *d_total = (T)s_prefix + tot;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        buf[threadIdx.x * SCAN_ITEMS + i] = e;
+        e += v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int j = i * SCAN_THREADS + threadIdx.x;
+        uint64_t k = base + j;
+        if (k < n) out[k] = buf[j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// onesweep radix sort: one histogram pass for all digits, then one
+// decoupled-look-back scatter per digit (status per (tile, digit): 2-bit flag |
+// 30-bit count)
+// ---------------------------------------------------------------------------
+constexpr uint32_t RS_AGG = 1u << 30, RS_INC = 2u << 30, RS_VAL = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const uint32_t *__restrict__ keys, uint64_t n,
+                                                           int begin_bit, int npass, int end_bit,
+                                                           uint32_t *__restrict__ ghist) {
+    __shared__ uint32_t h[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (uint64_t k = (uint64_t)blockIdx.x * RS_THREADS + threadIdx.x; k < n; k += (uint64_t)gridDim.x * RS_THREADS) {
+        uint32_t key = keys[k];
+        for (int p = 0; p < npass; ++p) {
+            int shift = begin_bit + 8 * p;
+            int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+            atomicAdd(&h[p][(key >> shift) & ((1u << nb) - 1u)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; ++p) {
+        uint32_t c = h[p][threadIdx.x];
+        if (c) atomicAdd(&ghist[p * 256 + threadIdx.x], c);
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint32_t *__restrict__ kin,
+                                                            const uint32_t *__restrict__ vin,
+                                                            uint32_t *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                            uint64_t n, int shift, uint32_t mask,
+                                                            const uint32_t *__restrict__ ghist,
+                                                            uint32_t *status, unsigned *tile_ctr) {
+    __shared__ uint32_t cnt[RS_WARPS][256];
+    __shared__ uint32_t dstart[256];
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t tot_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t key[RS_ROUNDS], val[RS_ROUNDS], rank[RS_ROUNDS];
+    int dig[RS_ROUNDS];
+    const uint64_t tbase = (uint64_t)tile * RS_TILE + (uint64_t)w * (32 * RS_ROUNDS);
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        uint64_t k = tbase + (uint64_t)r * 32 + lane;
+        bool valid = k < n;
+        key[r] = valid ? kin[k] : 0u;
+        val[r] = valid ? vin[k] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        uint64_t k = tbase + (uint64_t)r * 32 + lane;
+        int d = (k < n) ? (int)((key[r] >> shift) & mask) : 256;
+        dig[r] = d;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t lt = __popc(peers & lt_mask);
+        uint32_t c = (d < 256) ? cnt[w][d] : 0u;
+        rank[r] = c + lt;
+        __syncwarp();
+        if (d < 256 && lt == 0) cnt[w][d] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // thread = digit: tile count, exclusive over warps, publish, look back
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+        uint32_t t = cnt[ww][d];
+        cnt[ww][d] = run;
+        run += t;
+    }
+    uint32_t *st = status + (uint64_t)tile * 256 + d;
+    uint32_t excl = 0;
+    if (tile == 0) {
+        atomicExch(st, RS_INC | run);
+    } else {
+        atomicExch(st, RS_AGG | run);
+        int64_t k = (int64_t)tile - 1;
+        while (k >= 0) {
+            uint32_t sv;
+            do { sv = ld_volatile32(status + (uint64_t)k * 256 + d); } while ((sv >> 30) == 0);
+            excl += sv & RS_VAL;
+            if ((sv >> 30) == 2) break;
+            --k;
+        }
+        atomicExch(st, RS_INC | (excl + run));
+    }
+    // global digit start: exclusive scan of ghist over digits
+    uint32_t g = ghist[d];
+    uint32_t gex = block_excl_scan<uint32_t, RS_THREADS>(g, &tot_s);
+    dstart[d] = gex + excl;
+    __syncthreads();
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) cnt[ww][d] += dstart[d];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        if (dig[r] < 256) {
+            uint32_t pos = cnt[w][dig[r]] + rank[r];
+            kout[pos] = key[r];
+            vout[pos] = val[r];
+        }
+    }
+}
+
+template <class T>
+void exclusive_scan_impl(const T *in, T *out, uint64_t n, T *d_total, cudaStream_t s) {
+    if (n == 0) {
+        if (d_total) TDS_CUDA(cudaMemsetAsync(d_total, 0, sizeof(T), s));
+        return;
+    }
+    uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DBuf<unsigned long long> status(nb + 1, s);          // last word: tile counter
+    TDS_CUDA(cudaMemsetAsync(status.p, 0, 8 * (nb + 1), s));
+    k_scan_chained<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, status.p, (unsigned *)(status.p + nb),
+                                                            d_total, nb);
+    TDS_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *d_total, cudaStream_t s) {
@@ -218,23 +431,44 @@ void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t 
 void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit, cudaStream_t s) {
     if (n <= 1 || end_bit <= begin_bit) return;
     if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
-    uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
-    DBuf<uint32_t> k2(n, s), v2(n, s), hist((uint64_t)256 * ntiles, s);
+    const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    const int npass = (end_bit - begin_bit + 7) / 8;
+    DBuf<uint32_t> k2(n, s), v2(n, s);
     uint32_t *ka = keys, *va = vals, *kb = k2.p, *vb = v2.p;
-    int passes = 0;
-    for (int shift = begin_bit; shift < end_bit; shift += 8, ++passes) {
-        int nb = end_bit - shift < 8 ? end_bit - shift : 8;
-        uint32_t mask = (1u << nb) - 1u;
-        k_rs_hist<<<ntiles, RS_THREADS, 0, s>>>(ka, n, shift, mask, hist.p, ntiles);
+    if (n < (1ull << 30)) {
+        // onesweep: 1 upsweep + 1 scatter per digit
+        const uint64_t status_words = (uint64_t)npass * ntiles * 256;
+        DBuf<uint32_t> aux(npass * 256 + npass + status_words, s);
+        uint32_t *ghist = aux.p, *ctr = aux.p + npass * 256, *status = ctr + npass;
+        TDS_CUDA(cudaMemsetAsync(aux.p, 0, 4 * (npass * 256 + npass + status_words), s));
+        unsigned ublk = std::min<unsigned>(ntiles, (unsigned)num_sms() * 4);
+        k_rs_upsweep<<<ublk, RS_THREADS, 0, s>>>(keys, n, begin_bit, npass, end_bit, ghist);
         TDS_CHECK_LAUNCH();
-        exclusive_scan_u32(hist.p, hist.p, (uint64_t)256 * ntiles, nullptr, s);
-        k_rs_scatter<<<ntiles, RS_THREADS, 0, s>>>(ka, va, kb, vb, n, shift, mask, hist.p, ntiles);
-        TDS_CHECK_LAUNCH();
-        uint32_t *t;
-        t = ka; ka = kb; kb = t;
-        t = va; va = vb; vb = t;
+        for (int p = 0; p < npass; ++p) {
+            int shift = begin_bit + 8 * p;
+            int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+            k_rs_onesweep<<<ntiles, RS_THREADS, 0, s>>>(ka, va, kb, vb, n, shift, (1u << nb) - 1u, ghist + 256 * p,
+                                                         status + (uint64_t)p * ntiles * 256, ctr + p);
+            TDS_CHECK_LAUNCH();
+            std::swap(ka, kb);
+            std::swap(va, vb);
+        }
+    } else {
+        DBuf<uint32_t> hist((uint64_t)256 * ntiles, s);
+        for (int p = 0; p < npass; ++p) {
+            int shift = begin_bit + 8 * p;
+            int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+            uint32_t mask = (1u << nb) - 1u;
+            k_rs_hist<<<ntiles, RS_THREADS, 0, s>>>(ka, n, shift, mask, hist.p, ntiles);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u32(hist.p, hist.p, (uint64_t)256 * ntiles, nullptr, s);
+            k_rs_scatter<<<ntiles, RS_THREADS, 0, s>>>(ka, va, kb, vb, n, shift, mask, hist.p, ntiles);
+            TDS_CHECK_LAUNCH();
+            std::swap(ka, kb);
+            std::swap(va, vb);
+        }
     }
-    if (passes & 1) {
+    if (npass & 1) {
         TDS_CUDA(cudaMemcpyAsync(keys, ka, n * 4, cudaMemcpyDeviceToDevice, s));
         TDS_CUDA(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, s));
     }
