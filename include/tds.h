@@ -140,7 +140,10 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, flo
  * NULL to skip that column.  dst_is_device: 1 = outputs are device memory,
  * 0 = host memory.  sorted: 1 = records ordered by (query_id, entry_id)
  * (the order is otherwise unspecified: atomic appends).
- * Errors: TDS_EINVAL (range outside the result), TDS_ECUDA.  Synchronises stream.
+ * Device destinations: the copy is enqueued on `stream` and the call returns
+ * without synchronising (stream order makes the outputs valid for later work
+ * on that stream).  Host destinations: synchronises stream.
+ * Errors: TDS_EINVAL (range outside the result), TDS_ECUDA.
  */
 int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *query_id,
                       uint32_t *entry_id, float *t_in, float *t_out, int dst_is_device,

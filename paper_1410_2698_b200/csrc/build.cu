@@ -240,6 +240,14 @@ __global__ void k_cell_count(const float4 *__restrict__ rec, uint64_t n, Grid3 G
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
+__global__ void k_cell_min(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint32_t *__restrict__ ecell) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo[3], hi[3];
+    cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
+    ecell[i] = pack_cell(lo[0], lo[1], lo[2]);
+}
+
 __global__ void k_cell_emit(const float4 *__restrict__ rec, uint64_t n, Grid3 G, const uint32_t *__restrict__ pos,
                             uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -353,33 +361,12 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     k_prefix_max<<<1, 1024, 0, s>>>(bin_hi.p, bin_pmhi.p, m);
     TDS_CHECK_LAUNCH();
 
-    // ---- A5: spatiotemporal subbin arrays ------------------------------------
-    if (want_st) {
-        const int v = idx->v;
-        for (int c = 0; c < 3; ++c) {
-            float ext = E.hi[c] - E.lo[c];
-            E.w_st[c] = ext > 0.f ? ext / (float)v : 1.0f;
-            DBuf<uint32_t> cnt(n, s), pos(n, s), total(1, s);
-            k_slab_count<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, cnt.p);
-            TDS_CHECK_LAUNCH();
-            exclusive_scan_u32(cnt.p, pos.p, n, total.p, s);
-            uint32_t len = 0;
-            TDS_CUDA(cudaMemcpyAsync(&len, total.p, 4, cudaMemcpyDeviceToHost, s));
-            TDS_CUDA(cudaStreamSynchronize(s));
-            DBuf<uint32_t> k2(len, s), v2(len, s), off((uint64_t)v * m + 1, s);
-            k_slab_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, pos.p, k2.p, v2.p);
-            TDS_CHECK_LAUNCH();
-            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, s);
-            idx->st_arr[c] = v2.release();
-            idx->st_len[c] = len;
-            idx->st_off[c] = off.release();
-        }
-    }
-
-    // ---- A4: FSG (dense CSR over all cells) ----------------------------------
+    // ---- A5 + A4, phase 1: membership counts and their prefix sums for the three
+    // subbin arrays and the FSG, read back with ONE synchronisation
+    const int v = idx->v;
+    Grid3 G{};
+    uint64_t ncell = 1;
     if (want_fsg) {
-        Grid3 G;
-        uint64_t ncell = 1;
         for (int c = 0; c < 3; ++c) {
             if (idx->grid[c] < 1) fail(TDS_EINVAL, "grid[%d] = %d < 1", c, idx->grid[c]);
             float ext = E.hi[c] - E.lo[c];
@@ -390,21 +377,66 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
             ncell *= (uint64_t)idx->grid[c];
         }
         if (ncell >= (1ull << 31)) fail(TDS_EINVAL, "grid has %llu cells (limit 2^31)", (unsigned long long)ncell);
-        DBuf<uint32_t> cnt(n, s), pos(n, s);
-        DBuf<unsigned long long> total(1, s);
-        TDS_CUDA(cudaMemsetAsync(total.p, 0, 8, s));
-        k_cell_count<<<nblk(n), NT, 0, s>>>(rec.p, n, G, cnt.p, total.p);
+        if (idx->grid[0] > FSG_MAX_X || idx->grid[1] > FSG_MAX_Y || idx->grid[2] > FSG_MAX_Z)
+            fail(TDS_EINVAL, "grid %d x %d x %d exceeds %d x %d x %d", idx->grid[0], idx->grid[1], idx->grid[2],
+                 FSG_MAX_X, FSG_MAX_Y, FSG_MAX_Z);
+    }
+    DBuf<uint32_t> st_pos[3];
+    DBuf<uint32_t> fsg_pos;
+    DBuf<unsigned long long> totals(4, s);       // ST x, y, z lengths; FSG length
+    TDS_CUDA(cudaMemsetAsync(totals.p, 0, 32, s));
+    if (want_st) {
+        for (int c = 0; c < 3; ++c) {
+            float ext = E.hi[c] - E.lo[c];
+            E.w_st[c] = ext > 0.f ? ext / (float)v : 1.0f;
+            DBuf<uint32_t> cnt(n, s);
+            st_pos[c] = DBuf<uint32_t>(n, s);
+            k_slab_count<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, cnt.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u32(cnt.p, st_pos[c].p, n, (uint32_t *)(totals.p + c), s);
+        }
+    }
+    if (want_fsg) {
+        DBuf<uint32_t> cnt(n, s);
+        fsg_pos = DBuf<uint32_t>(n, s);
+        k_cell_count<<<nblk(n), NT, 0, s>>>(rec.p, n, G, cnt.p, totals.p + 3);
         TDS_CHECK_LAUNCH();
-        unsigned long long len = 0;
-        TDS_CUDA(cudaMemcpyAsync(&len, total.p, 8, cudaMemcpyDeviceToHost, s));
+        exclusive_scan_u32(cnt.p, fsg_pos.p, n, nullptr, s);
+    }
+    unsigned long long tot[4] = {0, 0, 0, 0};
+    if (want_st || want_fsg) {
+        TDS_CUDA(cudaMemcpyAsync(tot, totals.p, 32, cudaMemcpyDeviceToHost, s));
         TDS_CUDA(cudaStreamSynchronize(s));
+    }
+
+    // ---- A5, phase 2: spatiotemporal subbin arrays ------------------
+    if (want_st) {
+        for (int c = 0; c < 3; ++c) {
+            const uint64_t len = tot[c] & 0xffffffffull;
+            DBuf<uint32_t> k2(len, s), v2(len, s), off((uint64_t)v * m + 1, s);
+            k_slab_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, st_pos[c].p, k2.p,
+                                              v2.p);
+            TDS_CHECK_LAUNCH();
+            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, s);
+            idx->st_arr[c] = v2.release();
+            idx->st_len[c] = len;
+            idx->st_off[c] = off.release();
+        }
+    }
+
+    // ---- A4, phase 2: FSG (dense CSR over all cells) -----------------
+    if (want_fsg) {
+        const unsigned long long len = tot[3];
         if (len >= (1ull << 32) - 1)
             fail(TDS_EINVAL, "FSG lookup array would hold %llu ids (limit 2^32); use a coarser grid", len);
-        exclusive_scan_u32(cnt.p, pos.p, n, nullptr, s);
         DBuf<uint32_t> k2(len, s), v2(len, s), off(ncell + 1, s);
-        k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, pos.p, k2.p, v2.p);
+        k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
         TDS_CHECK_LAUNCH();
         group_by_key(k2.p, v2.p, len, ncell, off.p, s);
+        DBuf<uint32_t> ecell(n, s);
+        k_cell_min<<<nblk(n), NT, 0, s>>>(rec.p, n, G, ecell.p);
+        TDS_CHECK_LAUNCH();
+        idx->fsg_ecell = ecell.release();
         idx->fsg_A = v2.release();
         idx->A_len = len;
         idx->cell_off = off.release();
@@ -425,7 +457,7 @@ void free_index(tds_index_s *idx) {
     auto f = [&](void *p) { if (p) dfree(p, s); };
     f(idx->rec); f(idx->perm); f(idx->bin_off); f(idx->bin_lo); f(idx->bin_hi); f(idx->bin_pmhi);
     for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); }
-    f(idx->cell_off); f(idx->fsg_A);
+    f(idx->cell_off); f(idx->fsg_A); f(idx->fsg_ecell);
     cudaStreamSynchronize(s);
 }
 

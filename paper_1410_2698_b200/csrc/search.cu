@@ -729,6 +729,7 @@ __global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, c
 struct SpatialArgs {
     PairCtx pc;
     const uint32_t *A;               // lookup array
+    const uint32_t *ecell;           // packed min cell of each sorted entry
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
     const uint32_t *row_q, *row_alo, *row_cxy;
@@ -770,38 +771,53 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
         B = __shfl_sync(FULL, B, 0);
         if (B >= total) break;
         const unsigned long long Bend = min(B + GRAB, total);
-        uint32_t rr = 0;
-        if (lane < 2) rr = find_row(A.slot_start, 0, A.nrows, lane == 0 ? B : Bend - 1);
-        const uint32_t rlo = __shfl_sync(FULL, rr, 0), rhi = __shfl_sync(FULL, rr, 1) + 1;
-        uint32_t rprev = rlo;
+        // row of this lane's first slot; later slots advance the row linearly
+        // (rows are consecutive in slot order)
+        uint32_t r = 0;
+        unsigned long long r_start = 0, r_next = 0;
+        uint32_t r_alo = 0, r_cxy = 0, r_p = 0;
+        {
+            const unsigned long long s0 = min(B + lane, Bend - 1);
+            r = find_row(A.slot_start, 0, A.nrows, s0);
+            r_start = A.slot_start[r];
+            r_next = A.slot_start[r + 1];
+            r_alo = A.row_alo[r];
+            r_cxy = A.row_cxy[r];
+            r_p = A.row_q[r];
+        }
         exec += Bend - B;
         for (int u = 0; u < SP_PER_LANE; ++u) {
             const unsigned long long s = B + (unsigned long long)u * 32 + lane;
             bool maybe = false;
             uint32_t e = 0;
             if (s < Bend) {
-                const uint32_t r = find_row(A.slot_start, rprev, rhi, s);
-                rprev = r;
-                const uint32_t pl = A.row_q[r];
-                const uint32_t i = A.row_alo[r] + (uint32_t)(s - A.slot_start[r]);
+                if (s >= r_next) {
+                    do {
+                        ++r;
+                        r_start = r_next;
+                        r_next = A.slot_start[r + 1];
+                    } while (s >= r_next);
+                    r_alo = A.row_alo[r];
+                    r_cxy = A.row_cxy[r];
+                    r_p = A.row_q[r];
+                }
+                const uint32_t i = r_alo + (uint32_t)(s - r_start);
                 e = __ldg(A.A + i);
                 const float4 ea = __ldg(A.pc.rec + 2 * (uint64_t)e);
                 const float4 eb = __ldg(A.pc.rec + 2 * (uint64_t)e + 1);
-                if (pl != cur_p) {
-                    cur_p = pl;
-                    qlo = A.qbox[2 * pl];
+                const uint32_t ec = __ldg(A.ecell + e);
+                if (r_p != cur_p) {
+                    cur_p = r_p;
+                    qlo = A.qbox[2 * r_p];
                     cur_qrow = (uint32_t)qlo.w;
                     q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow), __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1),
                                     A.pc.T0, A.pc.T1);
                 }
                 // duplicate avoidance: test (q, e) only in the first cell (index-space min
                 // corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
-                const int ex = cell_of(fminf(ea.x, eb.x), A.G.o[0], A.G.w[0], A.G.g[0]);
-                const int ey = cell_of(fminf(ea.y, eb.y), A.G.o[1], A.G.w[1], A.G.g[1]);
-                const int ez = cell_of(fminf(ea.z, eb.z), A.G.o[2], A.G.w[2], A.G.g[2]);
-                const uint32_t cxy = A.row_cxy[r];
-                const int rx = max(ex, qlo.x), ry = max(ey, qlo.y), rz = max(ez, qlo.z);
-                bool first = (rx == (int)(cxy >> 16)) && (ry == (int)(cxy & 0xffffu));
+                const int rx = max((int)(ec >> 21), qlo.x), ry = max((int)((ec >> 10) & 0x7ffu), qlo.y);
+                const int rz = max((int)(ec & 0x3ffu), qlo.z);
+                bool first = (rx == (int)(r_cxy >> 16)) && (ry == (int)(r_cxy & 0xffffu));
                 if (first) {
                     const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
                     first = __ldg(A.cell_off + h) <= i && i < __ldg(A.cell_off + h + 1);
@@ -1003,6 +1019,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             uint64_t capacity, cudaStream_t s, tds_result_s *res) {
     tds_stats &S = res->stats;
     memset(&S, 0, sizeof S);
+    res->stream = s;
     res->n = 0;
     res->chunked = false;
     if (nq == 0) return;
@@ -1144,7 +1161,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     } else if (nrows > 0) {
         SpatialArgs a{};
         a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-        a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+        a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
         k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
@@ -1334,7 +1351,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             exclusive_scan_u64(rl64.p, (uint64_t *)ss.p, bnrows + 1, nullptr, s);
             SpatialArgs a{};
             a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-            a.A = idx->fsg_A; a.cell_off = idx->cell_off;
+            a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;
             if (bnrows) {
@@ -1367,6 +1384,7 @@ void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint3
     if (first > r->n || count > r->n - first) fail(TDS_EINVAL, "fetch range [%llu, +%llu) outside %llu records",
                                                    (unsigned long long)first, (unsigned long long)count,
                                                    (unsigned long long)r->n);
+    r->stream = s;
     if (count == 0) return;
     // device staging for host destinations
     DBuf<uint32_t> dq, de;
@@ -1408,25 +1426,23 @@ void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint3
         radix_sort_pairs(k2.p, ord2.p, n, 0, 32, s);
         k_fetch_flat<<<nblk(count), 256, 0, s>>>(rs, ord2.p, first, count, oq, oe, oi, oo);
         TDS_CHECK_LAUNCH();
-        TDS_CUDA(cudaStreamSynchronize(s));
     }
     if (!dst_dev) {
         if (qid) TDS_CUDA(cudaMemcpyAsync(qid, oq, 4 * count, cudaMemcpyDeviceToHost, s));
         if (eid) TDS_CUDA(cudaMemcpyAsync(eid, oe, 4 * count, cudaMemcpyDeviceToHost, s));
         if (tin) TDS_CUDA(cudaMemcpyAsync(tin, oi, 4 * count, cudaMemcpyDeviceToHost, s));
         if (tout) TDS_CUDA(cudaMemcpyAsync(tout, oo, 4 * count, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
     }
-    TDS_CUDA(cudaStreamSynchronize(s));
 }
 
 void free_result(tds_result_s *r) {
-    cudaStream_t s = 0;
+    cudaStream_t s = r->stream;      // ordered after the last fetch on that stream
     if (r->buf) dfree(r->buf, s);
     if (r->chunk_used) dfree(r->chunk_used, s);
     if (r->chunk_off) dfree(r->chunk_off, s);
     if (r->store) dfree(r->store, s);
     r->buf = nullptr; r->chunk_used = nullptr; r->chunk_off = nullptr; r->store = nullptr;
-    cudaStreamSynchronize(s);
 }
 
 }  // namespace tds

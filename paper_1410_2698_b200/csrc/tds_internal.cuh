@@ -105,6 +105,7 @@ struct tds_index_s {
     // FSG as a dense CSR over all cells + lookup array A
     uint32_t *cell_off = nullptr;   // [gx*gy*gz+1]
     uint32_t *fsg_A = nullptr;      // [A_len] sorted positions
+    uint32_t *fsg_ecell = nullptr;  // [n] min cell of each sorted entry's MBB, packed x<<21 | y<<10 | z
     uint64_t A_len = 0;
     uint64_t n_cells = 0;
     int device = 0;
@@ -134,6 +135,12 @@ __device__ __forceinline__ int cell_of(float c, float o, float w, int g) {
     float f = floorf(__fdiv_rn(__fsub_rn(c, o), w));
     int k = (f < 0.f) ? 0 : (f >= (float)g ? g - 1 : (int)f);
     return k;
+}
+
+// FSG cell coordinates packed in 32 bits (grid limits 2048 x 2048 x 1024)
+constexpr int FSG_MAX_X = 2048, FSG_MAX_Y = 2048, FSG_MAX_Z = 1024;
+__host__ __device__ __forceinline__ uint32_t pack_cell(int x, int y, int z) {
+    return ((uint32_t)x << 21) | ((uint32_t)y << 10) | (uint32_t)z;
 }
 
 // ---------------------------------------------------------------------------
@@ -187,6 +194,7 @@ struct tds_result_s {
     uint64_t n = 0;
     tds_stats stats{};
     int device = 0;
+    cudaStream_t stream = 0;          // stream of the last operation (frees are ordered after it)
 };
 
 namespace tds {
