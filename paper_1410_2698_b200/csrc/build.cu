@@ -240,12 +240,12 @@ __global__ void k_cell_count(const float4 *__restrict__ rec, uint64_t n, Grid3 G
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
-__global__ void k_cell_min(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint32_t *__restrict__ ecell) {
+__global__ void k_cell_min(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint2 *__restrict__ ecell) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int lo[3], hi[3];
     cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
-    ecell[i] = pack_cell(lo[0], lo[1], lo[2]);
+    ecell[i] = make_uint2(pack_cell(lo[0], lo[1], lo[2]), pack_cell(hi[0], hi[1], hi[2]));
 }
 
 __global__ void k_cell_emit(const float4 *__restrict__ rec, uint64_t n, Grid3 G, const uint32_t *__restrict__ pos,
@@ -433,7 +433,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
         TDS_CHECK_LAUNCH();
         group_by_key(k2.p, v2.p, len, ncell, off.p, s);
-        DBuf<uint32_t> ecell(n, s);
+        DBuf<uint2> ecell(n, s);
         k_cell_min<<<nblk(n), NT, 0, s>>>(rec.p, n, G, ecell.p);
         TDS_CHECK_LAUNCH();
         idx->fsg_ecell = ecell.release();

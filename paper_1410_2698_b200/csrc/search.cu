@@ -27,12 +27,13 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #define TDS_RANGE_BPS 2
 #endif
 #ifndef TDS_SPATIAL_BPS
-#define TDS_SPATIAL_BPS 3
+#define TDS_SPATIAL_BPS 2
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int UNROLL = 4;                // candidates per inner step (range kernel)
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
+constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
 // (derived bound 20 u M, u = 2^-24; 64 u used)
 constexpr float KU = 64.0f / 16777216.0f;
@@ -220,11 +221,13 @@ struct OutArgs {
 
 // Per-warp shared state (warp-uniform; lane 0 writes, every lane reads):
 // the result chunk being filled and the queue of pairs awaiting fp64 evaluation.
+constexpr int RQ_CAP = 192;          // refine queue capacity (32 + up to 5 x 32 additions)
+
 struct WarpState {
     unsigned long long ap_base;
     uint32_t ap_used, ap_size, ap_full;
     uint32_t refined, hits;
-    uint32_t rq[64], rj[64];         // refine queue: query row, sorted entry position
+    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: query row, sorted entry position
 };
 
 __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
@@ -326,26 +329,38 @@ __device__ __noinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32
     __syncwarp();
 }
 
-// warp-wide: queue the pairs whose fp32 filter passed; flush 32 at a time
-template <bool EXACT>
-__device__ __forceinline__ void push_refine(const PairCtx *C, WarpState &W, uint32_t &qn, bool maybe, uint32_t qid,
-                                            uint32_t j, int lane) {
+// warp-wide: queue the pairs whose fp32 filter passed (no flush here)
+__device__ __forceinline__ void queue_add(WarpState &W, uint32_t &qn, bool maybe, uint32_t qid, uint32_t j, int lane) {
     const unsigned mb = __ballot_sync(FULL, maybe);
     if (!mb) return;
     const uint32_t pos = qn + __popc(mb & ((1u << lane) - 1u));
     if (maybe) { W.rq[pos] = qid; W.rj[pos] = j; }
     qn += __popc(mb);
+}
+
+// warp-wide: evaluate queued pairs in fp64, 32 at a time, while >= 32 are queued
+template <bool EXACT>
+__device__ __forceinline__ void queue_drain(const PairCtx *C, WarpState &W, uint32_t &qn, int lane) {
+    if (qn < 32) return;
     __syncwarp();
-    if (qn >= 32) {
+    uint32_t head = 0;
+    do {
+        if (head) {                      // move the next 32 to the front
+            uint32_t t1 = W.rq[head + lane], t2 = W.rj[head + lane];
+            __syncwarp();
+            W.rq[lane] = t1; W.rj[lane] = t2;
+            __syncwarp();
+        }
         flush_refine<EXACT>(C, &W, 32);
-        const uint32_t rest = qn - 32;
-        uint32_t t1 = 0, t2 = 0;
-        if ((uint32_t)lane < rest) { t1 = W.rq[32 + lane]; t2 = W.rj[32 + lane]; }
-        __syncwarp();
-        if ((uint32_t)lane < rest) { W.rq[lane] = t1; W.rj[lane] = t2; }
-        __syncwarp();
-        qn = rest;
-    }
+        head += 32;
+    } while (qn - head >= 32);
+    const uint32_t rest = qn - head;
+    uint32_t t1 = 0, t2 = 0;
+    if ((uint32_t)lane < rest) { t1 = W.rq[head + lane]; t2 = W.rj[head + lane]; }
+    __syncwarp();
+    if ((uint32_t)lane < rest) { W.rq[lane] = t1; W.rj[lane] = t2; }
+    __syncwarp();
+    qn = rest;
 }
 
 // ---------------------------------------------------------------------------
@@ -662,8 +677,9 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
                 if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                push_refine<EXACT>(&A.pc, W.ws, qn, m0, qid, j0, lane);
-                push_refine<EXACT>(&A.pc, W.ws, qn, m1, qid, j1, lane);
+                queue_add(W.ws, qn, m0, qid, j0, lane);
+                queue_add(W.ws, qn, m1, qid, j1, lane);
+                queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
             }
             base = cend;
         }
@@ -729,7 +745,8 @@ __global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, c
 struct SpatialArgs {
     PairCtx pc;
     const uint32_t *A;               // lookup array
-    const uint32_t *ecell;           // packed min cell of each sorted entry
+    const uint2 *ecell;              // packed min / max cell of each sorted entry
+    const uint32_t *grab_row;        // [ngrab + 1] row of the first slot of each grab
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
     const uint32_t *row_q, *row_alo, *row_cxy;
@@ -748,6 +765,16 @@ __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint3
     return lo;
 }
 
+__global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, uint64_t ngrab,
+                            uint32_t *__restrict__ grab_row) {
+    uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > ngrab) return;
+    const unsigned long long total = ss[nrows];
+    unsigned long long s = k * SP_GRAB;
+    if (s >= total) s = total ? total - 1 : 0;
+    grab_row[k] = find_row(ss, 0, nrows, s);
+}
+
 // lane = candidate slot of the flattened (query, cell row) work list; warps grab
 // 32 x SP_PER_LANE consecutive slots at a time (dynamic load balance).
 template <bool EXACT>
@@ -764,34 +791,31 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     uint32_t cur_qrow = 0;
     QConst q = make_qconst(make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 1.f), A.pc.T0, A.pc.T1);
     int4 qlo = make_int4(0, 0, 0, 0);
-    constexpr unsigned long long GRAB = 32ull * SP_PER_LANE;
+    int qhiz = 0;
+    constexpr int SB = 4;                       // slots per lane per batch (loads hoisted)
     while (true) {
-        unsigned long long B = 0;
-        if (lane == 0) B = atomicAdd(&st->total_slots, GRAB);
-        B = __shfl_sync(FULL, B, 0);
+        unsigned gi = 0;
+        if (lane == 0) gi = atomicAdd(&st->work_ctr, 1u);
+        gi = __shfl_sync(FULL, gi, 0);
+        const unsigned long long B = (unsigned long long)gi * SP_GRAB;
         if (B >= total) break;
-        const unsigned long long Bend = min(B + GRAB, total);
-        // row of this lane's first slot; later slots advance the row linearly
-        // (rows are consecutive in slot order)
-        uint32_t r = 0;
-        unsigned long long r_start = 0, r_next = 0;
-        uint32_t r_alo = 0, r_cxy = 0, r_p = 0;
-        {
-            const unsigned long long s0 = min(B + lane, Bend - 1);
-            r = find_row(A.slot_start, 0, A.nrows, s0);
-            r_start = A.slot_start[r];
-            r_next = A.slot_start[r + 1];
-            r_alo = A.row_alo[r];
-            r_cxy = A.row_cxy[r];
-            r_p = A.row_q[r];
-        }
+        const unsigned long long Bend = min(B + SP_GRAB, total);
+        const uint32_t rlo = A.grab_row[gi], rhi = A.grab_row[gi + 1] + 1;
+        // row of this lane's first slot (small search inside the grab's row range);
+        // later slots advance the row linearly (rows are consecutive in slot order)
+        uint32_t r = find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
+        unsigned long long r_start = A.slot_start[r], r_next = A.slot_start[r + 1];
+        uint32_t r_alo = A.row_alo[r], r_cxy = A.row_cxy[r], r_p = A.row_q[r];
         exec += Bend - B;
-        for (int u = 0; u < SP_PER_LANE; ++u) {
-            const unsigned long long s = B + (unsigned long long)u * 32 + lane;
-            bool maybe = false;
-            uint32_t e = 0;
-            if (s < Bend) {
-                if (s >= r_next) {
+#pragma unroll 1
+        for (int u0 = 0; u0 < SP_PER_LANE; u0 += SB) {
+            uint32_t ii[SB], ee[SB], cxy[SB], pp[SB];
+            bool vv[SB];
+#pragma unroll
+            for (int u = 0; u < SB; ++u) {
+                const unsigned long long s = B + (unsigned long long)(u0 + u) * 32 + lane;
+                vv[u] = s < Bend;
+                if (vv[u] && s >= r_next) {
                     do {
                         ++r;
                         r_start = r_next;
@@ -801,30 +825,47 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     r_cxy = A.row_cxy[r];
                     r_p = A.row_q[r];
                 }
-                const uint32_t i = r_alo + (uint32_t)(s - r_start);
-                e = __ldg(A.A + i);
-                const float4 ea = __ldg(A.pc.rec + 2 * (uint64_t)e);
-                const float4 eb = __ldg(A.pc.rec + 2 * (uint64_t)e + 1);
-                const uint32_t ec = __ldg(A.ecell + e);
-                if (r_p != cur_p) {
-                    cur_p = r_p;
-                    qlo = A.qbox[2 * r_p];
-                    cur_qrow = (uint32_t)qlo.w;
-                    q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow), __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1),
-                                    A.pc.T0, A.pc.T1);
-                }
-                // duplicate avoidance: test (q, e) only in the first cell (index-space min
-                // corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
-                const int rx = max((int)(ec >> 21), qlo.x), ry = max((int)((ec >> 10) & 0x7ffu), qlo.y);
-                const int rz = max((int)(ec & 0x3ffu), qlo.z);
-                bool first = (rx == (int)(r_cxy >> 16)) && (ry == (int)(r_cxy & 0xffffu));
-                if (first) {
-                    const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
-                    first = __ldg(A.cell_off + h) <= i && i < __ldg(A.cell_off + h + 1);
-                }
-                maybe = first && filter32(q, ea, eb, A.pc.d);
+                ii[u] = r_alo + (uint32_t)(s - r_start);
+                cxy[u] = r_cxy;
+                pp[u] = r_p;
+                ee[u] = vv[u] ? __ldg(A.A + ii[u]) : 0u;
             }
-            push_refine<EXACT>(&A.pc, W, qn, maybe, cur_qrow, e, lane);
+            float4 ea[SB], eb[SB];
+            uint2 ec[SB];
+#pragma unroll
+            for (int u = 0; u < SB; ++u) {
+                ea[u] = __ldg(A.pc.rec + 2 * (uint64_t)ee[u]);
+                eb[u] = __ldg(A.pc.rec + 2 * (uint64_t)ee[u] + 1);
+                ec[u] = __ldg(A.ecell + ee[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < SB; ++u) {
+                bool maybe = false;
+                if (vv[u]) {
+                    if (pp[u] != cur_p) {
+                        cur_p = pp[u];
+                        qlo = A.qbox[2 * cur_p];
+                        qhiz = A.qbox[2 * cur_p + 1].z;
+                        cur_qrow = (uint32_t)qlo.w;
+                        q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow),
+                                        __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1), A.pc.T0, A.pc.T1);
+                    }
+                    // duplicate avoidance: test (q, e) only in the first cell (index-space
+                    // min corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
+                    const uint32_t m0 = ec[u].x, m1 = ec[u].y;
+                    const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
+                    bool first = (rx == (int)(cxy[u] >> 16)) && (ry == (int)(cxy[u] & 0xffffu));
+                    const int rz = max((int)(m0 & 0x3ffu), qlo.z);
+                    if (first && rz < min((int)(m1 & 0x3ffu), qhiz)) {
+                        // e occurs in several cells of this row: keep the occurrence in cell rz
+                        const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
+                        first = __ldg(A.cell_off + h) <= ii[u] && ii[u] < __ldg(A.cell_off + h + 1);
+                    }
+                    maybe = first && filter32(q, ea[u], eb[u], A.pc.d);
+                }
+                queue_add(W, qn, maybe, cur_qrow, ee[u], lane);
+            }
+            queue_drain<EXACT>(&A.pc, W, qn, lane);
         }
     }
     if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
@@ -1158,10 +1199,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
         k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
-    } else if (nrows > 0) {
+    } else if (nrows > 0 && hs.pair_tests > 0) {
+        const uint64_t ngrab = (hs.pair_tests + SP_GRAB - 1) / SP_GRAB;
+        DBuf<uint32_t> grab_row(ngrab + 1, s);
+        k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, ngrab, grab_row.p);
+        TDS_CHECK_LAUNCH();
         SpatialArgs a{};
         a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-        a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off;
+        a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
         k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
@@ -1349,12 +1394,19 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             k_u32_to_u64<<<nblk(bnrows + 1), 256, 0, s>>>(rlen.p, bnrows + 1, rl64.p);
             TDS_CHECK_LAUNCH();
             exclusive_scan_u64(rl64.p, (uint64_t *)ss.p, bnrows + 1, nullptr, s);
+            unsigned long long bslots = 0;
+            TDS_CUDA(cudaMemcpyAsync(&bslots, ss.p + bnrows, 8, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            const uint64_t ngrab = (bslots + SP_GRAB - 1) / SP_GRAB;
+            DBuf<uint32_t> grab_row(ngrab + 1, s);
+            k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, ngrab, grab_row.p);
+            TDS_CHECK_LAUNCH();
             SpatialArgs a{};
             a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-            a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off;
+            a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;
-            if (bnrows) {
+            if (bnrows && bslots) {
                 k_pair_spatial<true><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
                 TDS_CHECK_LAUNCH();
             }
