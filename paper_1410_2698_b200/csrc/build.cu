@@ -240,11 +240,20 @@ __global__ void k_cell_count(const float4 *__restrict__ rec, uint64_t n, Grid3 G
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
-__global__ void k_cell_min(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint2 *__restrict__ ecell) {
+// cell-ordered copies for the GPUSpatial pair kernel: record, original row and
+// min / max cell of entry A[i] at position i
+__global__ void k_fsg_materialise(const float4 *__restrict__ rec, const uint32_t *__restrict__ perm,
+                                  const uint32_t *__restrict__ A, uint64_t len, Grid3 G, float4 *__restrict__ frec,
+                                  uint32_t *__restrict__ fperm, uint2 *__restrict__ ecell) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= len) return;
+    const uint32_t e = A[i];
+    const float4 a = rec[2 * (uint64_t)e], b = rec[2 * (uint64_t)e + 1];
     int lo[3], hi[3];
-    cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
+    cell_box(a, b, G, lo, hi);
+    frec[2 * i] = a;
+    frec[2 * i + 1] = b;
+    fperm[i] = perm[e];
     ecell[i] = make_uint2(pack_cell(lo[0], lo[1], lo[2]), pack_cell(hi[0], hi[1], hi[2]));
 }
 
@@ -433,10 +442,14 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
         TDS_CHECK_LAUNCH();
         group_by_key(k2.p, v2.p, len, ncell, off.p, s);
-        DBuf<uint2> ecell(n, s);
-        k_cell_min<<<nblk(n), NT, 0, s>>>(rec.p, n, G, ecell.p);
+        DBuf<uint2> ecell(len, s);
+        DBuf<float4> frec(2 * len, s);
+        DBuf<uint32_t> fperm(len, s);
+        k_fsg_materialise<<<nblk(len), NT, 0, s>>>(rec.p, perm.p, v2.p, len, G, frec.p, fperm.p, ecell.p);
         TDS_CHECK_LAUNCH();
         idx->fsg_ecell = ecell.release();
+        idx->fsg_rec = frec.release();
+        idx->fsg_perm = fperm.release();
         idx->fsg_A = v2.release();
         idx->A_len = len;
         idx->cell_off = off.release();
@@ -457,7 +470,7 @@ void free_index(tds_index_s *idx) {
     auto f = [&](void *p) { if (p) dfree(p, s); };
     f(idx->rec); f(idx->perm); f(idx->bin_off); f(idx->bin_lo); f(idx->bin_hi); f(idx->bin_pmhi);
     for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); }
-    f(idx->cell_off); f(idx->fsg_A); f(idx->fsg_ecell);
+    f(idx->cell_off); f(idx->fsg_A); f(idx->fsg_ecell); f(idx->fsg_rec); f(idx->fsg_perm);
     cudaStreamSynchronize(s);
 }
 

@@ -743,9 +743,8 @@ __global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, c
 }
 
 struct SpatialArgs {
-    PairCtx pc;
-    const uint32_t *A;               // lookup array
-    const uint2 *ecell;              // packed min / max cell of each sorted entry
+    PairCtx pc;                      // rec / perm = the cell-ordered copies (indexed by A position)
+    const uint2 *ecell;              // packed min / max cell of entry A[i]
     const uint32_t *grab_row;        // [ngrab + 1] row of the first slot of each grab
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
@@ -809,7 +808,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
         exec += Bend - B;
 #pragma unroll 1
         for (int u0 = 0; u0 < SP_PER_LANE; u0 += SB) {
-            uint32_t ii[SB], ee[SB], cxy[SB], pp[SB];
+            uint32_t ii[SB], cxy[SB], pp[SB];
             bool vv[SB];
 #pragma unroll
             for (int u = 0; u < SB; ++u) {
@@ -825,18 +824,17 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     r_cxy = A.row_cxy[r];
                     r_p = A.row_q[r];
                 }
-                ii[u] = r_alo + (uint32_t)(s - r_start);
+                ii[u] = vv[u] ? r_alo + (uint32_t)(s - r_start) : 0u;
                 cxy[u] = r_cxy;
                 pp[u] = r_p;
-                ee[u] = vv[u] ? __ldg(A.A + ii[u]) : 0u;
             }
             float4 ea[SB], eb[SB];
             uint2 ec[SB];
 #pragma unroll
-            for (int u = 0; u < SB; ++u) {
-                ea[u] = __ldg(A.pc.rec + 2 * (uint64_t)ee[u]);
-                eb[u] = __ldg(A.pc.rec + 2 * (uint64_t)ee[u] + 1);
-                ec[u] = __ldg(A.ecell + ee[u]);
+            for (int u = 0; u < SB; ++u) {          // coalesced: consecutive slots, consecutive i
+                ea[u] = __ldg(A.pc.rec + 2 * (uint64_t)ii[u]);
+                eb[u] = __ldg(A.pc.rec + 2 * (uint64_t)ii[u] + 1);
+                ec[u] = __ldg(A.ecell + ii[u]);
             }
 #pragma unroll
             for (int u = 0; u < SB; ++u) {
@@ -863,7 +861,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     }
                     maybe = first && filter32(q, ea[u], eb[u], A.pc.d);
                 }
-                queue_add(W, qn, maybe, cur_qrow, ee[u], lane);
+                queue_add(W, qn, maybe, cur_qrow, ii[u], lane);
             }
             queue_drain<EXACT>(&A.pc, W, qn, lane);
         }
@@ -1205,8 +1203,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, ngrab, grab_row.p);
         TDS_CHECK_LAUNCH();
         SpatialArgs a{};
-        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-        a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
+        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o};
+        a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
         k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
@@ -1402,8 +1400,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, ngrab, grab_row.p);
             TDS_CHECK_LAUNCH();
             SpatialArgs a{};
-            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
-            a.A = idx->fsg_A; a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
+            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o};
+            a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;
             if (bnrows && bslots) {
