@@ -1,0 +1,96 @@
+"""Multi-GPU query sharding.
+
+The search is data-parallel over query segments (§4: one thread per
+query): queries are independent and the result set is the
+union of the per-query results.  On N GPUs every rank holds D and its index
+(replicated, built from the same input: the build is deterministic), answers a
+contiguous shard of Q, and keeps its records device-resident.  The only
+exchange step is the optional gather of the records to one rank
+(``gather_results``), done with ``torch.distributed`` collectives (NCCL over
+NVLink on the B200 box; gloo in the CPU tests).  Timing is max over ranks.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced slice [lo, hi) of n rows for ``rank`` of ``world``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def shard_by_trajectory(traj: np.ndarray, rank: int, world: int) -> tuple[int, int]:
+    """Slice [lo, hi) of rows that keeps whole trajectories on one rank.
+
+    ``traj`` is the (non-decreasing) trajectory id of each query row; segments of
+    a query trajectory stay together, which keeps the per-rank work
+    similar when trajectories have similar lengths."""
+    traj = np.asarray(traj)
+    n = traj.shape[0]
+    lo, hi = shard_bounds(n, rank, world)
+
+    def snap(i):
+        if i <= 0 or i >= n:
+            return min(max(i, 0), n)
+        # move to the start of the trajectory containing row i
+        return int(np.searchsorted(traj, traj[i], side="left"))
+    return snap(lo), snap(hi)
+
+
+def search_sharded(index, queries, d: float, kind: str = "spatiotemporal", window=(-math.inf, math.inf),
+                   rank: int | None = None, world: int | None = None, capacity: int = 0):
+    """Search this rank's shard of ``queries`` (all ranks pass the full query set).
+
+    Returns (result, q_offset): query ids in ``result`` are rows of the shard;
+    add ``q_offset`` for rows of the full query set."""
+    import torch.distributed as dist
+    if rank is None:
+        rank = dist.get_rank() if dist.is_initialized() else 0
+    if world is None:
+        world = dist.get_world_size() if dist.is_initialized() else 1
+    lo, hi = shard_bounds(int(queries.shape[0]), rank, world)
+    res = index.search(queries[lo:hi], d, window=window, kind=kind, capacity=capacity)
+    return res, lo
+
+
+def gather_results(qid, eid, t_in, t_out, q_offset: int = 0, dst: int = 0, group=None):
+    """Gather per-rank result columns to rank ``dst`` (the exchange step).
+
+    Inputs are 1-D tensors of equal length on the rank's device (CUDA with NCCL,
+    CPU with gloo); query ids are shifted by ``q_offset`` to rows of the full
+    query set.  Counts are exchanged first (all_gather of one int64 per rank);
+    records are then all-gathered padded to the largest count (a single
+    collective, no per-peer loops).  Returns the concatenated columns on
+    ``dst`` (rank order), None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = qid.device
+    n = torch.tensor([qid.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n, group=group)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts) if counts else 0
+    # pack as int32 x 4 columns (times bit-cast), pad to the max count
+    pack = torch.zeros((mx, 4), dtype=torch.int32, device=dev)
+    k = qid.numel()
+    if k:
+        pack[:k, 0] = qid.to(torch.int32) + int(q_offset)
+        pack[:k, 1] = eid.to(torch.int32)
+        pack[:k, 2] = t_in.to(torch.float32).view(torch.int32)
+        pack[:k, 3] = t_out.to(torch.float32).view(torch.int32)
+    bufs = [torch.empty_like(pack) for _ in range(world)]
+    dist.all_gather(bufs, pack, group=group)
+    if rank != dst:
+        return None
+    allp = torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+    return (allp[:, 0].clone(), allp[:, 1].clone(), allp[:, 2].clone().view(torch.float32),
+            allp[:, 3].clone().view(torch.float32))
