@@ -76,6 +76,25 @@ int num_sms() {
     return n;
 }
 
+uint64_t device_budget_bytes() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    uint64_t extra = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t reserved = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+            extra = reserved - used;
+    }
+    return (uint64_t)fr + extra;
+}
+
 // device copy of a caller buffer that may live in host memory
 struct Staged {
     const float4 *p = nullptr;

@@ -171,11 +171,11 @@ __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 e
     double a = fmax(fmax(t0q, t0e), T0);
     double b = fmin(fmin(t1q, t1e), T1);
     if (!(a < b)) return false;
-    double dq = t1q - t0q, de = t1e - t0e;
-    double vqx = ((double)qb.x - (double)qa.x) / dq, vqy = ((double)qb.y - (double)qa.y) / dq,
-           vqz = ((double)qb.z - (double)qa.z) / dq;
-    double vex = ((double)eb.x - (double)ea.x) / de, vey = ((double)eb.y - (double)ea.y) / de,
-           vez = ((double)eb.z - (double)ea.z) / de;
+    const double rq = 1.0 / (t1q - t0q), re = 1.0 / (t1e - t0e);   // 2 divisions instead of 6
+    double vqx = ((double)qb.x - (double)qa.x) * rq, vqy = ((double)qb.y - (double)qa.y) * rq,
+           vqz = ((double)qb.z - (double)qa.z) * rq;
+    double vex = ((double)eb.x - (double)ea.x) * re, vey = ((double)eb.y - (double)ea.y) * re,
+           vez = ((double)eb.z - (double)ea.z) * re;
     double Dx = ((double)qa.x + (a - t0q) * vqx) - ((double)ea.x + (a - t0e) * vex);
     double Dy = ((double)qa.y + (a - t0q) * vqy) - ((double)ea.y + (a - t0e) * vey);
     double Dz = ((double)qa.z + (a - t0q) * vqz) - ((double)ea.z + (a - t0e) * vez);
@@ -188,7 +188,8 @@ __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 e
         if (h <= d2) { t_in = (float)a; t_out = (float)b; return true; }
         return false;
     }
-    double su = -(Dx * Vx + Dy * Vy + Dz * Vz) / A;
+    const double iA = 1.0 / A;
+    double su = -(Dx * Vx + Dy * Vy + Dz * Vz) * iA;
     double ss = su < 0.0 ? 0.0 : (su > L ? L : su);
     double xs = Dx + ss * Vx, ys = Dy + ss * Vy, zs = Dz + ss * Vz;
     double hs = xs * xs + ys * ys + zs * zs;
@@ -197,7 +198,7 @@ __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 e
     double hu = xu * xu + yu * yu + zu * zu;
     double rem = d2 - hu;
     if (rem < 0.0) rem = 0.0;
-    double w = sqrt(rem / A);
+    double w = sqrt(rem * iA);
     double lo = fmin(fmax(su - w, 0.0), L), hi = fmin(fmax(su + w, 0.0), L);
     t_in = (float)(a + lo);
     t_out = (float)(a + hi);
@@ -246,8 +247,12 @@ __device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit,
     const unsigned hm = __ballot_sync(FULL, hit);
     if (!hm) return;
     if (EXACT) {
-        if (hit) {
-            uint32_t k = atomicAdd(&o.qfill[r.qid], 1u);
+        if (hit) {   // one atomic per (warp, query): lanes of the same query share it
+            const unsigned peers = __match_any_sync(hm, r.qid);
+            const int leader = __ffs(peers) - 1;
+            uint32_t k = 0;
+            if (lane == leader) k = atomicAdd(&o.qfill[r.qid], (uint32_t)__popc(peers));
+            k = __shfl_sync(peers, k, leader) + __popc(peers & ((1u << lane) - 1u));
             unsigned long long slot = o.qoff[r.qid] + k;
             reinterpret_cast<uint4 *>(o.buf)[slot] = make_uint4(r.qid, r.eid, __float_as_uint(r.t_in),
                                                                 __float_as_uint(r.t_out));
@@ -1168,9 +1173,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
 
     uint64_t cap = capacity;
     if (cap == 0) {
-        size_t fr = 0, tot = 0;
-        TDS_CUDA(cudaMemGetInfo(&fr, &tot));
-        uint64_t budget = (uint64_t)(fr * 0.35) / sizeof(Rec);
+        // budget: free device memory plus memory the stream-ordered pool holds unused
+        uint64_t budget = (uint64_t)(device_budget_bytes() * 0.45) / sizeof(Rec);
         cap = std::min<uint64_t>(hs.pair_tests + 64, budget);
         cap = std::max<uint64_t>(cap, 1024);
     }

@@ -170,6 +170,8 @@ void free_index(tds_index_s *idx);
 uint64_t validate_segments(const float4 *rec, uint64_t n, cudaStream_t s);
 
 int num_sms();
+// free device memory + memory reserved but unused in the default mempool (bytes)
+uint64_t device_budget_bytes();
 
 // ---------------------------------------------------------------------------
 // result records (16 B): (query row, entry row, t_in, t_out)
