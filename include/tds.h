@@ -171,7 +171,7 @@ const char *tds_last_error(void);
  *   6/7/8 st_off_x/y/z uint32[v*m+1]  start of subbin (slab j, bin i) at [j*m+i]
  *   9 fsg_cell_off uint32[gx*gy*gz+1]  dense CSR of cell h (row-major)
  *  10 fsg_A     uint32[len]     lookup array A of sorted-entry ids
- *  11 extents   float[16]       t_min, t_max, lo[3], hi[3], maxext[3], w_st[3], pad
+ *  11 extents   float[16]       t_min, t_max, lo[3], hi[3], maxext[3], w_st[3], max_dur, pad
  *  12 sorted_t0 float[n]        t_start of the sorted entries
  * Writes min(cap_bytes, size) bytes to dst (may be NULL to query the size) and the
  * full size to *n_bytes.  Errors: TDS_EINVAL (unknown / unbuilt array).

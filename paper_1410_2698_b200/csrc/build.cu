@@ -32,10 +32,10 @@ __host__ __device__ inline float key_float(uint32_t k) {
 }
 
 // A1: validate + reduce extents.  red[] layout (order-preserving keys):
-// 0 t_min, 1 t_max, 2..4 lo, 5..7 hi, 8..10 maxext
+// 0 t_min, 1 t_max, 2..4 lo, 5..7 hi, 8..10 maxext, 11 max duration (rounded up)
 __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
                                    unsigned long long *__restrict__ bad, uint32_t *__restrict__ red) {
-    float tmin = FLT_MAX, tmax = -FLT_MAX, lo[3], hi[3], mx[3];
+    float tmin = FLT_MAX, tmax = -FLT_MAX, lo[3], hi[3], mx[3], dur = 0.f;
 #pragma unroll
     for (int c = 0; c < 3; ++c) { lo[c] = FLT_MAX; hi[c] = -FLT_MAX; mx[c] = 0.f; }
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -46,6 +46,7 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
         if (!ok) { atomicMin(bad, (unsigned long long)i); continue; }
         tmin = fminf(tmin, a.w);
         tmax = fmaxf(tmax, b.w);
+        dur = fmaxf(dur, __fsub_ru(b.w, a.w));
         float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -59,6 +60,7 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
     for (int o = 16; o > 0; o >>= 1) {
         tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        dur = fmaxf(dur, __shfl_xor_sync(0xffffffffu, dur, o));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
@@ -66,14 +68,15 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
             mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
         }
     }
-    __shared__ float sred[NT / 32][11];
+    __shared__ float sred[NT / 32][12];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
         sred[w][0] = tmin; sred[w][1] = tmax;
         for (int c = 0; c < 3; ++c) { sred[w][2 + c] = lo[c]; sred[w][5 + c] = hi[c]; sred[w][8 + c] = mx[c]; }
+        sred[w][11] = dur;
     }
     __syncthreads();
-    if (threadIdx.x < 11) {
+    if (threadIdx.x < 12) {
         const int k = threadIdx.x;
         const bool is_min = (k == 0) || (k >= 2 && k <= 4);
         float v = sred[0][k];
@@ -84,7 +87,7 @@ __global__ void k_validate_extents(const float4 *__restrict__ rec, uint64_t n,
 
 __global__ void k_init_red(uint32_t *red, unsigned long long *bad) {
     int i = threadIdx.x;
-    if (i < 11) {
+    if (i < 12) {
         bool is_min = (i == 0) || (i >= 2 && i <= 4);
         red[i] = is_min ? 0xffffffffu : 0u;
     }
@@ -322,7 +325,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     unsigned long long hbad;
     uint32_t hred[16];
     TDS_CUDA(cudaMemcpyAsync(&hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
-    TDS_CUDA(cudaMemcpyAsync(hred, red.p, 11 * 4, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaMemcpyAsync(hred, red.p, 12 * 4, cudaMemcpyDeviceToHost, s));
     TDS_CUDA(cudaStreamSynchronize(s));
     if (hbad != ~0ull)
         fail(TDS_EDATA, "entry segment %llu has a non-finite value or t_end <= t_start", hbad);
@@ -334,6 +337,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         E.hi[c] = key_float(hred[5 + c]);
         E.maxext[c] = key_float(hred[8 + c]);
     }
+    E.max_dur = key_float(hred[11]);
     const bool want_st = (p->kinds & TDS_SPATIOTEMPORAL) != 0;
     const bool want_fsg = (p->kinds & TDS_SPATIAL) != 0;
     if (want_st) {   // admissible v: v <= (c_max - c_min) / max |c_start - c_end|

@@ -12,6 +12,7 @@
 //       of the affected queries (reading C22)
 //   A11 fetch
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -31,7 +32,7 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
-constexpr int UNROLL = 4;                // candidates per inner step (range kernel)
+constexpr int DIRECT_MIN = 12;           // lanes passing the filter for the in-place fp64 path
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
@@ -312,7 +313,7 @@ struct PairCtx {                     // what the fp64 path needs
 
 // Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
 template <bool EXACT>
-__device__ __noinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n) {
+__device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n) {
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
     const uint32_t q = v ? W->rq[lane] : 0u, j = v ? W->rj[lane] : 0u;
@@ -332,6 +333,29 @@ __device__ __noinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32
     __syncwarp();
     if (lane == 0) { W->refined += n; W->hits += __popc(hm); }
     __syncwarp();
+}
+
+// warp-wide dense path: when most lanes passed the filter for the same query,
+// evaluate in place (no queue round trip); returns the number of hits (all
+// belong to query `qid`, counted by the caller's owner lane).
+template <bool EXACT>
+__device__ __forceinline__ uint32_t refine_direct(const PairCtx *C, WarpState *W, bool m, uint32_t qid, uint32_t j,
+                                                  int lane) {
+    float tin = 0.f, tout = 0.f;
+    bool hit = false;
+    if (m)
+        hit = pair64(__ldg(C->Q + 2 * (uint64_t)qid), __ldg(C->Q + 2 * (uint64_t)qid + 1),
+                     __ldg(C->rec + 2 * (uint64_t)j), __ldg(C->rec + 2 * (uint64_t)j + 1), (double)C->d,
+                     (double)C->T0, (double)C->T1, tin, tout);
+    const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
+    Rec r{qid, eid, tin, tout};
+    append<EXACT>(C->o, *W, hit, r, lane);
+    const unsigned hm = __ballot_sync(FULL, hit);
+    const unsigned mm = __ballot_sync(FULL, m);
+    __syncwarp();
+    if (lane == 0) { W->refined += __popc(mm); W->hits += __popc(hm); }
+    __syncwarp();
+    return __popc(hm);
 }
 
 // warp-wide: queue the pairs whose fp32 filter passed (no flush here)
@@ -642,6 +666,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             whi = max(whi, __shfl_xor_sync(FULL, whi, o));
         }
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
+        uint32_t owner_hits = 0;             // hits of this lane's query found on the dense path
         // windows of 64 candidates: lane handles cand and cand + 32 (two independent
         // filter chains per query load)
         uint32_t base = wlo;
@@ -682,12 +707,24 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
                 if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                queue_add(W.ws, qn, m0, qid, j0, lane);
-                queue_add(W.ws, qn, m1, qid, j1, lane);
+                // dense windows (most lanes passed): evaluate in place; sparse: queue
+                uint32_t hits_g = 0;
+                if (__popc(__ballot_sync(FULL, m0)) >= DIRECT_MIN) {
+                    hits_g += refine_direct<EXACT>(&A.pc, &W.ws, m0, qid, j0, lane);
+                } else {
+                    queue_add(W.ws, qn, m0, qid, j0, lane);
+                }
+                if (__popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
+                    hits_g += refine_direct<EXACT>(&A.pc, &W.ws, m1, qid, j1, lane);
+                } else {
+                    queue_add(W.ws, qn, m1, qid, j1, lane);
+                }
+                if (lane == g) owner_hits += hits_g;
                 queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
             }
             base = cend;
         }
+        if (owner_hits) atomicAdd(&A.pc.o.qcount[S.qid], owner_hits);
     }
     if (qn) flush_refine<EXACT>(&A.pc, &W.ws, qn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
@@ -714,7 +751,8 @@ __device__ __forceinline__ void query_box(float4 a, float4 b, float d, const Fsg
 }
 
 __global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__restrict__ list, uint32_t n, float d,
-                            float T0, float T1, FsgGrid G, uint32_t *__restrict__ nrows, int4 *__restrict__ qbox) {
+                            float T0, float T1, FsgGrid G, uint32_t *__restrict__ nitems, int4 *__restrict__ qbox,
+                            unsigned long long *__restrict__ total) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     uint32_t k = list ? list[p] : p;
@@ -722,29 +760,61 @@ __global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__rest
     int lo[3], hi[3];
     query_box(a, b, d, G, lo, hi);
     bool live = fmaxf(a.w, T0) < fminf(b.w, T1);
-    nrows[p] = live ? (uint32_t)((hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1)) : 0u;
+    const unsigned long long cnt =
+        live ? (unsigned long long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1) : 0ull;
+    nitems[p] = (uint32_t)min(cnt, 0xffffffffull);
+    atomicAdd(total, cnt);
     qbox[2 * p] = make_int4(lo[0], lo[1], lo[2], (int)k);
     qbox[2 * p + 1] = make_int4(hi[0], hi[1], hi[2], 0);
 }
 
-__global__ void k_fsg_rows(const uint32_t *__restrict__ row_start, uint32_t n, const int4 *__restrict__ qbox,
-                           FsgGrid G, const uint32_t *__restrict__ cell_off, uint32_t *__restrict__ row_q,
-                           uint32_t *__restrict__ row_alo, uint32_t *__restrict__ row_len,
-                           uint32_t *__restrict__ row_cxy) {
-    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+// first i in [lo, hi) with t_start(i) > x (ge = false) or >= x (ge = true); the
+// entries of one cell are in t_start order (stable grouping of the sorted D)
+__device__ __forceinline__ uint32_t cell_time_bound(const float4 *__restrict__ frec, uint32_t lo, uint32_t hi, float x,
+                                                    bool ge) {
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        float t = __ldg(&frec[2 * (uint64_t)mid].w);
+        bool right = ge ? (t >= x) : (t > x);
+        if (right) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// one warp per query: work items = the (query, cell) pairs of its d-inflated
+// box, each a slice of the cell-ordered arrays.  Unless `literal`,
+// the slice is trimmed to the entries that can overlap the query in time:
+// t_start < t1q and t_start > t0q - max_dur (a time filter the paper's FSG does
+// not apply; the result set is unchanged).
+__global__ void k_fsg_items(const uint32_t *__restrict__ item_start, uint32_t n, const int4 *__restrict__ qbox,
+                            const float4 *__restrict__ Q, FsgGrid G, const uint32_t *__restrict__ cell_off,
+                            const float4 *__restrict__ frec, float T0, float T1, float max_dur, int literal,
+                            uint32_t *__restrict__ item_q, uint32_t *__restrict__ item_alo,
+                            uint32_t *__restrict__ item_len, uint32_t *__restrict__ item_cell) {
+    const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (p >= n) return;
-    int4 lo = qbox[2 * p], hi = qbox[2 * p + 1];
-    uint32_t r = row_start[p], rend = row_start[p + 1];
-    if (r == rend) return;
-    for (int x = lo.x; x <= hi.x; ++x)
-        for (int y = lo.y; y <= hi.y; ++y, ++r) {
-            uint64_t h0 = ((uint64_t)x * G.g[1] + y) * G.g[2];
-            uint32_t a0 = cell_off[h0 + lo.z], a1 = cell_off[h0 + hi.z + 1];
-            row_q[r] = p;                       // index into the query list / qbox
-            row_alo[r] = a0;
-            row_len[r] = a1 - a0;
-            row_cxy[r] = ((uint32_t)x << 16) | (uint32_t)y;
+    const uint32_t r0 = item_start[p], r1 = item_start[p + 1];
+    if (r0 == r1) return;
+    const int4 lo = qbox[2 * p], hi = qbox[2 * p + 1];
+    const uint32_t k = (uint32_t)lo.w;
+    const float t0c = fmaxf(Q[2 * (uint64_t)k].w, T0), t1c = fminf(Q[2 * (uint64_t)k + 1].w, T1);
+    const float tlo = __fsub_rd(t0c, max_dur);
+    const int ny = hi.y - lo.y + 1, nz = hi.z - lo.z + 1;
+    for (uint32_t c = lane; c < r1 - r0; c += 32) {
+        const int z = lo.z + (int)(c % nz), y = lo.y + (int)((c / nz) % ny), x = lo.x + (int)(c / (nz * ny));
+        const uint64_t h = ((uint64_t)x * G.g[1] + y) * G.g[2] + z;
+        uint32_t a0 = cell_off[h], a1 = cell_off[h + 1];
+        if (!literal && a0 < a1) {
+            a1 = cell_time_bound(frec, a0, a1, t1c, true);      // first t_start >= t1c
+            a0 = cell_time_bound(frec, a0, a1, tlo, false);     // first t_start > t0c - max_dur
         }
+        const uint32_t r = r0 + c;
+        item_q[r] = p;                        // index into the query list / qbox
+        item_alo[r] = a0;
+        item_len[r] = a1 > a0 ? a1 - a0 : 0u;
+        item_cell[r] = pack_cell(x, y, z);
+    }
 }
 
 struct SpatialArgs {
@@ -753,7 +823,7 @@ struct SpatialArgs {
     const uint32_t *grab_row;        // [ngrab + 1] row of the first slot of each grab
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
-    const uint32_t *row_q, *row_alo, *row_cxy;
+    const uint32_t *row_q, *row_alo, *row_cxy;   // work items (query, cell): query, slice start, packed cell
     const unsigned long long *slot_start;   // [nrows + 1]
     uint32_t nrows;
     FsgGrid G;
@@ -795,7 +865,6 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     uint32_t cur_qrow = 0;
     QConst q = make_qconst(make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 1.f), A.pc.T0, A.pc.T1);
     int4 qlo = make_int4(0, 0, 0, 0);
-    int qhiz = 0;
     constexpr int SB = 4;                       // slots per lane per batch (loads hoisted)
     while (true) {
         unsigned gi = 0;
@@ -848,22 +917,16 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     if (pp[u] != cur_p) {
                         cur_p = pp[u];
                         qlo = A.qbox[2 * cur_p];
-                        qhiz = A.qbox[2 * cur_p + 1].z;
                         cur_qrow = (uint32_t)qlo.w;
                         q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow),
                                         __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1), A.pc.T0, A.pc.T1);
                     }
                     // duplicate avoidance: test (q, e) only in the first cell (index-space
                     // min corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
-                    const uint32_t m0 = ec[u].x, m1 = ec[u].y;
+                    const uint32_t m0 = ec[u].x;
                     const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
-                    bool first = (rx == (int)(cxy[u] >> 16)) && (ry == (int)(cxy[u] & 0xffffu));
                     const int rz = max((int)(m0 & 0x3ffu), qlo.z);
-                    if (first && rz < min((int)(m1 & 0x3ffu), qhiz)) {
-                        // e occurs in several cells of this row: keep the occurrence in cell rz
-                        const uint64_t h = ((uint64_t)rx * A.G.g[1] + ry) * A.G.g[2] + rz;
-                        first = __ldg(A.cell_off + h) <= ii[u] && ii[u] < __ldg(A.cell_off + h + 1);
-                    }
+                    const bool first = pack_cell(rx, ry, rz) == cxy[u];
                     maybe = first && filter32(q, ea[u], eb[u], A.pc.d);
                 }
                 queue_add(W, qn, maybe, cur_qrow, ii[u], lane);
@@ -1023,6 +1086,13 @@ struct Timer {
 
 int persistent_blocks(int bps) { return num_sms() * bps; }
 
+// TDS_FSG_LITERAL=1: GPUSpatial candidates are whole cells, as in the paper
+// (no per-cell time trimming) — for ablation
+int fsg_literal() {
+    const char *e = getenv("TDS_FSG_LITERAL");
+    return (e && e[0] == '1') ? 1 : 0;
+}
+
 // build tiles + work items for schedule entries [lo, hi) of the sorted schedule
 // (the category counts in st describe the whole sorted schedule)
 uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, DBuf<Tile> &tiles,
@@ -1139,19 +1209,27 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         qbox = DBuf<int4>(2ull * n, s);
         row_start = DBuf<uint32_t>(n + 1, s);
         DBuf<uint32_t> nr(n + 1, s);
+        DBuf<unsigned long long> ntot(1, s);
         TDS_CUDA(cudaMemsetAsync(nr.p + n, 0, 4, s));
-        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p);
+        TDS_CUDA(cudaMemsetAsync(ntot.p, 0, 8, s));
+        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p, ntot.p);
         TDS_CHECK_LAUNCH();
         exclusive_scan_u32(nr.p, row_start.p, n + 1, nullptr, s);
-        TDS_CUDA(cudaMemcpyAsync(&nrows, row_start.p + n, 4, cudaMemcpyDeviceToHost, s));
+        unsigned long long items64 = 0;
+        TDS_CUDA(cudaMemcpyAsync(&items64, ntot.p, 8, cudaMemcpyDeviceToHost, s));
         TDS_CUDA(cudaStreamSynchronize(s));
+        if (items64 >= (1ull << 32) - 1)
+            fail(TDS_EINVAL, "the d-inflated query boxes cover %llu grid cells (limit 2^32): use a coarser grid",
+                 items64);
+        nrows = (uint32_t)items64;
         row_q = DBuf<uint32_t>(nrows, s);
         row_alo = DBuf<uint32_t>(nrows, s);
         row_len = DBuf<uint32_t>(nrows + 1, s);
         row_cxy = DBuf<uint32_t>(nrows, s);
         TDS_CUDA(cudaMemsetAsync(row_len.p + nrows, 0, 4, s));
-        k_fsg_rows<<<nblk(n), 256, 0, s>>>(row_start.p, n, qbox.p, G, idx->cell_off, row_q.p, row_alo.p, row_len.p,
-                                          row_cxy.p);
+        k_fsg_items<<<nblk((uint64_t)n * 32), 256, 0, s>>>(row_start.p, n, qbox.p, Q, G, idx->cell_off, idx->fsg_rec,
+                                                          T0, T1, idx->ext.max_dur, fsg_literal(), row_q.p,
+                                                          row_alo.p, row_len.p, row_cxy.p);
         TDS_CHECK_LAUNCH();
         DBuf<uint64_t> rl64(nrows + 1, s);
         k_u32_to_u64<<<nblk(nrows + 1), 256, 0, s>>>(row_len.p, nrows + 1, rl64.p);
@@ -1380,8 +1458,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             uint32_t nb = b1 - b0;
             DBuf<int4> bq(2ull * nb, s);
             DBuf<uint32_t> bnr(nb + 1, s), brs(nb + 1, s);
+            DBuf<unsigned long long> btot(1, s);
             TDS_CUDA(cudaMemsetAsync(bnr.p + nb, 0, 4, s));
-            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p);
+            TDS_CUDA(cudaMemsetAsync(btot.p, 0, 8, s));
+            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p, btot.p);
             TDS_CHECK_LAUNCH();
             exclusive_scan_u32(bnr.p, brs.p, nb + 1, nullptr, s);
             uint32_t bnrows = 0;
@@ -1389,7 +1469,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             TDS_CUDA(cudaStreamSynchronize(s));
             DBuf<uint32_t> rq(bnrows, s), ra(bnrows, s), rlen(bnrows + 1, s), rc(bnrows, s);
             TDS_CUDA(cudaMemsetAsync(rlen.p + bnrows, 0, 4, s));
-            k_fsg_rows<<<nblk(nb), 256, 0, s>>>(brs.p, nb, bq.p, G, idx->cell_off, rq.p, ra.p, rlen.p, rc.p);
+            k_fsg_items<<<nblk((uint64_t)nb * 32), 256, 0, s>>>(brs.p, nb, bq.p, Q, G, idx->cell_off, idx->fsg_rec, T0,
+                                                                T1, idx->ext.max_dur, fsg_literal(), rq.p, ra.p,
+                                                                rlen.p, rc.p);
             TDS_CHECK_LAUNCH();
             DBuf<uint64_t> rl64(bnrows + 1, s);
             DBuf<unsigned long long> ss(bnrows + 1, s);

@@ -79,7 +79,8 @@ struct DBuf {                      // RAII device buffer, freed stream-ordered
 struct Extents {                   // export layout (tds_index_export what=11)
     float t_min, t_max;
     float lo[3], hi[3], maxext[3], w_st[3];
-    float pad[2];
+    float max_dur;                 // max (t_end - t_start) over D, rounded up
+    float pad;
 };
 
 }  // namespace tds

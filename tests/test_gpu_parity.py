@@ -243,3 +243,20 @@ def test_dense_and_merger_subsample(tds, name, kinds):
         sets.append(np.sort(keys(got[0], got[1])))
     for s2 in sets[1:]:
         assert np.array_equal(s2, sets[0])
+
+
+@pytest.mark.parametrize("name", ["tiny", "merger-small"])
+def test_fsg_time_trim_equals_literal(tds, name, monkeypatch):
+    """GPUSpatial with per-cell time trimming returns exactly the paper-literal
+    FSG result (TDS_FSG_LITERAL=1: whole cells as candidates)."""
+    w = synth.tiny() if name == "tiny" else synth.merger(n_per_disk=4096)
+    d = w.d if name == "tiny" else 1.5
+    idx = tds.Index(_cuda(w.D), kinds=tds.SPATIAL, m=10, grid=w.grid)
+    got, st = _run(idx, w.Q, d, "spatial")
+    monkeypatch.setenv("TDS_FSG_LITERAL", "1")
+    lit, st_l = _run(idx, w.Q, d, "spatial")
+    monkeypatch.delenv("TDS_FSG_LITERAL")
+    assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(lit[0], lit[1])))
+    assert st["pair_tests"] <= st_l["pair_tests"]
+    if name != "tiny":
+        assert st["pair_tests"] < st_l["pair_tests"] / 4      # time trimming prunes most of a cell
