@@ -65,16 +65,32 @@ void dfree(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+// A separate stream-ordered pool for the large result buffers, so that their
+// blocks are reused by later searches instead of being split by the many small
+// temporaries of the default pool (which forces fresh mappings of tens of GB).
+static cudaMemPool_t big_pool() {
+    static cudaMemPool_t pool = nullptr;
+    static int dev_of_pool = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (pool && dev_of_pool == dev) return pool;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        pool = nullptr;
+        return nullptr;
     }
-    return n;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    dev_of_pool = dev;
+    return pool;
 }
+
+void *dalloc_big(size_t bytes, cudaStream_t s);
 
 uint64_t device_budget_bytes() {
     size_t fr = 0, tot = 0;
@@ -85,14 +101,40 @@ uint64_t device_budget_bytes() {
     uint64_t extra = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaMemPool_t pools[2] = {nullptr, big_pool()};
+    cudaDeviceGetDefaultMemPool(&pools[0], dev);
+    for (cudaMemPool_t pool : pools) {
+        if (!pool) continue;
         uint64_t reserved = 0, used = 0;
         if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
             cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
-            extra = reserved - used;
+            extra += reserved - used;
     }
     return (uint64_t)fr + extra;
+}
+
+void *dalloc_big(size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool = big_pool();
+    if (!pool) return dalloc(bytes, s);
+    void *p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? TDS_ENOMEM : TDS_ECUDA, "cudaMallocFromPoolAsync(%zu bytes): %s", bytes,
+             cudaGetErrorString(e));
+    }
+    return p;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
 
 // device copy of a caller buffer that may live in host memory

@@ -889,11 +889,10 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                 const unsigned long long s = B + (unsigned long long)(u0 + u) * 32 + lane;
                 vv[u] = s < Bend;
                 if (vv[u] && s >= r_next) {
-                    do {
-                        ++r;
-                        r_start = r_next;
-                        r_next = A.slot_start[r + 1];
-                    } while (s >= r_next);
+                    // next item holding slot s (binary search: many (query, cell) items are empty)
+                    r = find_row(A.slot_start, r + 1, rhi, s);
+                    r_start = A.slot_start[r];
+                    r_next = A.slot_start[r + 1];
                     r_alo = A.row_alo[r];
                     r_cxy = A.row_cxy[r];
                     r_p = A.row_q[r];
@@ -1262,7 +1261,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(32, cap / (16 * nwarps)));
     CS = (CS + 31) / 32 * 32;
     const uint64_t nchunks = (cap + CS - 1) / CS;
-    DBuf<Rec> buf(cap, s);
+    DBuf<Rec> buf(cap, s, /*big=*/true);
     DBuf<uint32_t> chunk_used(nchunks, s);
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
 
@@ -1304,6 +1303,24 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     TDS_CHECK_LAUNCH();
     exclusive_scan_u64(chunk_off.p, chunk_off.p, nchunks, nullptr, s);
 
+    if (hs.dropped == 0 && cap >= (1ull << 22) && hs.hits <= cap / 8) {
+        // few results in a large pass buffer: compact them into a right-sized store
+        // and return the buffer to the pool for the next search
+        DBuf<Rec> store(hs.hits, s, /*big=*/hs.hits * sizeof(Rec) > (256ull << 20));
+        k_flatten<<<nblk(nchunks * 32), 256, 0, s>>>(buf.p, CS, nchunks, chunk_used.p, chunk_off.p, store.p);
+        TDS_CHECK_LAUNCH();
+        res->chunked = false;
+        res->store = store.release();
+        res->n = hs.hits;
+        tm.mark(4);
+        TDS_CUDA(cudaEventSynchronize(tm.e[4]));
+        S.n_results = res->n;
+        S.ms_schedule = tm.ms(0, 1);
+        S.ms_pairs = tm.ms(2, 3);
+        S.ms_compact = tm.ms(3, 4);
+        S.ms_total = tm.ms(0, 4);
+        return;
+    }
     if (hs.dropped == 0) {
         res->chunked = true;
         res->buf = buf.release();
@@ -1326,7 +1343,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     const uint64_t stored = std::min<unsigned long long>(hs.reserved, cap);
     uint64_t nflat = hs.hits - hs.dropped;          // records physically in the buffer
     (void)stored;
-    DBuf<Rec> flat(nflat, s);
+    DBuf<Rec> flat(nflat, s, /*big=*/true);
     DBuf<uint8_t> keep(nflat, s);
     k_keep_flags<<<nblk(nchunks * 32), 256, 0, s>>>(buf.p, CS, nchunks, chunk_used.p, chunk_off.p, redo.p, flat.p,
                                                   keep.p, nflat);
@@ -1378,7 +1395,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         redo_total += c;
     }
     const uint64_t total = (uint64_t)nkept + redo_total;
-    DBuf<Rec> store(total, s);
+    DBuf<Rec> store(total, s, /*big=*/true);
     k_scatter_kept<<<nblk(nflat), 256, 0, s>>>(flat.p, keep.p, kpos.p, nflat, store.p);
     TDS_CHECK_LAUNCH();
     flat.reset();

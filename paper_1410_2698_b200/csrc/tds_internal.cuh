@@ -52,6 +52,7 @@ void count_launch();
 // stream-ordered device memory (cudaMallocAsync from the default pool)
 // ---------------------------------------------------------------------------
 void *dalloc(size_t bytes, cudaStream_t s);
+void *dalloc_big(size_t bytes, cudaStream_t s);   // large result buffers (separate pool)
 void dfree(void *p, cudaStream_t s);
 
 template <class T>
@@ -60,7 +61,9 @@ struct DBuf {                      // RAII device buffer, freed stream-ordered
     size_t n = 0;
     cudaStream_t s = 0;
     DBuf() = default;
-    DBuf(size_t n_, cudaStream_t s_) : n(n_), s(s_) { p = (T *)dalloc((n_ ? n_ : 1) * sizeof(T), s_); }
+    DBuf(size_t n_, cudaStream_t s_, bool big = false) : n(n_), s(s_) {
+        p = (T *)(big ? dalloc_big((n_ ? n_ : 1) * sizeof(T), s_) : dalloc((n_ ? n_ : 1) * sizeof(T), s_));
+    }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
     DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; }
