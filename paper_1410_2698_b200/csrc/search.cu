@@ -48,6 +48,8 @@ struct DevStats {
     unsigned long long pair_tests;   // algorithmic candidate pairs
     unsigned long long fallback;     // ST temporal fallbacks
     unsigned long long total_slots;  // spatial: flattened slots
+    unsigned long long bad;          // ~(first invalid query row), 0 = none (atomicMax)
+    unsigned long long union_total;  // sum of tile union lengths (chunk sizing)
     unsigned int work_ctr;           // dynamic work distribution
     unsigned int total_items;
     unsigned int ch;                 // candidates per work item
@@ -450,6 +452,9 @@ __global__ void k_schedule(SchedArgs A) {
     if (p < A.nq) {
         uint32_t k = A.order ? A.order[p] : p;
         float4 a = A.Q[2 * (uint64_t)k], b = A.Q[2 * (uint64_t)k + 1];
+        const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) &&
+                        isfinite(b.y) && isfinite(b.z) && isfinite(b.w) && (b.w > a.w);
+        if (!ok) atomicMax(&A.st->bad, ~(unsigned long long)k);
         float t0c = fmaxf(a.w, A.T0), t1c = fminf(b.w, A.T1);
         Sched S{k, 0u, 0u, 3};
         if (t0c < t1c) {
@@ -517,8 +522,9 @@ __global__ void k_permute_sched(const Sched *__restrict__ in, const uint32_t *__
 
 // tiles: runs of <= 32 consecutive schedule entries within one category
 __global__ void k_make_tiles(const Sched *__restrict__ S, uint32_t n_base, uint32_t n_total_entries,
-                             const DevStats *__restrict__ st, uint32_t range_lo, uint32_t range_hi,
+                             DevStats *__restrict__ st_w, uint32_t range_lo, uint32_t range_hi,
                              Tile *__restrict__ tiles, uint32_t max_tiles, uint32_t *__restrict__ nchunk_len) {
+    const DevStats *st = st_w;
     // one warp per tile slot; the tile layout is derived from the category counts
     uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
@@ -564,6 +570,8 @@ __global__ void k_make_tiles(const Sched *__restrict__ S, uint32_t n_base, uint3
     if (lane == 0) {
         tiles[t] = T;
         nchunk_len[t] = T.uhi - T.ulo;
+        if (T.uhi > T.ulo) atomicAdd(&st_w->union_total, (unsigned long long)(T.uhi - T.ulo));
+        if (t == max_tiles - 1) nchunk_len[max_tiles] = 0;
     }
 }
 
@@ -622,7 +630,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     const int lane = threadIdx.x & 31;
     RangeWarpSmem &W = sm[threadIdx.x >> 5];
     DevStats *st = A.pc.o.st;
-    const uint32_t total = st->total_items;
+    const uint32_t total = A.item_start[A.ntiles];
     const uint32_t CH = st->ch;
     const float d = A.pc.d;
     warp_state_init(W.ws, lane);
@@ -752,11 +760,14 @@ __device__ __forceinline__ void query_box(float4 a, float4 b, float d, const Fsg
 
 __global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__restrict__ list, uint32_t n, float d,
                             float T0, float T1, FsgGrid G, uint32_t *__restrict__ nitems, int4 *__restrict__ qbox,
-                            unsigned long long *__restrict__ total) {
+                            unsigned long long *__restrict__ total, unsigned long long *__restrict__ bad) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     uint32_t k = list ? list[p] : p;
     float4 a = Q[2 * (uint64_t)k], b = Q[2 * (uint64_t)k + 1];
+    const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) &&
+                    isfinite(b.y) && isfinite(b.z) && isfinite(b.w) && (b.w > a.w);
+    if (!ok) atomicMax(bad, ~(unsigned long long)k);
     int lo[3], hi[3];
     query_box(a, b, d, G, lo, hi);
     bool live = fmaxf(a.w, T0) < fminf(b.w, T1);
@@ -1085,6 +1096,25 @@ struct Timer {
 
 int persistent_blocks(int bps) { return num_sms() * bps; }
 
+// per-thread reusable CUDA events and pinned host copy of DevStats (avoid
+// creating events / staging pageable copies on every search)
+Timer &timer_for(cudaStream_t s) {
+    static thread_local Timer *t = nullptr;
+    if (!t) t = new Timer(s);
+    t->s = s;
+    return *t;
+}
+
+DevStats *pinned_stats() {
+    static thread_local DevStats *p = nullptr;
+    if (!p && cudaMallocHost(&p, sizeof(DevStats)) != cudaSuccess) {
+        cudaGetLastError();
+        static thread_local DevStats fallback;
+        p = &fallback;
+    }
+    return p;
+}
+
 // TDS_FSG_LITERAL=1: GPUSpatial candidates are whole cells, as in the paper
 // (no per-cell time trimming) — for ablation
 int fsg_literal() {
@@ -1100,20 +1130,13 @@ uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, 
     uint32_t max_tiles = n / 32 + 5;
     tiles = DBuf<Tile>(max_tiles, s);
     item_start = DBuf<uint32_t>(max_tiles + 1, s);
-    TDS_CUDA(cudaMemsetAsync(item_start.p, 0, 4ull * (max_tiles + 1), s));
-    DBuf<unsigned long long> tot(1, s);
-    TDS_CUDA(cudaMemsetAsync(tot.p, 0, 8, s));
     k_make_tiles<<<nblk((uint64_t)max_tiles * 32), 256, 0, s>>>(sched, lo, n, st, lo, hi, tiles.p, max_tiles,
                                                                 item_start.p);
     TDS_CHECK_LAUNCH();
-    k_sum_u32<<<std::min<unsigned>(nblk(max_tiles), 1024), 256, 0, s>>>(item_start.p, max_tiles, tot.p);
-    TDS_CHECK_LAUNCH();
     uint32_t target = (uint32_t)persistent_blocks(RANGE_BPS) * (PT / 32) * 4;
-    k_tile_chunks<<<nblk(max_tiles), 256, 0, s>>>(item_start.p, max_tiles, tot.p, st, target);
+    k_tile_chunks<<<nblk(max_tiles), 256, 0, s>>>(item_start.p, max_tiles, &st->union_total, st, target);
     TDS_CHECK_LAUNCH();
     exclusive_scan_u32(item_start.p, item_start.p, max_tiles + 1, nullptr, s);
-    k_set_total_items<<<1, 1, 0, s>>>(item_start.p, max_tiles, st);
-    TDS_CHECK_LAUNCH();
     return max_tiles;
 }
 
@@ -1137,26 +1160,27 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     res->chunked = false;
     if (nq == 0) return;
     if (nq >= (1ull << 31)) fail(TDS_EINVAL, "nq = %llu too large", (unsigned long long)nq);
-    Timer tm(s);
+    Timer &tm = timer_for(s);
     tm.mark(0);
-    DBuf<DevStats> dst(1, s);
-    TDS_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(DevStats), s));
-    DBuf<unsigned long long> bad(1, s);
-    TDS_CUDA(cudaMemsetAsync(bad.p, 0xff, 8, s));
     const uint32_t n = (uint32_t)nq;
+    // one zeroed header allocation: device stats, per-query counts, redo flags
+    const size_t hdr = (sizeof(DevStats) + 4ull * n + n + 15) & ~(size_t)15;
+    DBuf<uint8_t> header(hdr, s);
+    TDS_CUDA(cudaMemsetAsync(header.p, 0, hdr, s));
+    DevStats *dstp = reinterpret_cast<DevStats *>(header.p);
+    uint32_t *qcount_p = reinterpret_cast<uint32_t *>(header.p + sizeof(DevStats));
+    uint8_t *redo_p = header.p + sizeof(DevStats) + 4ull * n;
+    struct { DevStats *p; } dst{dstp};
+    struct { uint32_t *p; } qcount{qcount_p};
+    struct { uint8_t *p; } redo{redo_p};
 
-    // ---- A6: validate queries; GPUTemporal / GPUSpatioTemporal order them by
-    // (selector, range start) below, which subsumes the t_start sort of P:681-682
-    // (range starts are monotone in t_start); FSG keeps input order
-    DBuf<uint32_t> keys(n, s), order(n, s);
-    k_query_keys<<<nblk(n), 256, 0, s>>>(Q, nq, keys.p, order.p, bad.p);
-    TDS_CHECK_LAUNCH();
+    // ---- A6: queries are validated inside the schedule kernels; GPUTemporal /
+    // GPUSpatioTemporal order them by (selector, range start) below, which subsumes
+    // the t_start sort of P:681-682 (range starts are monotone in t_start); FSG
+    // keeps input order
     const bool spatial = (kind == TDS_SPATIAL);
-
-    DBuf<uint32_t> qcount(n, s);
-    DBuf<uint8_t> redo(n, s);
-    TDS_CUDA(cudaMemsetAsync(qcount.p, 0, 4ull * n, s));
-    TDS_CUDA(cudaMemsetAsync(redo.p, 0, n, s));
+    DBuf<uint32_t> keys, order;
+    if (!spatial) { keys = DBuf<uint32_t>(n, s); order = DBuf<uint32_t>(n, s); }
 
     // ---- A7: schedule ---------------------------------------------------------
     DBuf<Sched> sched;
@@ -1211,7 +1235,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         DBuf<unsigned long long> ntot(1, s);
         TDS_CUDA(cudaMemsetAsync(nr.p + n, 0, 4, s));
         TDS_CUDA(cudaMemsetAsync(ntot.p, 0, 8, s));
-        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p, ntot.p);
+        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p, ntot.p, &dst.p->bad);
         TDS_CHECK_LAUNCH();
         exclusive_scan_u32(nr.p, row_start.p, n + 1, nullptr, s);
         unsigned long long items64 = 0;
@@ -1237,12 +1261,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         exclusive_scan_u64(rl64.p, (uint64_t *)slot_start.p, nrows + 1, (uint64_t *)&dst.p->pair_tests, s);
     }
     // pair tests bound the result count: size the pass buffer
-    DevStats hs;
+    DevStats &hs = *pinned_stats();
     TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
-    unsigned long long hbad = 0;
-    TDS_CUDA(cudaMemcpyAsync(&hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
     TDS_CUDA(cudaStreamSynchronize(s));
-    if (hbad != ~0ull) fail(TDS_EDATA, "query segment %llu has a non-finite value or t_end <= t_start", hbad);
+    if (hs.bad) fail(TDS_EDATA, "query segment %llu has a non-finite value or t_end <= t_start", ~hs.bad);
     tm.mark(1);
     S.pair_tests = hs.pair_tests;
     S.fallback_queries = hs.fallback;
@@ -1298,17 +1320,21 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     S.refined_pairs = hs.refined;
     S.pairs_executed = hs.executed;
 
-    DBuf<uint64_t> chunk_off(nchunks, s);
-    k_chunk_offsets_u64<<<nblk(nchunks), 256, 0, s>>>(chunk_used.p, nchunks, chunk_off.p);
+    // only the first nres chunks were ever reserved (reservations are sequential)
+    const uint64_t nres = std::min<uint64_t>(nchunks, (std::min<unsigned long long>(hs.reserved, cap) + CS - 1) / CS);
+    DBuf<uint64_t> chunk_off(std::max<uint64_t>(nres, 1), s);
+    k_chunk_offsets_u64<<<nblk(std::max<uint64_t>(nres, 1)), 256, 0, s>>>(chunk_used.p, nres, chunk_off.p);
     TDS_CHECK_LAUNCH();
-    exclusive_scan_u64(chunk_off.p, chunk_off.p, nchunks, nullptr, s);
+    exclusive_scan_u64(chunk_off.p, chunk_off.p, nres, nullptr, s);
 
     if (hs.dropped == 0 && cap >= (1ull << 22) && hs.hits <= cap / 8) {
         // few results in a large pass buffer: compact them into a right-sized store
         // and return the buffer to the pool for the next search
         DBuf<Rec> store(hs.hits, s, /*big=*/hs.hits * sizeof(Rec) > (256ull << 20));
-        k_flatten<<<nblk(nchunks * 32), 256, 0, s>>>(buf.p, CS, nchunks, chunk_used.p, chunk_off.p, store.p);
-        TDS_CHECK_LAUNCH();
+        if (nres) {
+            k_flatten<<<nblk(nres * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, chunk_off.p, store.p);
+            TDS_CHECK_LAUNCH();
+        }
         res->chunked = false;
         res->store = store.release();
         res->n = hs.hits;
@@ -1326,7 +1352,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         res->buf = buf.release();
         res->cap = cap;
         res->CS = CS;
-        res->nchunks = nchunks;
+        res->nchunks = nres;
         res->chunk_used = chunk_used.release();
         res->chunk_off = chunk_off.release();
         res->n = hs.hits;
@@ -1345,7 +1371,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     (void)stored;
     DBuf<Rec> flat(nflat, s, /*big=*/true);
     DBuf<uint8_t> keep(nflat, s);
-    k_keep_flags<<<nblk(nchunks * 32), 256, 0, s>>>(buf.p, CS, nchunks, chunk_used.p, chunk_off.p, redo.p, flat.p,
+    k_keep_flags<<<nblk(std::max<uint64_t>(nres, 1) * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, chunk_off.p, redo.p, flat.p,
                                                   keep.p, nflat);
     TDS_CHECK_LAUNCH();
     DBuf<uint32_t> kpos(nflat + 1, s), k32(nflat + 1, s);
@@ -1478,7 +1504,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             DBuf<unsigned long long> btot(1, s);
             TDS_CUDA(cudaMemsetAsync(bnr.p + nb, 0, 4, s));
             TDS_CUDA(cudaMemsetAsync(btot.p, 0, 8, s));
-            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p, btot.p);
+            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p, btot.p,
+                                                 &dst.p->bad);
             TDS_CHECK_LAUNCH();
             exclusive_scan_u32(bnr.p, brs.p, nb + 1, nullptr, s);
             uint32_t bnrows = 0;
