@@ -201,20 +201,16 @@ class Result:
         cnt = self.count - first if count is None else int(count)
         if device:
             import torch
-            if out is None:
-                q = torch.empty(cnt, dtype=torch.int32, device="cuda")
-                e = torch.empty(cnt, dtype=torch.int32, device="cuda")
-                ti = torch.empty(cnt, dtype=torch.float32, device="cuda")
-                to = torch.empty(cnt, dtype=torch.float32, device="cuda")
+            if out is None:     # one allocation for the four columns
+                buf = torch.empty((4, cnt), dtype=torch.int32, device="cuda")
+                q, e, ti, to = buf[0], buf[1], buf[2].view(torch.float32), buf[3].view(torch.float32)
             else:
                 q, e, ti, to = out
             ptrs = [ctypes.c_void_p(t.data_ptr()) for t in (q, e, ti, to)]
         else:
             if out is None:
-                q = np.empty(cnt, np.uint32)
-                e = np.empty(cnt, np.uint32)
-                ti = np.empty(cnt, np.float32)
-                to = np.empty(cnt, np.float32)
+                buf = np.empty((4, cnt), np.uint32)
+                q, e, ti, to = buf[0], buf[1], buf[2].view(np.float32), buf[3].view(np.float32)
             else:
                 q, e, ti, to = out
             ptrs = [ctypes.c_void_p(a.ctypes.data) for a in (q, e, ti, to)]

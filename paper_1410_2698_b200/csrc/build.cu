@@ -461,6 +461,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     }
 
     idx->rec = rec.release();
+    idx->mem_budget = device_budget_bytes();
     idx->perm = perm.release();
     idx->bin_off = bin_off.release();
     idx->bin_lo = bin_lo.release();

@@ -12,6 +12,8 @@
 //       of the affected queries (reading C22)
 //   A11 fetch
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -1272,8 +1274,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
 
     uint64_t cap = capacity;
     if (cap == 0) {
-        // budget: free device memory plus memory the stream-ordered pool holds unused
-        uint64_t budget = (uint64_t)(device_budget_bytes() * 0.45) / sizeof(Rec);
+        // budget: free device memory plus memory the pools hold unused, measured at
+        // index build (cudaMemGetInfo costs up to milliseconds: not per search)
+        uint64_t budget = (uint64_t)(idx->mem_budget * 0.45) / sizeof(Rec);
         cap = std::min<uint64_t>(hs.pair_tests + 64, budget);
         cap = std::max<uint64_t>(cap, 1024);
     }
@@ -1283,7 +1286,17 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(32, cap / (16 * nwarps)));
     CS = (CS + 31) / 32 * 32;
     const uint64_t nchunks = (cap + CS - 1) / CS;
-    DBuf<Rec> buf(cap, s, /*big=*/true);
+    DBuf<Rec> buf;
+    for (;;) {
+        try {
+            buf = DBuf<Rec>(cap, s, /*big=*/true);
+            break;
+        } catch (const Error &e) {
+            if (e.code != TDS_ENOMEM || capacity != 0 || cap <= (1ull << 20)) throw;
+            cap /= 2;                     // auto capacity: retry smaller (overflow re-plan covers the rest)
+            set_error(0, "");
+        }
+    }
     DBuf<uint32_t> chunk_used(nchunks, s);
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
 
