@@ -2,8 +2,10 @@
 // checking, host/device input detection, error reporting, handle lifetime.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <new>
 #include <atomic>
+#include <chrono>
 
 #include "tds_internal.cuh"
 
@@ -92,7 +94,26 @@ static cudaMemPool_t big_pool() {
 
 void *dalloc_big(size_t bytes, cudaStream_t s);
 
+static uint64_t device_budget_bytes_now();
+
+// cached: cudaMemGetInfo costs up to milliseconds, so refresh at most every 0.5 s
+// (allocation failures fall back to smaller buffers)
 uint64_t device_budget_bytes() {
+    static thread_local uint64_t cached = 0;
+    static thread_local std::chrono::steady_clock::time_point when{};
+    static thread_local int dev_of = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto now = std::chrono::steady_clock::now();
+    if (dev != dev_of || cached == 0 || now - when > std::chrono::milliseconds(500)) {
+        cached = device_budget_bytes_now();
+        when = now;
+        dev_of = dev;
+    }
+    return cached;
+}
+
+static uint64_t device_budget_bytes_now() {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
         cudaGetLastError();
@@ -124,6 +145,35 @@ void *dalloc_big(size_t bytes, cudaStream_t s) {
              cudaGetErrorString(e));
     }
     return p;
+}
+
+Trace::Trace(cudaStream_t s_) : s(s_) {
+    const char *e = getenv("TDS_TRACE");
+    on = e && e[0] == '1';
+    if (on) mark("start");
+}
+
+void Trace::mark(const char *name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+}
+
+Trace::~Trace() {
+    if (!on) return;
+    cudaEventSynchronize(ev.back().second);
+    std::string line = "[tds trace]";
+    for (size_t i = 1; i < ev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+        char b[96];
+        snprintf(b, sizeof b, " %s %.3f", ev[i].first, ms);
+        line += b;
+    }
+    fprintf(stderr, "%s\n", line.c_str());
+    for (auto &x : ev) cudaEventDestroy(x.second);
 }
 
 int num_sms() {

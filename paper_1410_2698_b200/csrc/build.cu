@@ -277,6 +277,41 @@ __global__ void k_cell_emit(const float4 *__restrict__ rec, uint64_t n, Grid3 G,
 
 inline unsigned nblk(uint64_t n, int nt = NT) { return (unsigned)((n + nt - 1) / nt); }
 
+// per-thread side streams and events used to overlap independent build phases
+void side_streams(cudaStream_t out[4]) {
+    static thread_local cudaStream_t ss[4] = {nullptr, nullptr, nullptr, nullptr};
+    static thread_local int dev_of = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev_of != dev) {
+        for (auto &x : ss) TDS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        dev_of = dev;
+    }
+    for (int i = 0; i < 4; ++i) out[i] = ss[i];
+}
+
+cudaEvent_t fork_event() {
+    static thread_local cudaEvent_t e = nullptr;
+    if (!e) TDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+}
+
+cudaEvent_t join_event(cudaStream_t s) {
+    static thread_local cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+    static thread_local cudaStream_t owner[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int i = 0; i < 4; ++i) {
+        if (owner[i] == s && e[i]) return e[i];
+        if (!owner[i]) {
+            TDS_CUDA(cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming));
+            owner[i] = s;
+            return e[i];
+        }
+    }
+    cudaEvent_t x;
+    TDS_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    return x;
+}
+
 int bits_for(uint64_t nk) {
     int b = 0;
     while ((1ull << b) < nk) ++b;
@@ -309,6 +344,7 @@ uint64_t validate_segments(const float4 *rec, uint64_t n, cudaStream_t s) {
 void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, cudaStream_t s,
                  tds_index_s *idx) {
     const float4 *in = reinterpret_cast<const float4 *>(entries);
+    Trace tr(s);
     idx->n = n;
     idx->m = p->m_bins;
     idx->v = p->v_subbins;
@@ -349,6 +385,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         }
     }
 
+    tr.mark("validate+sync");
     // ---- A2: stable radix sort by t_start, renumber, gather -----------------
     DBuf<uint32_t> keys(n, s), perm(n, s);
     k_time_keys<<<nblk(n), NT, 0, s>>>(in, n, keys.p, perm.p);
@@ -359,6 +396,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     TDS_CHECK_LAUNCH();
     keys.reset();
 
+    tr.mark("tsort+gather");
     // ---- A3: temporal bins ---------------------------------------------------
     const int m = idx->m;
     double t_min = E.t_min, b = ((double)E.t_max - (double)E.t_min) / (double)m;
@@ -374,6 +412,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     k_prefix_max<<<1, 1024, 0, s>>>(bin_hi.p, bin_pmhi.p, m);
     TDS_CHECK_LAUNCH();
 
+    tr.mark("bins");
     // ---- A5 + A4, phase 1: membership counts and their prefix sums for the three
     // subbin arrays and the FSG, read back with ONE synchronisation
     const int v = idx->v;
@@ -422,15 +461,26 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         TDS_CUDA(cudaStreamSynchronize(s));
     }
 
+    tr.mark("counts+sync");
+    // ---- phase 2: the three subbin arrays and the FSG are independent: build them
+    // concurrently on forked streams (joined before returning)
+    cudaStream_t side[4];
+    side_streams(side);
+    cudaEvent_t fork = fork_event();
+    TDS_CUDA(cudaEventRecord(fork, s));
+    for (auto ss : side) TDS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+
     // ---- A5, phase 2: spatiotemporal subbin arrays ------------------
     if (want_st) {
         for (int c = 0; c < 3; ++c) {
+            cudaStream_t sc = side[c];
             const uint64_t len = tot[c] & 0xffffffffull;
-            DBuf<uint32_t> k2(len, s), v2(len, s), off((uint64_t)v * m + 1, s);
-            k_slab_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, st_pos[c].p, k2.p,
-                                              v2.p);
+            DBuf<uint32_t> k2(len, sc), v2(len, sc), off((uint64_t)v * m + 1, sc);
+            k_slab_emit<<<nblk(n), NT, 0, sc>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, st_pos[c].p, k2.p,
+                                               v2.p);
             TDS_CHECK_LAUNCH();
-            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, s);
+            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, sc);
+            st_pos[c].s = sc;                      // free after its last use, on that stream
             idx->st_arr[c] = v2.release();
             idx->st_len[c] = len;
             idx->st_off[c] = off.release();
@@ -439,18 +489,20 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
 
     // ---- A4, phase 2: FSG (dense CSR over all cells) -----------------
     if (want_fsg) {
+        cudaStream_t sf = side[3];
         const unsigned long long len = tot[3];
         if (len >= (1ull << 32) - 1)
             fail(TDS_EINVAL, "FSG lookup array would hold %llu ids (limit 2^32); use a coarser grid", len);
-        DBuf<uint32_t> k2(len, s), v2(len, s), off(ncell + 1, s);
-        k_cell_emit<<<nblk(n), NT, 0, s>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
+        DBuf<uint32_t> k2(len, sf), v2(len, sf), off(ncell + 1, sf);
+        k_cell_emit<<<nblk(n), NT, 0, sf>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
         TDS_CHECK_LAUNCH();
-        group_by_key(k2.p, v2.p, len, ncell, off.p, s);
-        DBuf<uint2> ecell(len, s);
-        DBuf<float4> frec(2 * len, s);
-        DBuf<uint32_t> fperm(len, s);
-        k_fsg_materialise<<<nblk(len), NT, 0, s>>>(rec.p, perm.p, v2.p, len, G, frec.p, fperm.p, ecell.p);
+        group_by_key(k2.p, v2.p, len, ncell, off.p, sf);
+        DBuf<uint2> ecell(len, sf);
+        DBuf<float4> frec(2 * len, sf);
+        DBuf<uint32_t> fperm(len, sf);
+        k_fsg_materialise<<<nblk(len), NT, 0, sf>>>(rec.p, perm.p, v2.p, len, G, frec.p, fperm.p, ecell.p);
         TDS_CHECK_LAUNCH();
+        fsg_pos.s = sf;
         idx->fsg_ecell = ecell.release();
         idx->fsg_rec = frec.release();
         idx->fsg_perm = fperm.release();
@@ -459,9 +511,15 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         idx->cell_off = off.release();
         idx->n_cells = ncell;
     }
+    for (auto ss : side) {                         // join
+        cudaEvent_t ev = join_event(ss);
+        TDS_CUDA(cudaEventRecord(ev, ss));
+        TDS_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    }
+    bin.s = s;
+    tr.mark("st+fsg");
 
     idx->rec = rec.release();
-    idx->mem_budget = device_budget_bytes();
     idx->perm = perm.release();
     idx->bin_off = bin_off.release();
     idx->bin_lo = bin_lo.release();

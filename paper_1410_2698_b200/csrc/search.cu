@@ -1164,6 +1164,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     if (nq >= (1ull << 31)) fail(TDS_EINVAL, "nq = %llu too large", (unsigned long long)nq);
     Timer &tm = timer_for(s);
     tm.mark(0);
+    Trace tr(s);
     const uint32_t n = (uint32_t)nq;
     // one zeroed header allocation: device stats, per-query counts, redo flags
     const size_t hdr = (sizeof(DevStats) + 4ull * n + n + 15) & ~(size_t)15;
@@ -1262,6 +1263,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         slot_start = DBuf<unsigned long long>(nrows + 1, s);
         exclusive_scan_u64(rl64.p, (uint64_t *)slot_start.p, nrows + 1, (uint64_t *)&dst.p->pair_tests, s);
     }
+    tr.mark("schedule");
     // pair tests bound the result count: size the pass buffer
     DevStats &hs = *pinned_stats();
     TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -1276,7 +1278,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     if (cap == 0) {
         // budget: free device memory plus memory the pools hold unused, measured at
         // index build (cudaMemGetInfo costs up to milliseconds: not per search)
-        uint64_t budget = (uint64_t)(idx->mem_budget * 0.45) / sizeof(Rec);
+        uint64_t budget = (uint64_t)(device_budget_bytes() * 0.45) / sizeof(Rec);
         cap = std::min<uint64_t>(hs.pair_tests + 64, budget);
         cap = std::max<uint64_t>(cap, 1024);
     }
@@ -1305,6 +1307,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     o.redo = redo.p; o.qcount = qcount.p; o.st = dst.p;
 
     // ---- A8-A10: pass 1 --------------------------------------------------------
+    tr.mark("sync+alloc");
     tm.mark(2);
     if (!spatial) {
         RangeArgs a{};
@@ -1327,6 +1330,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         TDS_CHECK_LAUNCH();
     }
     tm.mark(3);
+    tr.mark("pairs");
     TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
     TDS_CUDA(cudaStreamSynchronize(s));
     S.passes = 1;

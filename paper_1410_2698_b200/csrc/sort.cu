@@ -321,53 +321,68 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const uint32_t *__res
     }
 }
 
+constexpr int OS_ROUNDS = 16;                       // keys per thread (onesweep)
+constexpr int OS_TILE = RS_THREADS * OS_ROUNDS;      // 4096 keys per tile
+
+struct __align__(16) OsSmem {
+    uint32_t cnt[RS_WARPS][256];     // per-warp digit counts -> warp offsets in the tile
+    uint32_t tstart[256];            // digit start in the tile-sorted order
+    uint32_t gpos[256];              // global start of this tile's run of digit d
+    uint32_t key[OS_TILE];           // tile staged in digit order
+    uint32_t val[OS_TILE];
+    unsigned tile;
+    uint32_t tot;
+};
+
+// One onesweep pass: rank the tile's keys per digit (warp match + per-warp
+// counts), publish per-digit tile counts and look back over predecessor tiles
+// (decoupled look-back), stage the tile in digit order in shared memory, then
+// write each digit's run to its global position with consecutive threads on
+// consecutive addresses (coalesced).
 __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint32_t *__restrict__ kin,
                                                             const uint32_t *__restrict__ vin,
                                                             uint32_t *__restrict__ kout, uint32_t *__restrict__ vout,
                                                             uint64_t n, int shift, uint32_t mask,
                                                             const uint32_t *__restrict__ ghist,
                                                             uint32_t *status, unsigned *tile_ctr) {
-    __shared__ uint32_t cnt[RS_WARPS][256];
-    __shared__ uint32_t dstart[256];
-    __shared__ unsigned s_tile;
-    __shared__ uint32_t tot_s;
+    extern __shared__ __align__(16) unsigned char os_raw[];
+    OsSmem &S = *reinterpret_cast<OsSmem *>(os_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+    if (threadIdx.x == 0) S.tile = atomicAdd(tile_ctr, 1u);
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&S.cnt[0][0])[i] = 0;
     __syncthreads();
-    const uint32_t tile = s_tile;
+    const uint32_t tile = S.tile;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    uint32_t key[RS_ROUNDS], val[RS_ROUNDS], rank[RS_ROUNDS];
-    int dig[RS_ROUNDS];
-    const uint64_t tbase = (uint64_t)tile * RS_TILE + (uint64_t)w * (32 * RS_ROUNDS);
+    uint32_t key[OS_ROUNDS], val[OS_ROUNDS];
+    uint32_t rank[OS_ROUNDS];
+    const uint64_t tbase = (uint64_t)tile * OS_TILE + (uint64_t)w * (32 * OS_ROUNDS);
 #pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
+    for (int r = 0; r < OS_ROUNDS; ++r) {
         uint64_t k = tbase + (uint64_t)r * 32 + lane;
         bool valid = k < n;
         key[r] = valid ? kin[k] : 0u;
         val[r] = valid ? vin[k] : 0u;
     }
 #pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
+    for (int r = 0; r < OS_ROUNDS; ++r) {
         uint64_t k = tbase + (uint64_t)r * 32 + lane;
         int d = (k < n) ? (int)((key[r] >> shift) & mask) : 256;
-        dig[r] = d;
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t lt = __popc(peers & lt_mask);
-        uint32_t c = (d < 256) ? cnt[w][d] : 0u;
-        rank[r] = c + lt;
+        uint32_t c = (d < 256) ? S.cnt[w][d] : 0u;
+        rank[r] = (d < 256) ? (c + lt) : 0xffffffffu;
         __syncwarp();
-        if (d < 256 && lt == 0) cnt[w][d] = c + __popc(peers);
+        if (d < 256 && lt == 0) S.cnt[w][d] = c + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    // thread = digit: tile count, exclusive over warps, publish, look back
+    // thread = digit: exclusive over warps, tile count, publish, look back
     const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-        uint32_t t = cnt[ww][d];
-        cnt[ww][d] = run;
+        uint32_t t = S.cnt[ww][d];
+        S.cnt[ww][d] = run;
         run += t;
     }
     uint32_t *st = status + (uint64_t)tile * 256 + d;
@@ -376,31 +391,49 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_onesweep(const uint32_t *__re
         atomicExch(st, RS_INC | run);
     } else {
         atomicExch(st, RS_AGG | run);
+        // look back 8 predecessor tiles per step (independent loads in flight)
         int64_t k = (int64_t)tile - 1;
-        while (k >= 0) {
-            uint32_t sv;
-            do { sv = ld_volatile32(status + (uint64_t)k * 256 + d); } while ((sv >> 30) == 0);
-            excl += sv & RS_VAL;
-            if ((sv >> 30) == 2) break;
-            --k;
+        bool done = false;
+        while (!done) {
+            uint32_t sv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sv[j] = (k - j >= 0) ? ld_volatile32(status + (uint64_t)(k - j) * 256 + d)
+                                                          : RS_INC;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (done) break;
+                while ((sv[j] >> 30) == 0) sv[j] = ld_volatile32(status + (uint64_t)(k - j) * 256 + d);
+                excl += sv[j] & RS_VAL;
+                if ((sv[j] >> 30) == 2) done = true;
+            }
+            k -= 8;
         }
         atomicExch(st, RS_INC | (excl + run));
     }
-    // global digit start: exclusive scan of ghist over digits
-    uint32_t g = ghist[d];
-    uint32_t gex = block_excl_scan<uint32_t, RS_THREADS>(g, &tot_s);
-    dstart[d] = gex + excl;
+    const uint32_t tstart = block_excl_scan<uint32_t, RS_THREADS>(run, &S.tot);
+    const uint32_t gex = block_excl_scan<uint32_t, RS_THREADS>(ghist[d], &S.tot);
+    S.tstart[d] = tstart;
+    S.gpos[d] = gex + excl;
     __syncthreads();
+    // stage the tile in digit order
 #pragma unroll
-    for (int ww = 0; ww < RS_WARPS; ++ww) cnt[ww][d] += dstart[d];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
-        if (dig[r] < 256) {
-            uint32_t pos = cnt[w][dig[r]] + rank[r];
-            kout[pos] = key[r];
-            vout[pos] = val[r];
+    for (int r = 0; r < OS_ROUNDS; ++r) {
+        if (rank[r] != 0xffffffffu) {
+            const int dd = (int)((key[r] >> shift) & mask);
+            const uint32_t pos = S.tstart[dd] + S.cnt[w][dd] + rank[r];
+            S.key[pos] = key[r];
+            S.val[pos] = val[r];
         }
+    }
+    __syncthreads();
+    // coalesced write-out: position i of the tile-sorted order
+    const uint64_t tile_n = min((uint64_t)OS_TILE, n - (uint64_t)tile * OS_TILE);
+    for (uint32_t i = threadIdx.x; i < tile_n; i += RS_THREADS) {
+        const uint32_t kk = S.key[i];
+        const int dd = (int)((kk >> shift) & mask);
+        const uint32_t pos = S.gpos[dd] + (i - S.tstart[dd]);
+        kout[pos] = kk;
+        vout[pos] = S.val[i];
     }
 }
 
@@ -432,23 +465,31 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit,
     if (n <= 1 || end_bit <= begin_bit) return;
     if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
     const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    const uint32_t os_tiles = (uint32_t)((n + OS_TILE - 1) / OS_TILE);
     const int npass = (end_bit - begin_bit + 7) / 8;
     DBuf<uint32_t> k2(n, s), v2(n, s);
     uint32_t *ka = keys, *va = vals, *kb = k2.p, *vb = v2.p;
     if (n < (1ull << 30)) {
         // onesweep: 1 upsweep + 1 scatter per digit
-        const uint64_t status_words = (uint64_t)npass * ntiles * 256;
+        const uint64_t status_words = (uint64_t)npass * os_tiles * 256;
+        static bool attr_set = false;
+        if (!attr_set) {
+            TDS_CUDA(cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(OsSmem)));
+            attr_set = true;
+        }
         DBuf<uint32_t> aux(npass * 256 + npass + status_words, s);
         uint32_t *ghist = aux.p, *ctr = aux.p + npass * 256, *status = ctr + npass;
         TDS_CUDA(cudaMemsetAsync(aux.p, 0, 4 * (npass * 256 + npass + status_words), s));
-        unsigned ublk = std::min<unsigned>(ntiles, (unsigned)num_sms() * 4);
+        unsigned ublk = std::min<unsigned>(os_tiles, (unsigned)num_sms() * 4);
         k_rs_upsweep<<<ublk, RS_THREADS, 0, s>>>(keys, n, begin_bit, npass, end_bit, ghist);
         TDS_CHECK_LAUNCH();
         for (int p = 0; p < npass; ++p) {
             int shift = begin_bit + 8 * p;
             int nb = end_bit - shift < 8 ? end_bit - shift : 8;
-            k_rs_onesweep<<<ntiles, RS_THREADS, 0, s>>>(ka, va, kb, vb, n, shift, (1u << nb) - 1u, ghist + 256 * p,
-                                                         status + (uint64_t)p * ntiles * 256, ctr + p);
+            k_rs_onesweep<<<os_tiles, RS_THREADS, sizeof(OsSmem), s>>>(ka, va, kb, vb, n, shift, (1u << nb) - 1u,
+                                                                        ghist + 256 * p,
+                                                                        status + (uint64_t)p * os_tiles * 256, ctr + p);
             TDS_CHECK_LAUNCH();
             std::swap(ka, kb);
             std::swap(va, vb);

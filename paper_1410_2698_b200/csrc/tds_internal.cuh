@@ -175,6 +175,16 @@ void free_index(tds_index_s *idx);
 uint64_t validate_segments(const float4 *rec, uint64_t n, cudaStream_t s);
 
 int num_sms();
+
+// opt-in phase trace (env TDS_TRACE=1): CUDA events on a stream, printed to stderr
+struct Trace {
+    bool on = false;
+    cudaStream_t s = 0;
+    std::vector<std::pair<const char *, cudaEvent_t>> ev;
+    explicit Trace(cudaStream_t s_);
+    void mark(const char *name);
+    ~Trace();
+};
 // free device memory + memory reserved but unused in the default mempool (bytes)
 uint64_t device_budget_bytes();
 
