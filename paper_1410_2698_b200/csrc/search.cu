@@ -34,7 +34,6 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
-constexpr int DIRECT_MIN = 12;           // lanes passing the filter for the in-place fp64 path
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
@@ -102,33 +101,6 @@ __device__ __forceinline__ QConst make_qconst(float4 a, float4 b, float T0, floa
     return q;
 }
 
-// Certified fp32 filter: returns false only if the pair is certainly not within
-// d (shared span empty, or min distance over the span > d).  The computed
-// closest-approach distance differs from the exact one by at most 20 u M
-// (DESIGN.md), M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e - p0e|_1; the test
-// keeps every pair with dist <= d + 64 u M for the fp64 evaluation.
-__device__ __forceinline__ bool filter32(const QConst &q, float4 ea, float4 eb, float d) {
-    float a = fmaxf(q.t0c, ea.w), b = fminf(q.t1c, eb.w);
-    float dex = eb.x - ea.x, dey = eb.y - ea.y, dez = eb.z - ea.z;
-    float r = rcp_approx(eb.w - ea.w);
-    float evx = dex * r, evy = dey * r, evz = dez * r;
-    float aq = a - q.t0, ae = a - ea.w;
-    float dpx = q.px - ea.x, dpy = q.py - ea.y, dpz = q.pz - ea.z;
-    float Dx = fmaf(-ae, evx, fmaf(aq, q.vx, dpx));
-    float Dy = fmaf(-ae, evy, fmaf(aq, q.vy, dpy));
-    float Dz = fmaf(-ae, evz, fmaf(aq, q.vz, dpz));
-    float Vx = q.vx - evx, Vy = q.vy - evy, Vz = q.vz - evz;
-    float L = b - a;
-    float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
-    float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
-    float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);     // NaN (A=B=0) -> 0
-    float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
-    float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
-    float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + q.ext + fabsf(dex) + fabsf(dey) + fabsf(dez);
-    float thr = fmaf(KU, M, d);
-    return (a < b) & (h <= thr * thr);
-}
-
 // candidate-side terms of the filter, computed once per loaded candidate and
 // reused for every query of the group
 struct ECand {
@@ -147,25 +119,58 @@ __device__ __forceinline__ ECand make_ecand(float4 a, float4 b) {
     return e;
 }
 
-// the per-pair part of filter32 (same arithmetic, same certified margin);
-// q0 = (p0, t0), q1 = (v, ext) of the query, [t0c, t1c] its window-clipped span
-__device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
-    float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
-    float aq = a - q0.w, ae = a - e.t0;
-    float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
-    float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
-    float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
-    float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
-    float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
-    float L = b - a;
-    float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
-    float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
-    float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);
-    float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
-    float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
-    float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
-    float thr = fmaf(KU, M, d);
-    return (a < b) & (h <= thr * thr);
+// Certified fp32 classification of one pair.  q0 = (p0, t0),
+// q1 = (v, ext) of the query, [t0c, t1c] its window-clipped span, e the
+// candidate's terms.  Returns
+//   0  certainly not within d (empty span, or closest approach > d + eta),
+//   2  certainly within d, and the fp32 interval [tin, tout] is within its
+//      bound E_t <= 1e-6 * max(b - a, min(|a|, |b|)) of the exact one,
+//   1  undecided: evaluate in fp64 (pair64).
+// eta = 64 u M bounds the fp32 closest-approach error (derived 20 u M), with
+// M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e - p0e|_1 and u = 2^-24.
+__device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
+                                             float &tin, float &tout) {
+    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    const float aq = a - q0.w, ae = a - e.t0;
+    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
+    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
+    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
+    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
+    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
+    const float L = b - a;
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    const float rA = rcp_approx(A);
+    const float su = -B * rA;
+    const float s = fminf(fmaxf(su, 0.f), L);                  // NaN (A = B = 0) -> 0
+    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    const float eta = KU * M;
+    const float thr = d + eta;
+    if (!(a < b) || !(h <= thr * thr)) return 0;
+    const float dl = d - eta;
+    if (!(dl > 0.f) || !(h < dl * dl)) return 1;
+    // certain hit: the interval in fp32 and its error bound
+    const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
+    const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
+    const float d2 = d * d;
+    const float rem = fmaxf(d2 - hu, 0.f);
+    const float w = sqrtf(rem * rA);
+    tin = a + fminf(fmaxf(su - w, 0.f), L);
+    tout = a + fminf(fmaxf(su + w, 0.f), L);
+    const float sqA = sqrtf(A);
+    const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
+    constexpr float U = 1.0f / 16777216.0f;
+    const float Et = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem +
+                     (8.f * U) * w + (4.f * U) * fmaxf(fabsf(a), fabsf(b)) + (2.f * U) * L;
+    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b)));
+    return (Et <= tol) ? 2 : 1;                                 // NaN bounds -> fp64
+}
+
+__device__ __forceinline__ int classify32(const QConst &q, float4 ea, float4 eb, float d, float &tin, float &tout) {
+    return classify_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c,
+                         make_ecand(ea, eb), d, tin, tout);
 }
 
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
@@ -337,29 +342,6 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
     __syncwarp();
     if (lane == 0) { W->refined += n; W->hits += __popc(hm); }
     __syncwarp();
-}
-
-// warp-wide dense path: when most lanes passed the filter for the same query,
-// evaluate in place (no queue round trip); returns the number of hits (all
-// belong to query `qid`, counted by the caller's owner lane).
-template <bool EXACT>
-__device__ __forceinline__ uint32_t refine_direct(const PairCtx *C, WarpState *W, bool m, uint32_t qid, uint32_t j,
-                                                  int lane) {
-    float tin = 0.f, tout = 0.f;
-    bool hit = false;
-    if (m)
-        hit = pair64(__ldg(C->Q + 2 * (uint64_t)qid), __ldg(C->Q + 2 * (uint64_t)qid + 1),
-                     __ldg(C->rec + 2 * (uint64_t)j), __ldg(C->rec + 2 * (uint64_t)j + 1), (double)C->d,
-                     (double)C->T0, (double)C->T1, tin, tout);
-    const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
-    Rec r{qid, eid, tin, tout};
-    append<EXACT>(C->o, *W, hit, r, lane);
-    const unsigned hm = __ballot_sync(FULL, hit);
-    const unsigned mm = __ballot_sync(FULL, m);
-    __syncwarp();
-    if (lane == 0) { W->refined += __popc(mm); W->hits += __popc(hm); }
-    __syncwarp();
-    return __popc(hm);
 }
 
 // warp-wide: queue the pairs whose fp32 filter passed (no flush here)
@@ -637,7 +619,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     const float d = A.pc.d;
     warp_state_init(W.ws, lane);
     uint32_t qn = 0;
-    unsigned long long exec = 0;
+    unsigned long long exec = 0, direct_hits = 0;
     while (true) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
@@ -713,22 +695,28 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
                 const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                const bool m0 = v0 && c0 >= glo && c0 < ghi && filter_pair(q0, q1, q2.x, q2.y, e0, d);
-                const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
-                if (!__any_sync(FULL, m0 | m1)) continue;
+                float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
+                const int k0 = (v0 && c0 >= glo && c0 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e0, d, ti0, to0) : 0;
+                const int k1 = (v1 && c1 >= glo && c1 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e1, d, ti1, to1) : 0;
+                if (!__any_sync(FULL, (k0 | k1) != 0)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                // dense windows (most lanes passed): evaluate in place; sparse: queue
                 uint32_t hits_g = 0;
-                if (__popc(__ballot_sync(FULL, m0)) >= DIRECT_MIN) {
-                    hits_g += refine_direct<EXACT>(&A.pc, &W.ws, m0, qid, j0, lane);
-                } else {
-                    queue_add(W.ws, qn, m0, qid, j0, lane);
+                // certain hits: fp32 interval, appended directly
+                const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
+                if (hm0) {
+                    Rec r{qid, k0 == 2 ? __ldg(A.pc.perm + j0) : 0u, ti0, to0};
+                    append<EXACT>(A.pc.o, W.ws, k0 == 2, r, lane);
+                    hits_g += __popc(hm0);
                 }
-                if (__popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
-                    hits_g += refine_direct<EXACT>(&A.pc, &W.ws, m1, qid, j1, lane);
-                } else {
-                    queue_add(W.ws, qn, m1, qid, j1, lane);
+                if (hm1) {
+                    Rec r{qid, k1 == 2 ? __ldg(A.pc.perm + j1) : 0u, ti1, to1};
+                    append<EXACT>(A.pc.o, W.ws, k1 == 2, r, lane);
+                    hits_g += __popc(hm1);
                 }
+                direct_hits += hits_g;
+                // undecided: queue for fp64
+                queue_add(W.ws, qn, k0 == 1, qid, j0, lane);
+                queue_add(W.ws, qn, k1 == 1, qid, j1, lane);
                 if (lane == g) owner_hits += hits_g;
                 queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
             }
@@ -739,6 +727,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     if (qn) flush_refine<EXACT>(&A.pc, &W.ws, qn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
+    if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
 }
 
 // ---------------------------------------------------------------------------
@@ -873,7 +862,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     const unsigned long long total = A.slot_start[A.nrows];
     warp_state_init(W, lane);
     uint32_t qn = 0;
-    unsigned long long exec = 0;
+    unsigned long long exec = 0, direct_hits = 0;
     uint32_t cur_p = 0xffffffffu;
     uint32_t cur_qrow = 0;
     QConst q = make_qconst(make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 1.f), A.pc.T0, A.pc.T1);
@@ -924,7 +913,8 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
             }
 #pragma unroll
             for (int u = 0; u < SB; ++u) {
-                bool maybe = false;
+                int kk = 0;
+                float ti = 0.f, to = 0.f;
                 if (vv[u]) {
                     if (pp[u] != cur_p) {
                         cur_p = pp[u];
@@ -939,9 +929,20 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
                     const int rz = max((int)(m0 & 0x3ffu), qlo.z);
                     const bool first = pack_cell(rx, ry, rz) == cxy[u];
-                    maybe = first && filter32(q, ea[u], eb[u], A.pc.d);
+                    if (first) kk = classify32(q, ea[u], eb[u], A.pc.d, ti, to);
                 }
-                queue_add(W, qn, maybe, cur_qrow, ii[u], lane);
+                // certain hits: fp32 interval appended directly; undecided: fp64 queue
+                const unsigned hm = __ballot_sync(FULL, kk == 2);
+                if (hm) {
+                    Rec rr{cur_qrow, kk == 2 ? __ldg(A.pc.perm + ii[u]) : 0u, ti, to};
+                    append<EXACT>(A.pc.o, W, kk == 2, rr, lane);
+                    if (kk == 2) {
+                        const unsigned peers = __match_any_sync(hm, cur_qrow);
+                        if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&A.pc.o.qcount[cur_qrow], (uint32_t)__popc(peers));
+                    }
+                    direct_hits += __popc(hm);
+                }
+                queue_add(W, qn, kk == 1, cur_qrow, ii[u], lane);
             }
             queue_drain<EXACT>(&A.pc, W, qn, lane);
         }
@@ -949,6 +950,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
     warp_state_finish<EXACT>(A.pc.o, W, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
+    if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
 }
 
 // ---------------------------------------------------------------------------
