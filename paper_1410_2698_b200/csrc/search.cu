@@ -121,15 +121,41 @@ __device__ __forceinline__ ECand make_ecand(float4 a, float4 b) {
 
 // Certified fp32 classification of one pair.  q0 = (p0, t0),
 // q1 = (v, ext) of the query, [t0c, t1c] its window-clipped span, e the
-// candidate's terms.  Returns
-//   0  certainly not within d (empty span, or closest approach > d + eta),
-//   2  certainly within d, and the fp32 interval [tin, tout] is within its
-//      bound E_t <= 1e-6 * max(b - a, min(|a|, |b|)) of the exact one,
-//   1  undecided: evaluate in fp64 (pair64).
-// eta = 64 u M bounds the fp32 closest-approach error (derived 20 u M), with
-// M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e - p0e|_1 and u = 2^-24.
-__device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
-                                             float &tin, float &tout) {
+// candidate's terms.  Returns 0 if certainly not within d (empty span, or
+// closest approach > d + eta), 2 if certainly within d (closest approach
+// < d - eta), 1 if undecided (evaluate in fp64).  eta = 64 u M bounds the fp32
+// closest-approach error (derived 20 u M), M = |p0q - p0e|_1 + |p1q - p0q|_1 +
+// |p1e - p0e|_1, u = 2^-24.
+__device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
+    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    const float aq = a - q0.w, ae = a - e.t0;
+    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
+    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
+    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
+    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
+    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
+    const float L = b - a;
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    const float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);  // NaN (A = B = 0) -> 0
+    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    const float eta = KU * M;
+    const float thr = d + eta, dl = d - eta;
+    if (!(a < b) || !(h <= thr * thr)) return 0;
+    return (dl > 0.f && h < dl * dl) ? 2 : 1;
+}
+
+// The interval [tin, tout] of a certainly-hitting pair in fp32 (same arithmetic
+// as classify_pair up to the unclamped minimiser s_u), with a first-order error
+// bound: |d s_u| <= 12 u M / sqrt(A) (rounding of D.V, A, the reciprocal),
+// |d w| <= w (d rem / 2 rem + 6 u V1 / sqrt(A) + 4 u) with d rem <= 40 u d M +
+// 2 u d^2 (closest-approach error, rounding of d^2), V1 = |vq|_1 + |ve|_1; an
+// end that is certainly clamped to a or b is exact.  Returns false (use fp64)
+// unless every unclamped end is within 1e-6 * max(b - a, min(|a|, |b|)).
+__device__ __forceinline__ bool interval_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
+                                              float &tin, float &tout) {
     const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
     const float aq = a - q0.w, ae = a - e.t0;
     const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
@@ -142,35 +168,32 @@ __device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, fl
     const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
     const float rA = rcp_approx(A);
     const float su = -B * rA;
-    const float s = fminf(fmaxf(su, 0.f), L);                  // NaN (A = B = 0) -> 0
-    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
-    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
-    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
-    const float eta = KU * M;
-    const float thr = d + eta;
-    if (!(a < b) || !(h <= thr * thr)) return 0;
-    const float dl = d - eta;
-    if (!(dl > 0.f) || !(h < dl * dl)) return 1;
-    // certain hit: the interval in fp32 and its error bound
     const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
     const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
     const float d2 = d * d;
     const float rem = fmaxf(d2 - hu, 0.f);
     const float w = sqrtf(rem * rA);
-    tin = a + fminf(fmaxf(su - w, 0.f), L);
-    tout = a + fminf(fmaxf(su + w, 0.f), L);
-    const float sqA = sqrtf(A);
+    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
     const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
     constexpr float U = 1.0f / 16777216.0f;
-    const float Et = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem +
-                     (8.f * U) * w + (4.f * U) * fmaxf(fabsf(a), fabsf(b)) + (2.f * U) * L;
-    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b)));
-    return (Et <= tol) ? 2 : 1;                                 // NaN bounds -> fp64
+    const float sqA = sqrtf(A);
+    const float dst = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem + (8.f * U) * w;
+    const float lo = su - w, hi = su + w;
+    tin = a + fminf(fmaxf(lo, 0.f), L);
+    tout = a + fminf(fmaxf(hi, 0.f), L);
+    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b))) - (4.f * U) * fmaxf(fabsf(a), fabsf(b)) - 2.f * U * L;
+    const bool in_ok = (lo + dst < 0.f) || (dst <= tol);       // clamped to a for sure, or accurate
+    const bool out_ok = (hi - dst > L) || (dst <= tol);        // clamped to b for sure, or accurate
+    return in_ok && out_ok;                                     // NaN -> false -> fp64
 }
 
-__device__ __forceinline__ int classify32(const QConst &q, float4 ea, float4 eb, float d, float &tin, float &tout) {
-    return classify_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c,
-                         make_ecand(ea, eb), d, tin, tout);
+__device__ __forceinline__ int classify32(const QConst &q, const ECand &e, float d) {
+    return classify_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c, e, d);
+}
+
+__device__ __forceinline__ bool interval32(const QConst &q, const ECand &e, float d, float &tin, float &tout) {
+    return interval_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c, e,
+                         d, tin, tout);
 }
 
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
@@ -695,13 +718,15 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
                 const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
-                const int k0 = (v0 && c0 >= glo && c0 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e0, d, ti0, to0) : 0;
-                const int k1 = (v1 && c1 >= glo && c1 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e1, d, ti1, to1) : 0;
+                int k0 = (v0 && c0 >= glo && c0 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e0, d) : 0;
+                int k1 = (v1 && c1 >= glo && c1 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e1, d) : 0;
                 if (!__any_sync(FULL, (k0 | k1) != 0)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 uint32_t hits_g = 0;
-                // certain hits: fp32 interval, appended directly
+                // certain hits: fp32 interval when its error bound allows, appended directly
+                float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
+                if (k0 == 2 && !interval_pair(q0, q1, q2.x, q2.y, e0, d, ti0, to0)) k0 = 1;
+                if (k1 == 2 && !interval_pair(q0, q1, q2.x, q2.y, e1, d, ti1, to1)) k1 = 1;
                 const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
                 if (hm0) {
                     Rec r{qid, k0 == 2 ? __ldg(A.pc.perm + j0) : 0u, ti0, to0};
@@ -929,7 +954,11 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
                     const int rz = max((int)(m0 & 0x3ffu), qlo.z);
                     const bool first = pack_cell(rx, ry, rz) == cxy[u];
-                    if (first) kk = classify32(q, ea[u], eb[u], A.pc.d, ti, to);
+                    if (first) {
+                        const ECand ec = make_ecand(ea[u], eb[u]);
+                        kk = classify32(q, ec, A.pc.d);
+                        if (kk == 2 && !interval32(q, ec, A.pc.d, ti, to)) kk = 1;
+                    }
                 }
                 // certain hits: fp32 interval appended directly; undecided: fp64 queue
                 const unsigned hm = __ballot_sync(FULL, kk == 2);
