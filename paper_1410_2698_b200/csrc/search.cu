@@ -35,6 +35,7 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
+constexpr int DIRECT_MIN = 16;           // filter passes per 64-candidate window for the in-place path
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
 // (derived bound 20 u M, u = 2^-24; 64 u used)
@@ -143,8 +144,30 @@ __device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, fl
     const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
     const float eta = KU * M;
     const float thr = d + eta, dl = d - eta;
-    if (!(a < b) || !(h <= thr * thr)) return 0;
-    return (dl > 0.f && h < dl * dl) ? 2 : 1;
+    const bool in = (a < b) & (h <= thr * thr);                // branch-free
+    const bool sure = (dl > 0.f) & (h < dl * dl);
+    return (int)in + (int)(in & sure);
+}
+
+// The hot-loop filter: true unless the pair is certainly not within d (same
+// arithmetic as classify_pair, branch-free bool).
+__device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
+    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    const float aq = a - q0.w, ae = a - e.t0;
+    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
+    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
+    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
+    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
+    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
+    const float L = b - a;
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    const float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);
+    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    const float thr = fmaf(KU, M, d);
+    return (a < b) & (h <= thr * thr);
 }
 
 // The interval [tin, tout] of a certainly-hitting pair in fp32 (same arithmetic
@@ -185,6 +208,47 @@ __device__ __forceinline__ bool interval_pair(float4 q0, float4 q1, float t0c, f
     const bool in_ok = (lo + dst < 0.f) || (dst <= tol);       // clamped to a for sure, or accurate
     const bool out_ok = (hi - dst > L) || (dst <= tol);        // clamped to b for sure, or accurate
     return in_ok && out_ok;                                     // NaN -> false -> fp64
+}
+
+// For a pair that passed filter_pair: 2 = certain hit (closest approach < d -
+// eta) with an accurate fp32 interval in [tin, tout]; 1 = evaluate in fp64.
+// One pass of the arithmetic of classify_pair + interval_pair.
+__device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
+                                        float &tin, float &tout) {
+    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    const float aq = a - q0.w, ae = a - e.t0;
+    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
+    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
+    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
+    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
+    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
+    const float L = b - a;
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    const float rA = rcp_approx(A);
+    const float su = -B * rA;
+    const float s = fminf(fmaxf(su, 0.f), L);
+    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    const float dl = d - KU * M;
+    if (!(dl > 0.f) || !(h < dl * dl)) return 1;
+    const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
+    const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
+    const float d2 = d * d;
+    const float rem = fmaxf(d2 - hu, 0.f);
+    const float w = sqrtf(rem * rA);
+    const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
+    constexpr float U = 1.0f / 16777216.0f;
+    const float sqA = sqrtf(A);
+    const float dst = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem + (8.f * U) * w;
+    const float lo = su - w, hi = su + w;
+    tin = a + fminf(fmaxf(lo, 0.f), L);
+    tout = a + fminf(fmaxf(hi, 0.f), L);
+    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b))) - (4.f * U) * fmaxf(fabsf(a), fabsf(b)) - 2.f * U * L;
+    const bool in_ok = (lo + dst < 0.f) || (dst <= tol);
+    const bool out_ok = (hi - dst > L) || (dst <= tol);
+    return (in_ok && out_ok) ? 2 : 1;
 }
 
 __device__ __forceinline__ int classify32(const QConst &q, const ECand &e, float d) {
@@ -350,20 +414,33 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
     const bool v = (uint32_t)lane < n;
     const uint32_t q = v ? W->rq[lane] : 0u, j = v ? W->rj[lane] : 0u;
     float tin = 0.f, tout = 0.f;
-    bool hit = false;
-    if (v)
-        hit = pair64(__ldg(C->Q + 2 * (uint64_t)q), __ldg(C->Q + 2 * (uint64_t)q + 1), __ldg(C->rec + 2 * (uint64_t)j),
-                     __ldg(C->rec + 2 * (uint64_t)j + 1), (double)C->d, (double)C->T0, (double)C->T1, tin, tout);
+    bool hit = false, need64 = false;
+    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f), ea = qa, eb = qb;
+    if (v) {
+        qa = __ldg(C->Q + 2 * (uint64_t)q);
+        qb = __ldg(C->Q + 2 * (uint64_t)q + 1);
+        ea = __ldg(C->rec + 2 * (uint64_t)j);
+        eb = __ldg(C->rec + 2 * (uint64_t)j + 1);
+        // certain hit with an accurate fp32 interval, else fp64
+        const QConst qc = make_qconst(qa, qb, C->T0, C->T1);
+        const int k = hit_kind(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext),
+                               qc.t0c, qc.t1c, make_ecand(ea, eb), C->d, tin, tout);
+        hit = (k == 2);
+        need64 = !hit;
+    }
+    if (__any_sync(FULL, need64) && need64)
+        hit = pair64(qa, qb, ea, eb, (double)C->d, (double)C->T0, (double)C->T1, tin, tout);
     const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
     Rec r{q, eid, tin, tout};
     append<EXACT>(C->o, *W, hit, r, lane);
     const unsigned hm = __ballot_sync(FULL, hit);
+    const unsigned m64 = __ballot_sync(FULL, need64);
     if (hit) {   // per-query counts, aggregated over the lanes of the same query
         const unsigned peers = __match_any_sync(hm, q);
         if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&C->o.qcount[q], (uint32_t)__popc(peers));
     }
     __syncwarp();
-    if (lane == 0) { W->refined += n; W->hits += __popc(hm); }
+    if (lane == 0) { W->refined += __popc(m64); W->hits += __popc(hm); }
     __syncwarp();
 }
 
@@ -618,9 +695,46 @@ struct RangeArgs {
     uint32_t ntiles;
 };
 
+// Pairs of query qid that passed the fp32 filter (lane's candidates j0, j1):
+// certain hits with an accurate fp32 interval are appended; the rest is queued
+// for fp64.  Out of line: the hit path must not cost the pair loop registers.
+// Returns the number of hits appended here.
+template <bool EXACT>
+__device__ __forceinline__ uint32_t handle_passed(const PairCtx *C, WarpState *W, uint32_t *qn_io, bool m0, bool m1,
+                                               float4 q0, float4 q1, float t0c, float t1c, uint32_t qid, uint32_t j0,
+                                               uint32_t j1, const ECand &e0, const ECand &e1) {
+    const int lane = threadIdx.x & 31;
+    const float d = C->d;
+    float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
+    int k0 = 0, k1 = 0;
+    if (m0) k0 = hit_kind(q0, q1, t0c, t1c, e0, d, ti0, to0);
+    if (m1) k1 = hit_kind(q0, q1, t0c, t1c, e1, d, ti1, to1);
+    uint32_t hits = 0;
+    const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
+    if (hm0) {
+        Rec r{qid, k0 == 2 ? __ldg(C->perm + j0) : 0u, ti0, to0};
+        append<EXACT>(C->o, *W, k0 == 2, r, lane);
+        hits += __popc(hm0);
+    }
+    if (hm1) {
+        Rec r{qid, k1 == 2 ? __ldg(C->perm + j1) : 0u, ti1, to1};
+        append<EXACT>(C->o, *W, k1 == 2, r, lane);
+        hits += __popc(hm1);
+    }
+    uint32_t qn = *qn_io;
+    queue_add(*W, qn, k0 == 1, qid, j0, lane);
+    queue_add(*W, qn, k1 == 1, qid, j1, lane);
+    queue_drain<EXACT>(C, *W, qn, lane);
+    __syncwarp();
+    if (lane == 0) *qn_io = qn;
+    __syncwarp();
+    return hits;
+}
+
 struct __align__(16) RangeWarpSmem {
     float4 q[32][3];                 // group query constants: (p0,t0) (v,ext) (t0c,t1c,lo,hi)
     WarpState ws;
+    uint32_t qn;                     // refine queue fill
 };
 
 // Mapping: a work item is a group of <= 32
@@ -641,7 +755,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     const uint32_t CH = st->ch;
     const float d = A.pc.d;
     warp_state_init(W.ws, lane);
-    uint32_t qn = 0;
+    if (lane == 0) W.qn = 0;
+    __syncwarp();
     unsigned long long exec = 0, direct_hits = 0;
     while (true) {
         uint32_t item = 0;
@@ -718,38 +833,33 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
                 const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                int k0 = (v0 && c0 >= glo && c0 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e0, d) : 0;
-                int k1 = (v1 && c1 >= glo && c1 < ghi) ? classify_pair(q0, q1, q2.x, q2.y, e1, d) : 0;
-                if (!__any_sync(FULL, (k0 | k1) != 0)) continue;
+                const bool m0 = v0 && c0 >= glo && c0 < ghi && filter_pair(q0, q1, q2.x, q2.y, e0, d);
+                const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
+                if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                uint32_t hits_g = 0;
-                // certain hits: fp32 interval when its error bound allows, appended directly
-                float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
-                if (k0 == 2 && !interval_pair(q0, q1, q2.x, q2.y, e0, d, ti0, to0)) k0 = 1;
-                if (k1 == 2 && !interval_pair(q0, q1, q2.x, q2.y, e1, d, ti1, to1)) k1 = 1;
-                const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
-                if (hm0) {
-                    Rec r{qid, k0 == 2 ? __ldg(A.pc.perm + j0) : 0u, ti0, to0};
-                    append<EXACT>(A.pc.o, W.ws, k0 == 2, r, lane);
-                    hits_g += __popc(hm0);
+                if (__popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
+                    // dense: most lanes passed -> in place (fp32 interval or fp64 queue)
+                    const uint32_t hits_g =
+                        handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, m0, m1, q0, q1, q2.x, q2.y, qid, j0, j1, e0, e1);
+                    direct_hits += hits_g;
+                    if (lane == g) owner_hits += hits_g;
+                } else {
+                    // sparse: queue; the flush evaluates 32 at a time with every lane busy
+                    uint32_t qn = W.qn;
+                    queue_add(W.ws, qn, m0, qid, j0, lane);
+                    queue_add(W.ws, qn, m1, qid, j1, lane);
+                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
+                    __syncwarp();
+                    if (lane == 0) W.qn = qn;
+                    __syncwarp();
                 }
-                if (hm1) {
-                    Rec r{qid, k1 == 2 ? __ldg(A.pc.perm + j1) : 0u, ti1, to1};
-                    append<EXACT>(A.pc.o, W.ws, k1 == 2, r, lane);
-                    hits_g += __popc(hm1);
-                }
-                direct_hits += hits_g;
-                // undecided: queue for fp64
-                queue_add(W.ws, qn, k0 == 1, qid, j0, lane);
-                queue_add(W.ws, qn, k1 == 1, qid, j1, lane);
-                if (lane == g) owner_hits += hits_g;
-                queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
             }
             base = cend;
         }
         if (owner_hits) atomicAdd(&A.pc.o.qcount[S.qid], owner_hits);
     }
-    if (qn) flush_refine<EXACT>(&A.pc, &W.ws, qn);
+    __syncwarp();
+    if (W.qn) flush_refine<EXACT>(&A.pc, &W.ws, W.qn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
     if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
@@ -939,7 +1049,6 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
 #pragma unroll
             for (int u = 0; u < SB; ++u) {
                 int kk = 0;
-                float ti = 0.f, to = 0.f;
                 if (vv[u]) {
                     if (pp[u] != cur_p) {
                         cur_p = pp[u];
@@ -954,23 +1063,11 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
                     const int rz = max((int)(m0 & 0x3ffu), qlo.z);
                     const bool first = pack_cell(rx, ry, rz) == cxy[u];
-                    if (first) {
-                        const ECand ec = make_ecand(ea[u], eb[u]);
-                        kk = classify32(q, ec, A.pc.d);
-                        if (kk == 2 && !interval32(q, ec, A.pc.d, ti, to)) kk = 1;
-                    }
+                    if (first) kk = filter_pair(make_float4(q.px, q.py, q.pz, q.t0),
+                                                make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c,
+                                                make_ecand(ea[u], eb[u]), A.pc.d) ? 1 : 0;
                 }
-                // certain hits: fp32 interval appended directly; undecided: fp64 queue
-                const unsigned hm = __ballot_sync(FULL, kk == 2);
-                if (hm) {
-                    Rec rr{cur_qrow, kk == 2 ? __ldg(A.pc.perm + ii[u]) : 0u, ti, to};
-                    append<EXACT>(A.pc.o, W, kk == 2, rr, lane);
-                    if (kk == 2) {
-                        const unsigned peers = __match_any_sync(hm, cur_qrow);
-                        if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&A.pc.o.qcount[cur_qrow], (uint32_t)__popc(peers));
-                    }
-                    direct_hits += __popc(hm);
-                }
+                // passes are queued; the flush classifies (fp32 interval or fp64) 32 at a time
                 queue_add(W, qn, kk == 1, cur_qrow, ii[u], lane);
             }
             queue_drain<EXACT>(&A.pc, W, qn, lane);
