@@ -241,7 +241,18 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
     constexpr float U = 1.0f / 16777216.0f;
     const float sqA = sqrtf(A);
-    const float dst = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem + (8.f * U) * w;
+    // s_u may lie far outside [0, L]: magnitudes along the line up to |s_u| enter M_u,
+    // and the relative errors of A and of the reciprocal scale |s_u| and w
+    // first-order bounds: |dDa| <= 11 u M_u, |dDV| <= 6 u V1,
+    // s_u = -(Da.DV)/A -> |ds_u| <= 14 u M_u/sqrt(A) + 6 u V1 M_u/A + |s_u| (dA/A + 2u);
+    // rem = d^2 - h_u -> |drem| <= 2 d 14 u M_u + A ds_u^2 + 2 u (d^2 + rem)
+    const float Su = fmaxf(fabsf(su), L);
+    const float Mu = M + Su * V1;
+    const float relA = (12.f * U) * V1 / sqA + 5.f * U;
+    const float dsu = (14.f * U) * Mu / sqA + (6.f * U) * V1 * Mu * rA + fabsf(su) * relA;
+    const float drem = (28.f * U) * d * Mu + A * dsu * dsu + (2.f * U) * (d2 + rem);
+    const float dw = w * (drem / (2.f * rem) + 0.5f * relA + 2.f * U);
+    const float dst = 2.f * (dsu + dw);                         // x2 safety
     const float lo = su - w, hi = su + w;
     tin = a + fminf(fmaxf(lo, 0.f), L);
     tout = a + fminf(fmaxf(hi, 0.f), L);

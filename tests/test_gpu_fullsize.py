@@ -34,9 +34,17 @@ def _search_sampled(idx, Qd, d, kind, sel, capacity=0):
     n = r.count
     st = r.stats()
     q, e, ti, to = r.fetch(device=True)
-    h = int(_mix(q, e).sum().item()) & ((1 << 64) - 1)
-    m = torch.isin(q, torch.as_tensor(sel, dtype=torch.int32, device=q.device))
-    got = tuple(x[m].cpu().numpy() for x in (q, e, ti, to))
+    lut = torch.zeros(Qd.shape[0], dtype=torch.bool, device=q.device)
+    lut[torch.as_tensor(sel, device=q.device)] = True
+    h = 0
+    parts = []
+    CH = 1 << 27                      # chunked: the dense point has ~2.5e9 records
+    for a in range(0, n, CH):
+        qa, ea = q[a:a + CH], e[a:a + CH]
+        h = (h + int(_mix(qa, ea).sum().item())) & ((1 << 64) - 1)
+        m = lut[qa]
+        parts.append(tuple(x[a:a + CH][m].cpu().numpy() for x in (q, e, ti, to)))
+    got = tuple(np.concatenate([p_[k] for p_ in parts]) if parts else np.zeros(0) for k in range(4))
     r.close()
     del q, e, ti, to
     torch.cuda.empty_cache()
