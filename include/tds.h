@@ -118,7 +118,9 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
  *
  *   kind      : TDS_TEMPORAL, TDS_SPATIAL or TDS_SPATIOTEMPORAL (must have been built)
  *   queries   : nq segments (device or host memory); nq == 0 gives an empty result
- *   d         : distance threshold, finite and > 0 ("within d" is <= d, reading C4)
+ *   d         : distance threshold, finite and > 0 ("within d" is <= d, reading C4); a double:
+ *               the hit decision and interval are exact for this d (fp32 filters use d
+ *               rounded up, which only adds candidates)
  *   t_start, t_end : query window [T0, T1]; pass -INFINITY / +INFINITY for none
  *   capacity  : records the pass buffer holds (the paper's fixed result buffer);
  *               0 = automatic.  When a pass overflows, the records of the queries that
@@ -129,7 +131,7 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
  * Errors: TDS_EINVAL, TDS_EDATA (bad query segment), TDS_ENOMEM, TDS_ECAPACITY, TDS_ECUDA.
  * Synchronises stream (one host synchronisation per pass).
  */
-int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, float d,
+int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d,
                float t_start, float t_end, uint64_t capacity, void *stream,
                tds_result *out, uint64_t *n_results);
 

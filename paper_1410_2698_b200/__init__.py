@@ -69,7 +69,7 @@ def load_library(path: str = LIB_PATH):
     lib = ctypes.CDLL(path)
     vp, u64, i32, f32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_float
     lib.tds_build_index.argtypes = [vp, u64, ctypes.POINTER(_Params), vp, ctypes.POINTER(vp)]
-    lib.tds_search.argtypes = [vp, i32, vp, u64, f32, f32, f32, u64, vp, ctypes.POINTER(vp),
+    lib.tds_search.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, vp, ctypes.POINTER(vp),
                                ctypes.POINTER(u64)]
     lib.tds_fetch_results.argtypes = [vp, u64, u64, vp, vp, vp, vp, i32, i32, vp]
     lib.tds_result_stats.argtypes = [vp, ctypes.POINTER(_Stats)]

@@ -270,7 +270,7 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
     ABI_CATCH
 }
 
-int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, float d, float t_start, float t_end,
+int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
                uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results) {
     ABI_TRY
     tds::set_error(0, "");
@@ -279,7 +279,7 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, flo
     if (kind != TDS_TEMPORAL && kind != TDS_SPATIAL && kind != TDS_SPATIOTEMPORAL)
         fail(TDS_EINVAL, "kind = %d is not one of TDS_TEMPORAL/SPATIAL/SPATIOTEMPORAL", kind);
     if (!(idx->kinds & (uint32_t)kind)) fail(TDS_EINVAL, "index was not built for kind %d", kind);
-    if (!(d > 0.f) || !isfinite(d)) fail(TDS_EINVAL, "d = %g must be finite and > 0", (double)d);
+    if (!(d > 0.0) || !isfinite(d) || d > 3.0e38) fail(TDS_EINVAL, "d = %g must be finite and > 0", d);
     if (isnan(t_start) || isnan(t_end) || t_start > t_end) fail(TDS_EINVAL, "bad window [%g, %g]",
                                                                (double)t_start, (double)t_end);
     cudaStream_t s = (cudaStream_t)stream;

@@ -120,37 +120,11 @@ __device__ __forceinline__ ECand make_ecand(float4 a, float4 b) {
     return e;
 }
 
-// Certified fp32 classification of one pair.  q0 = (p0, t0),
-// q1 = (v, ext) of the query, [t0c, t1c] its window-clipped span, e the
-// candidate's terms.  Returns 0 if certainly not within d (empty span, or
-// closest approach > d + eta), 2 if certainly within d (closest approach
-// < d - eta), 1 if undecided (evaluate in fp64).  eta = 64 u M bounds the fp32
-// closest-approach error (derived 20 u M), M = |p0q - p0e|_1 + |p1q - p0q|_1 +
-// |p1e - p0e|_1, u = 2^-24.
-__device__ __forceinline__ int classify_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
-    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
-    const float aq = a - q0.w, ae = a - e.t0;
-    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
-    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
-    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
-    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
-    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
-    const float L = b - a;
-    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
-    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
-    const float s = fminf(fmaxf(-B * rcp_approx(A), 0.f), L);  // NaN (A = B = 0) -> 0
-    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
-    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
-    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
-    const float eta = KU * M;
-    const float thr = d + eta, dl = d - eta;
-    const bool in = (a < b) & (h <= thr * thr);                // branch-free
-    const bool sure = (dl > 0.f) & (h < dl * dl);
-    return (int)in + (int)(in & sure);
-}
-
-// The hot-loop filter: true unless the pair is certainly not within d (same
-// arithmetic as classify_pair, branch-free bool).
+// The hot-loop filter (certified): false only if the pair is
+// certainly not within d — empty shared span, or fp32 closest approach > d + eta
+// with eta = 64 u M >= the derived error bound 20 u M, M = |p0q - p0e|_1 +
+// |p1q - p0q|_1 + |p1e - p0e|_1, u = 2^-24.  q0 = (p0, t0), q1 = (v, ext) of the
+// query, [t0c, t1c] its window-clipped span, e the candidate's terms.
 __device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d) {
     const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
     const float aq = a - q0.w, ae = a - e.t0;
@@ -170,49 +144,11 @@ __device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, flo
     return (a < b) & (h <= thr * thr);
 }
 
-// The interval [tin, tout] of a certainly-hitting pair in fp32 (same arithmetic
-// as classify_pair up to the unclamped minimiser s_u), with a first-order error
-// bound: |d s_u| <= 12 u M / sqrt(A) (rounding of D.V, A, the reciprocal),
-// |d w| <= w (d rem / 2 rem + 6 u V1 / sqrt(A) + 4 u) with d rem <= 40 u d M +
-// 2 u d^2 (closest-approach error, rounding of d^2), V1 = |vq|_1 + |ve|_1; an
-// end that is certainly clamped to a or b is exact.  Returns false (use fp64)
-// unless every unclamped end is within 1e-6 * max(b - a, min(|a|, |b|)).
-__device__ __forceinline__ bool interval_pair(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
-                                              float &tin, float &tout) {
-    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
-    const float aq = a - q0.w, ae = a - e.t0;
-    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
-    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
-    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
-    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
-    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
-    const float L = b - a;
-    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
-    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
-    const float rA = rcp_approx(A);
-    const float su = -B * rA;
-    const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
-    const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    const float d2 = d * d;
-    const float rem = fmaxf(d2 - hu, 0.f);
-    const float w = sqrtf(rem * rA);
-    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
-    const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
-    constexpr float U = 1.0f / 16777216.0f;
-    const float sqA = sqrtf(A);
-    const float dst = (12.f * U) * (M + V1 * w) / sqA + w * ((40.f * U) * d * M + (2.f * U) * d2) / rem + (8.f * U) * w;
-    const float lo = su - w, hi = su + w;
-    tin = a + fminf(fmaxf(lo, 0.f), L);
-    tout = a + fminf(fmaxf(hi, 0.f), L);
-    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b))) - (4.f * U) * fmaxf(fabsf(a), fabsf(b)) - 2.f * U * L;
-    const bool in_ok = (lo + dst < 0.f) || (dst <= tol);       // clamped to a for sure, or accurate
-    const bool out_ok = (hi - dst > L) || (dst <= tol);        // clamped to b for sure, or accurate
-    return in_ok && out_ok;                                     // NaN -> false -> fp64
-}
-
-// For a pair that passed filter_pair: 2 = certain hit (closest approach < d -
-// eta) with an accurate fp32 interval in [tin, tout]; 1 = evaluate in fp64.
-// One pass of the arithmetic of classify_pair + interval_pair.
+// For a pair that passed filter_pair: 2 = certain hit (fp32 closest approach
+// < d - eta) whose fp32 interval [tin, tout] is within its first-order error
+// bound of the exact one, the bound being <= 1e-6 * max(b - a, min(|a|, |b|))
+// for every end not certainly clamped to a or b (clamped ends are exact);
+// 1 = evaluate in fp64 (pair64).
 __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
                                         float &tin, float &tout) {
     const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
@@ -260,15 +196,6 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     const bool in_ok = (lo + dst < 0.f) || (dst <= tol);
     const bool out_ok = (hi - dst > L) || (dst <= tol);
     return (in_ok && out_ok) ? 2 : 1;
-}
-
-__device__ __forceinline__ int classify32(const QConst &q, const ECand &e, float d) {
-    return classify_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c, e, d);
-}
-
-__device__ __forceinline__ bool interval32(const QConst &q, const ECand &e, float d, float &tin, float &tout) {
-    return interval_pair(make_float4(q.px, q.py, q.pz, q.t0), make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c, e,
-                         d, tin, tout);
 }
 
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
@@ -414,8 +341,9 @@ struct PairCtx {                     // what the fp64 path needs
     const float4 *Q;                 // queries (original rows)
     const float4 *rec;               // sorted entries
     const uint32_t *perm;            // sorted position -> entry row
-    float d, T0, T1;
+    float d, T0, T1;                 // d: the threshold rounded up to float (fp32 paths)
     OutArgs o;
+    double d64;                      // the caller's threshold (fp64 path)
 };
 
 // Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
@@ -440,7 +368,7 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
         need64 = !hit;
     }
     if (__any_sync(FULL, need64) && need64)
-        hit = pair64(qa, qb, ea, eb, (double)C->d, (double)C->T0, (double)C->T1, tin, tout);
+        hit = pair64(qa, qb, ea, eb, C->d64, (double)C->T0, (double)C->T1, tin, tout);
     const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
     Rec r{q, eid, tin, tout};
     append<EXACT>(C->o, *W, hit, r, lane);
@@ -487,21 +415,6 @@ __device__ __forceinline__ void queue_drain(const PairCtx *C, WarpState &W, uint
     if ((uint32_t)lane < rest) { W.rq[lane] = t1; W.rj[lane] = t2; }
     __syncwarp();
     qn = rest;
-}
-
-// ---------------------------------------------------------------------------
-// A6/A7: query sort and schedules
-// ---------------------------------------------------------------------------
-__global__ void k_query_keys(const float4 *__restrict__ Q, uint64_t nq, uint32_t *keys, uint32_t *vals,
-                             unsigned long long *bad) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nq) return;
-    float4 a = Q[2 * i], b = Q[2 * i + 1];
-    bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) && isfinite(b.y) &&
-              isfinite(b.z) && isfinite(b.w) && (b.w > a.w);
-    if (!ok) atomicMin(bad, (unsigned long long)i);
-    keys[i] = float_key(a.w);
-    vals[i] = (uint32_t)i;
 }
 
 struct SchedArgs {
@@ -604,11 +517,6 @@ __global__ void k_schedule(SchedArgs A) {
     }
 }
 
-__global__ void k_cat_keys(const Sched *__restrict__ S, uint32_t n, uint32_t *keys) {
-    uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) keys[p] = (uint32_t)(S[p].sel + 1);
-}
-
 __global__ void k_permute_sched(const Sched *__restrict__ in, const uint32_t *__restrict__ idx, uint32_t n,
                                 Sched *__restrict__ out) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -679,19 +587,6 @@ __global__ void k_tile_chunks(uint32_t *len_to_chunks, uint32_t ntiles, const un
     uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) st->ch = (uint32_t)ch;
     if (t < ntiles) len_to_chunks[t] = (uint32_t)((len_to_chunks[t] + ch - 1) / ch);
-}
-
-__global__ void k_sum_u32(const uint32_t *__restrict__ a, uint32_t n, unsigned long long *out) {
-    unsigned long long s = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s += a[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
-}
-
-__global__ void k_set_total_items(const uint32_t *item_start, uint32_t ntiles, DevStats *st) {
-    st->total_items = item_start[ntiles];
-    st->work_ctr = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1292,8 +1187,12 @@ struct Ctx {
 
 }  // namespace
 
-void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, float T0, float T1,
+void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64, float T0, float T1,
             uint64_t capacity, cudaStream_t s, tds_result_s *res) {
+    // fp32 paths use d rounded up (conservative: never drops a pair within the
+    // caller's d); the fp64 evaluation uses the caller's d exactly
+    float d = (float)d64;
+    if ((double)d < d64) d = nextafterf(d, INFINITY);
     tds_stats &S = res->stats;
     memset(&S, 0, sizeof S);
     res->stream = s;
@@ -1450,7 +1349,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
     tm.mark(2);
     if (!spatial) {
         RangeArgs a{};
-        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
+        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
         for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
         k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
@@ -1461,7 +1360,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
         k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, ngrab, grab_row.p);
         TDS_CHECK_LAUNCH();
         SpatialArgs a{};
-        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o};
+        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
         a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
@@ -1642,7 +1541,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             DBuf<uint32_t> bis;
             uint32_t bnt = plan_items(rsched.p + b0, 0, b1 - b0, bst.p, bt, bis, s);
             RangeArgs a{};
-            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o};
+            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
             a.pc.o.st = bst.p;
             for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
             a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
@@ -1686,7 +1585,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, float d, f
             k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, ngrab, grab_row.p);
             TDS_CHECK_LAUNCH();
             SpatialArgs a{};
-            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o};
+            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
             a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;

@@ -217,7 +217,7 @@ struct tds_result_s {
 };
 
 namespace tds {
-void search(tds_index_s *idx, int kind, const float4 *q, uint64_t nq, float d, float T0, float T1,
+void search(tds_index_s *idx, int kind, const float4 *q, uint64_t nq, double d, float T0, float T1,
             uint64_t capacity, cudaStream_t s, tds_result_s *res);
 void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint32_t *eid, float *tin,
            float *tout, bool dst_dev, bool sorted, cudaStream_t s);
