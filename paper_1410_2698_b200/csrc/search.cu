@@ -78,6 +78,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // A9: pair test
 // ---------------------------------------------------------------------------
@@ -149,6 +161,7 @@ __device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, flo
 // bound of the exact one, the bound being <= 1e-6 * max(b - a, min(|a|, |b|))
 // for every end not certainly clamped to a or b (clamped ends are exact);
 // 1 = evaluate in fp64 (pair64).
+template <bool CHECK_MISS = false>
 __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
                                         float &tin, float &tout) {
     const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
@@ -167,16 +180,22 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
     const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
     const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    if (CHECK_MISS) {                                           // fused filter (dense windows)
+        const float thr = fmaf(KU, M, d);
+        if (!((a < b) & (h <= thr * thr))) return 0;
+    }
     const float dl = d - KU * M;
     if (!(dl > 0.f) || !(h < dl * dl)) return 1;
     const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
     const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
     const float d2 = d * d;
     const float rem = fmaxf(d2 - hu, 0.f);
-    const float w = sqrtf(rem * rA);
+    const float w = sqrt_approx(rem * rA);                     // MUFU.SQRT: |rel err| <= 2^-22, in dw
     const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
     constexpr float U = 1.0f / 16777216.0f;
-    const float sqA = sqrtf(A);
+    // the bound itself needs no IEEE division / sqrt: approximate MUFU results,
+    // covered by the x2 safety factor
+    const float rsA = rsqrt_approx(A);                         // 1 / sqrt(A)
     // s_u may lie far outside [0, L]: magnitudes along the line up to |s_u| enter M_u,
     // and the relative errors of A and of the reciprocal scale |s_u| and w
     // first-order bounds: |dDa| <= 11 u M_u, |dDV| <= 6 u V1,
@@ -184,10 +203,10 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     // rem = d^2 - h_u -> |drem| <= 2 d 14 u M_u + A ds_u^2 + 2 u (d^2 + rem)
     const float Su = fmaxf(fabsf(su), L);
     const float Mu = M + Su * V1;
-    const float relA = (12.f * U) * V1 / sqA + 5.f * U;
-    const float dsu = (14.f * U) * Mu / sqA + (6.f * U) * V1 * Mu * rA + fabsf(su) * relA;
+    const float relA = (12.f * U) * V1 * rsA + 5.f * U;
+    const float dsu = (14.f * U) * Mu * rsA + (6.f * U) * V1 * Mu * rA + fabsf(su) * relA;
     const float drem = (28.f * U) * d * Mu + A * dsu * dsu + (2.f * U) * (d2 + rem);
-    const float dw = w * (drem / (2.f * rem) + 0.5f * relA + 2.f * U);
+    const float dw = w * (0.5f * drem * rcp_approx(rem) + 0.5f * relA + 4.f * U);
     const float dst = 2.f * (dsu + dw);                         // x2 safety
     const float lo = su - w, hi = su + w;
     tin = a + fminf(fmaxf(lo, 0.f), L);
@@ -664,6 +683,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     if (lane == 0) W.qn = 0;
     __syncwarp();
     unsigned long long exec = 0, direct_hits = 0;
+    bool dense = false;                      // warp-uniform: last filtered window was output-bound
     while (true) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
@@ -709,6 +729,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         while (base < whi) {
             const uint32_t cend = min(base + 64, whi);
             unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
+            const unsigned wmask = mask;
             if (!mask) {                       // skip the gap to the next range start
                 uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
 #pragma unroll
@@ -734,6 +755,50 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             }
             const ECand e0 = make_ecand(a0, b0), e1 = make_ecand(a1, b1);
             exec += (unsigned long long)(cend - base) * __popc(mask);
+            if (dense) {
+                // output-bound regime (last window was dense): fused filter + certain-hit
+                // interval per pair, no recomputation
+                uint32_t passes = 0;
+                while (mask) {
+                    const int g = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
+                    const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
+                    float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
+                    const int k0 = (v0 && c0 >= glo && c0 < ghi)
+                                       ? hit_kind<true>(q0, q1, q2.x, q2.y, e0, d, ti0, to0) : 0;
+                    const int k1 = (v1 && c1 >= glo && c1 < ghi)
+                                       ? hit_kind<true>(q0, q1, q2.x, q2.y, e1, d, ti1, to1) : 0;
+                    const unsigned p0 = __ballot_sync(FULL, k0 != 0), p1 = __ballot_sync(FULL, k1 != 0);
+                    passes += __popc(p0) + __popc(p1);
+                    if (!(p0 | p1)) continue;
+                    const uint32_t qid = __shfl_sync(FULL, S.qid, g);
+                    uint32_t hits_g = 0;
+                    const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
+                    if (hm0) {
+                        Rec r{qid, k0 == 2 ? __ldg(A.pc.perm + j0) : 0u, ti0, to0};
+                        append<EXACT>(A.pc.o, W.ws, k0 == 2, r, lane);
+                        hits_g += __popc(hm0);
+                    }
+                    if (hm1) {
+                        Rec r{qid, k1 == 2 ? __ldg(A.pc.perm + j1) : 0u, ti1, to1};
+                        append<EXACT>(A.pc.o, W.ws, k1 == 2, r, lane);
+                        hits_g += __popc(hm1);
+                    }
+                    direct_hits += hits_g;
+                    if (lane == g) owner_hits += hits_g;
+                    uint32_t qn = W.qn;
+                    queue_add(W.ws, qn, k0 == 1, qid, j0, lane);
+                    queue_add(W.ws, qn, k1 == 1, qid, j1, lane);
+                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
+                    __syncwarp();
+                    if (lane == 0) W.qn = qn;
+                    __syncwarp();
+                }
+                dense = passes >= (uint32_t)DIRECT_MIN * __popc(wmask);
+                base = cend;
+                continue;
+            }
             while (mask) {
                 const int g = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -744,7 +809,9 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 if (__popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
-                    // dense: most lanes passed -> in place (fp32 interval or fp64 queue)
+                    // dense: most lanes passed -> in place (fp32 interval or fp64 queue); the
+                    // following windows use the fused path
+                    dense = true;
                     const uint32_t hits_g =
                         handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, m0, m1, q0, q1, q2.x, q2.y, qid, j0, j1, e0, e1);
                     direct_hits += hits_g;
