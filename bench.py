@@ -213,6 +213,7 @@ def config_dict(args, w, ws):
     return {"workload": f"{w.name}-shaped", "n_entries": int(w.D.shape[0]), "n_queries_per_rank": int(w.Q.shape[0]),
             "d": w.d, "m_bins": w.m_bins, "v_subbins": w.v_subbins, "grid": list(w.grid),
             "variants": list(args.variants), "parallelism": f"query-sharded x{ws}, index replicated",
+            "variant_streams": 1 if args.serial else len(args.variants),
             "l2": "flushed between steps (256 MiB write); timed steps bracketed by barrier + synchronize",
             "note": w.note}
 
@@ -240,25 +241,48 @@ def run_tds(args, ws, rank, local):
         if dist is not None:
             dist.barrier()
 
-    def step(collect=None, host=False):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 + 2 * len(args.variants))]
-        ev[0].record(stream)
-        idx = tds.Index(Dh if host else D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
-        ev[1].record(stream)
-        per = {}
-        d2h = 0
-        for j, kind in enumerate(args.variants):
-            r = idx.search(Qh if host else Q, w.d, kind=kind, capacity=args.capacity)
-            ev[2 + 2 * j].record(stream)
-            out = r.fetch(device=not host)
-            ev[3 + 2 * j].record(stream)
-            st = r.stats()
-            per[kind] = st
-            d2h += 16 * r.count
+    # the three variants are independent searches of one index; --concurrent runs
+    # them one host thread + CUDA stream each (the C-ABI releases the GIL and
+    # supports concurrent searches on different streams).  Default: serial (faster
+    # on Random-1M: 1.86 vs 2.05 ms per step, thread/join overheads dominate)
+    side = [torch.cuda.Stream(dev) for _ in args.variants]
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=len(args.variants))
+
+    def one_variant(j, kind, idx, host):
+        st_ = side[j] if not args.serial else stream
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        with torch.cuda.stream(st_):
+            e[0].record(st_)
+            r = idx.search(Qh if host else Q, w.d, kind=kind, capacity=args.capacity, stream=st_.cuda_stream)
+            e[1].record(st_)
+            r.fetch(device=not host, stream=st_.cuda_stream)
+            e[2].record(st_)
+            stt = r.stats()
+            n = r.count
             r.close()
+        return e, stt, 16 * n
+
+    def step(collect=None, host=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        idx = tds.Index(Dh if host else D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid,
+                        stream=stream.cuda_stream)
+        ev[1].record(stream)                    # build_index synchronises: the index is ready
+        if args.serial:
+            outs = [one_variant(j, k, idx, host) for j, k in enumerate(args.variants)]
+        else:
+            futs = [pool.submit(one_variant, j, k, idx, host) for j, k in enumerate(args.variants)]
+            outs = [f.result() for f in futs]
+            for sj in side:
+                stream.wait_stream(sj)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(stream)
         idx.close()
+        per = {k: o[1] for k, o in zip(args.variants, outs)}
+        d2h = sum(o[2] for o in outs)
         if collect is not None:
-            collect.append((ev, per, d2h))
+            collect.append((ev + [end], per, d2h, [o[0] for o in outs]))
         return per
 
     # warm-up
@@ -297,27 +321,28 @@ def run_tds(args, ws, rank, local):
     nvar = len(args.variants)
     value = ws * nvar * nq * args.steps / (total_ms / 1e3)
     # per-phase breakdown (medians over the timed steps)
-    build_ms = statistics.median(ev[0].elapsed_time(ev[1]) for ev, _, _ in recs)
+    build_ms = statistics.median(r[0][0].elapsed_time(r[0][1]) for r in recs)
     per_kind = {}
     for j, kind in enumerate(args.variants):
-        pt = [p[kind]["pair_tests"] for _, p, _ in recs]
-        pm = [p[kind]["ms_pairs"] for _, p, _ in recs]
+        pt = [r[1][kind]["pair_tests"] for r in recs]
+        pm = [r[1][kind]["ms_pairs"] for r in recs]
+        first = recs[0][1][kind]
         per_kind[kind] = {
-            "search_ms": statistics.median(ev[1 if j == 0 else 1 + 2 * j].elapsed_time(ev[2 + 2 * j])
-                                           for ev, _, _ in recs),
-            "fetch_ms": statistics.median(ev[2 + 2 * j].elapsed_time(ev[3 + 2 * j]) for ev, _, _ in recs),
+            "search_ms": statistics.median(r[3][j][0].elapsed_time(r[3][j][1]) for r in recs),
+            "fetch_ms": statistics.median(r[3][j][1].elapsed_time(r[3][j][2]) for r in recs),
             "pair_kernel_ms": statistics.median(pm),
             "pair_tests": int(pt[0]),
-            "pairs_executed": int(recs[0][1][kind]["pairs_executed"]),
-            "refined_pairs": int(recs[0][1][kind]["refined_pairs"]),
-            "results": int(recs[0][1][kind]["n_results"]),
-            "passes": int(recs[0][1][kind]["passes"]),
-            "fallback_queries": int(recs[0][1][kind]["fallback_queries"]),
+            "pairs_executed": int(first["pairs_executed"]),
+            "refined_pairs": int(first["refined_pairs"]),
+            "results": int(first["n_results"]),
+            "passes": int(first["passes"]),
+            "fallback_queries": int(first["fallback_queries"]),
             "pair_tests_per_s": pt[0] / (statistics.median(pm) / 1e3) if statistics.median(pm) > 0 else None,
         }
+    searches_ms = statistics.median(r[0][1].elapsed_time(r[0][2]) for r in recs)
     pair_tests_step = sum(v["pair_tests"] for v in per_kind.values())
     # the paper's response time excludes the index build: search + fetch only
-    search_ms = sum(v["search_ms"] + v["fetch_ms"] for v in per_kind.values())
+    search_ms = searches_ms
     peaks = load_peaks()
     # roofline of the dominant kernel: the pair kernel with the largest share
     dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
@@ -375,8 +400,8 @@ def run_tds(args, ws, rank, local):
             "breakdown": {"build_index_ms": build_ms, "variants": per_kind,
                           "step_ms_median": statistics.median(step_ms)},
             "search_only": {"value": ws * nvar * nq / (search_ms / 1e3), "unit": "query segments/s",
-                            "note": "per-step medians of tds_search + tds_fetch_results only (index build "
-                                    "excluded, as in the paper's response time, P:1301-1304); rank 0"},
+                            "note": "per-step median of the three variants' tds_search + tds_fetch_results "
+                                    "(index build excluded, as in the paper's response time, P:1301-1304); rank 0"},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -400,9 +425,12 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="run the variants concurrently (one host thread + stream each)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.variants = VARIANTS if args.variants == "all" else tuple(args.variants.split(","))
+    args.serial = not args.concurrent
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
