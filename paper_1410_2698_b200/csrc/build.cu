@@ -198,7 +198,7 @@ __global__ void k_slab_count(const float4 *__restrict__ rec, uint64_t n, int c, 
     cnt[i] = (uint32_t)(s1 - s0 + 1);
 }
 
-__global__ void k_slab_emit(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v, int m,
+__global__ void k_slab_emit(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v, int mbits,
                             const uint32_t *__restrict__ bin, const uint32_t *__restrict__ pos,
                             uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -209,7 +209,7 @@ __global__ void k_slab_emit(const float4 *__restrict__ rec, uint64_t n, int c, f
     int s0 = cell_of(fminf(p0, p1), o, w, v), s1 = cell_of(fmaxf(p0, p1), o, w, v);
     uint32_t k = pos[i];
     for (int s = s0; s <= s1; ++s, ++k) {
-        keys[k] = (uint32_t)s * (uint32_t)m + bin[i];    // subbin (slab j, bin i) at j*m + i
+        keys[k] = ((uint32_t)s << mbits) | bin[i];      // subbin (slab j, bin i)
         vals[k] = (uint32_t)i;
     }
 }
@@ -316,6 +316,22 @@ int bits_for(uint64_t nk) {
     int b = 0;
     while ((1ull << b) < nk) ++b;
     return b;
+}
+
+// st_off[j*m + i] = first position of subbin (slab j, bin i) in keys sorted by
+// (j << mbits) | i (one thread per subbin, binary search)
+__global__ void k_subbin_offsets(const uint32_t *__restrict__ keys, uint64_t len, int v, int m, int mbits,
+                                 uint32_t *__restrict__ off) {
+    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > (uint64_t)v * m) return;
+    uint32_t key = (t == (uint64_t)v * m) ? 0xffffffffu
+                                          : (((uint32_t)(t / m) << mbits) | (uint32_t)(t % m));
+    uint64_t lo = 0, hi = len;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    off[t] = (uint32_t)lo;
 }
 
 // group (key, val) pairs by key with a stable radix sort; vals -> out ids,
@@ -476,10 +492,15 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
             cudaStream_t sc = side[c];
             const uint64_t len = tot[c] & 0xffffffffull;
             DBuf<uint32_t> k2(len, sc), v2(len, sc), off((uint64_t)v * m + 1, sc);
-            k_slab_emit<<<nblk(n), NT, 0, sc>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, m, bin.p, st_pos[c].p, k2.p,
-                                               v2.p);
+            const int mbits = bits_for((uint64_t)m);
+            k_slab_emit<<<nblk(n), NT, 0, sc>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, mbits, bin.p, st_pos[c].p,
+                                               k2.p, v2.p);
             TDS_CHECK_LAUNCH();
-            group_by_key(k2.p, v2.p, len, (uint64_t)v * m, off.p, sc);
+            // emitted in sorted-position order, so within a slab the bins are already
+            // ascending: a stable sort on the slab bits alone groups the subbins
+            radix_sort_pairs(k2.p, v2.p, len, mbits, mbits + bits_for((uint64_t)v), sc);
+            k_subbin_offsets<<<nblk((uint64_t)v * m + 1), NT, 0, sc>>>(k2.p, len, v, m, mbits, off.p);
+            TDS_CHECK_LAUNCH();
             st_pos[c].s = sc;                      // free after its last use, on that stream
             idx->st_arr[c] = v2.release();
             idx->st_len[c] = len;

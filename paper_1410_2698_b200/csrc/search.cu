@@ -1449,9 +1449,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     TDS_CHECK_LAUNCH();
     exclusive_scan_u64(chunk_off.p, chunk_off.p, nres, nullptr, s);
 
-    if (hs.dropped == 0 && cap >= (1ull << 22) && hs.hits <= cap / 8) {
-        // few results in a large pass buffer: compact them into a right-sized store
-        // and return the buffer to the pool for the next search
+    if (hs.dropped == 0 && cap >= (1ull << 26) && hs.hits <= cap / 8) {
+        // few results in a large (>= 1 GB) pass buffer: compact them into a
+        // right-sized store and return the buffer to the pool for the next search
         DBuf<Rec> store(hs.hits, s, /*big=*/hs.hits * sizeof(Rec) > (256ull << 20));
         if (nres) {
             k_flatten<<<nblk(nres * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, chunk_off.p, store.p);
