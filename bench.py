@@ -136,11 +136,21 @@ def max_over_ranks(dist, x, dev):
     return float(t.item())
 
 
+def sum_over_ranks(dist, x, dev):
+    import torch
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def make_workload(args, rank):
     import synth
     kw = {}
     if args.config in ("random-1m", "random-dense", "random-dense-1m", "merger"):
-        kw["offset"] = rank
+        kw["offset"] = rank                       # weak scaling: each rank its own query set
+    elif args.config == "scale-out":
+        kw["shard"] = (rank, int(os.environ.get("WORLD_SIZE", "1")))   # strong: one query set, sharded
     w = synth.make_workload(args.config, **kw)
     if args.d is not None:
         w.d = args.d
@@ -319,7 +329,8 @@ def run_tds(args, ws, rank, local):
 
     nq = w.Q.shape[0]
     nvar = len(args.variants)
-    value = ws * nvar * nq * args.steps / (total_ms / 1e3)
+    nq_all = nq if dist is None else int(round(sum_over_ranks(dist, float(nq), dev)))
+    value = nvar * nq_all * args.steps / (total_ms / 1e3)
     # per-phase breakdown (medians over the timed steps)
     build_ms = statistics.median(r[0][0].elapsed_time(r[0][1]) for r in recs)
     per_kind = {}
@@ -343,6 +354,7 @@ def run_tds(args, ws, rank, local):
     pair_tests_step = sum(v["pair_tests"] for v in per_kind.values())
     # the paper's response time excludes the index build: search + fetch only
     search_ms = searches_ms
+    pt_all = pair_tests_step if dist is None else sum_over_ranks(dist, float(pair_tests_step), dev)
     peaks = load_peaks()
     # roofline of the dominant kernel: the pair kernel with the largest share
     dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
@@ -376,7 +388,7 @@ def run_tds(args, ws, rank, local):
         tot = sum(e2e_ms)
         if dist is not None:
             tot = max_over_ranks(dist, tot, dev)
-        e2e = {"value": ws * nvar * nq * args.steps / (tot / 1e3), "unit": "query segments/s",
+        e2e = {"value": nvar * nq_all * args.steps / (tot / 1e3), "unit": "query segments/s",
                "h2d_bytes_per_step": int(w.D.nbytes + nvar * w.Q.nbytes),
                "d2h_bytes_per_step": int(statistics.median(x[2] for x in er)),
                "timing": "host wall clock around each step, synchronize on both sides, max over ranks"}
@@ -392,14 +404,16 @@ def run_tds(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": "query segments/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "scaling": "strong" if args.config == "scale-out" else "weak", "vs_baseline": None,
+            "dtype": "f32+f64", "data": "synthetic",
             "config": config_dict(args, w, ws),
-            "pair_tests_per_s": ws * pair_tests_step * args.steps / (total_ms / 1e3),
+            "pair_tests_per_s": pt_all * args.steps / (total_ms / 1e3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,
             "breakdown": {"build_index_ms": build_ms, "variants": per_kind,
                           "step_ms_median": statistics.median(step_ms)},
             "search_only": {"value": ws * nvar * nq / (search_ms / 1e3), "unit": "query segments/s",
+                            "ranks": "rank 0's time, scaled by the rank count",
                             "note": "per-step median of the three variants' tds_search + tds_fetch_results "
                                     "(index build excluded, as in the paper's response time, P:1301-1304); rank 0"},
         }

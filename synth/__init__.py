@@ -40,7 +40,7 @@ BASE_SEED = 1410269800
 
 __all__ = [
     "Workload", "BASE_SEED", "random_walk", "tiny", "random_1m", "random_1m_s1",
-    "random_dense", "merger", "query_stride", "segments_from_positions",
+    "random_dense", "merger", "scale_out", "query_stride", "segments_from_positions",
     "dense_cube_side_kpc", "CONFIGS", "make_workload",
 ]
 
@@ -244,6 +244,41 @@ def merger(n_per_disk: int = 65536, n_timesteps: int = 193, seed: int = BASE_SEE
                     f"two disks x {n_per_disk}, {n_query_traj} query trajectories from D")
 
 
+def scale_out(n_traj: int = 250_000, n_steps: int = 400, seed: int = BASE_SEED + 4, query_stride: int = 10,
+              shard: tuple = (0, 1), d: float = 50.0) -> Workload:
+    """Scale-out (BASELINE.json configs[4]): a 100M-segment random-walk database
+    (250,000 trajectories x 400 timesteps = 99,750,000 segments) at the Random-1M
+    density (cube side 1000 * 100^(1/3) ~= 4642, steps U[-1,1], start times
+    U[0,100]), and 10% of its trajectories (every 10th) as the query set
+    (25,000 x 399 = 9,975,000 query segments).  ``shard = (rank, world)`` keeps
+    every world-th query trajectory starting at rank (strong scaling: the query
+    set is split across GPUs).  Generated in chunks of trajectories straight
+    into the float32 output (peak host memory ~ 1.2x the 3.2 GB database).
+    m = 10,000 bins, v = 4.
+    """
+    box = 1000.0 * (n_traj / 2500.0) ** (1.0 / 3.0)
+    D = np.empty((n_traj * (n_steps - 1), 8), dtype=np.float32)
+    chunk = 10_000
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    for t0 in range(0, n_traj, chunk):
+        nt = min(chunk, n_traj - t0)
+        start = rng.uniform(-box / 2, box / 2, size=(nt, 1, 3))
+        steps = rng.uniform(-1.0, 1.0, size=(nt, n_steps - 1, 3))
+        pos = np.concatenate([start, start + np.cumsum(steps, axis=1)], axis=1).astype(np.float32)
+        t_start = rng.uniform(0.0, 100.0, size=(nt, 1))
+        times = (t_start + np.arange(n_steps)[None, :]).astype(np.float32)
+        D[t0 * (n_steps - 1):(t0 + nt) * (n_steps - 1)] = segments_from_positions(pos, times)
+    tD = np.repeat(np.arange(n_traj, dtype=np.int32), n_steps - 1)
+    rank, world = shard
+    qtraj = np.arange(0, n_traj, query_stride)[rank::world]
+    Dr = D.reshape(n_traj, n_steps - 1, 8)
+    Q = np.ascontiguousarray(Dr[qtraj].reshape(-1, 8))
+    tQ = np.repeat(qtraj.astype(np.int32), n_steps - 1)
+    return Workload("scale-out", D, Q, d, 10000, 4, (50, 50, 50), tD, tQ,
+                    f"100M database at Random-1M density (cube {box:.0f}); query trajectories every "
+                    f"{query_stride}th, shard {rank}/{world}")
+
+
 CONFIGS = {
     "tiny": tiny,
     "random-1m": random_1m,
@@ -251,6 +286,7 @@ CONFIGS = {
     "random-dense": random_dense,
     "random-dense-1m": lambda **kw: random_dense(n_particles=5184, **kw),
     "merger": merger,
+    "scale-out": scale_out,
 }
 
 

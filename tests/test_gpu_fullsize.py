@@ -111,3 +111,23 @@ def test_merger_full(tds):
         check(got, ref, w.D, w.Q, d, label=f"merger {kind}")
         out[kind] = (n, h)
     assert out["temporal"] == out["spatiotemporal"] == out["spatial"]
+
+
+def test_scale_out_shard(tds):
+    """scale-out (BASELINE.json configs[4]): the 100M-segment database, one GPU's
+    shard of the 10M query segments (1/8), GPUTemporal and GPUSpatioTemporal,
+    sampled against the oracle and cross-checked by hash."""
+    w = synth.scale_out(shard=(3, 8), d=5.0)
+    assert w.D.shape[0] == 99_750_000
+    d = 5.0
+    rng = np.random.default_rng(9)
+    sel = np.sort(rng.choice(w.Q.shape[0], 24, replace=False))
+    ref = oracle.search(w.D, w.Q, d, qsel=sel)
+    idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=w.m_bins, v=w.v_subbins)
+    Qd = _cuda(w.Q)
+    out = {}
+    for kind in ("temporal", "spatiotemporal"):
+        got, n, h, st = _search_sampled(idx, Qd, d, kind, sel)
+        check(got, ref, w.D, w.Q, d, label=f"scale-out {kind}")
+        out[kind] = (n, h)
+    assert out["temporal"] == out["spatiotemporal"]
