@@ -804,8 +804,9 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
                 const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                const bool m0 = v0 && c0 >= glo && c0 < ghi && filter_pair(q0, q1, q2.x, q2.y, e0, d);
-                const bool m1 = v1 && c1 >= glo && c1 < ghi && filter_pair(q0, q1, q2.x, q2.y, e1, d);
+                // branch-free (bitwise &): no divergent branch around each filter
+                const bool m0 = (v0 & (c0 >= glo) & (c0 < ghi)) & filter_pair(q0, q1, q2.x, q2.y, e0, d);
+                const bool m1 = (v1 & (c1 >= glo) & (c1 < ghi)) & filter_pair(q0, q1, q2.x, q2.y, e1, d);
                 if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 if (__popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
