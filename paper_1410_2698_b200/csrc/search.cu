@@ -371,6 +371,7 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
     const uint32_t q = v ? W->rq[lane] : 0u, j = v ? W->rj[lane] : 0u;
+    __syncwarp();                    // queue slots read: later queue_add may reuse them
     float tin = 0.f, tout = 0.f;
     bool hit = false, need64 = false;
     float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f), ea = qa, eb = qb;
@@ -1047,6 +1048,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
             queue_drain<EXACT>(&A.pc, W, qn, lane);
         }
     }
+    __syncwarp();                    // last queue_add writes -> flush reads
     if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
     warp_state_finish<EXACT>(A.pc.o, W, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);

@@ -1,0 +1,28 @@
+"""compute-sanitizer on a small end-to-end run (build, the three variants, forced
+overflow, sorted fetch): memcheck, racecheck (shared-memory hazards, incl.
+warp-synchronous ones) and synccheck must report nothing."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not found")
+    r = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "7", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_smoke.py")],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "sanitize smoke ok" in out
+    if tool == "racecheck":
+        assert "0 hazards displayed (0 errors, 0 warnings)" in out, out[-3000:]
+    else:
+        assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]
