@@ -151,6 +151,25 @@ int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *qu
                       uint32_t *entry_id, float *t_in, float *t_out, int dst_is_device,
                       int sorted, void *stream);
 
+/*
+ * tds_merge_trajectories — the trajectory-level answer ("find all
+ * trajectories within d ... over [t_start, t_end]", "and corresponding
+ * time periods").  Segments belong to trajectories:
+ * q_traj[k] / e_traj[i] is the trajectory id of query row k / entry row i
+ * (device or host memory; nq must equal the searched query count, ne the
+ * index's entry count).  For every (query trajectory, entry trajectory) pair
+ * the closed intervals of its segment-pair records are merged into maximal
+ * disjoint intervals (an interval merges with the next when the next starts
+ * no later than `gap` after it ends; gap = 0: overlapping or touching, e.g.
+ * contacts across a shared timestep).  The new result holds records
+ * (query trajectory id, entry trajectory id, t_in, t_out), fetched with
+ * tds_fetch_results (query_id / entry_id columns carry the trajectory ids).
+ * Errors: TDS_EINVAL (NULL, size mismatch, bad gap), TDS_ENOMEM, TDS_ECUDA.
+ * Synchronises stream.
+ */
+int tds_merge_trajectories(tds_result r, const uint32_t *q_traj, uint64_t nq, const uint32_t *e_traj,
+                           uint64_t ne, float gap, void *stream, tds_result *out, uint64_t *n_out);
+
 /* tds_result_stats — counters and device timings of the search that made r. */
 int tds_result_stats(tds_result r, tds_stats *out);
 

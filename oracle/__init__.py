@@ -105,3 +105,35 @@ def search(D, Q, d: float, window=(-np.inf, np.inf), near: float = 1.01, nthread
     lib.oracle_fetch(*(out[k].ctypes.data for k in ("qid", "eid", "t_in", "t_out", "dmin", "hit")))
     out["hit"] = out["hit"].astype(bool)
     return out
+
+
+def merge_trajectories(qid, eid, t_in, t_out, q_traj, e_traj, gap: float = 0.0) -> dict:
+    """Trajectory-level answer ("find all trajectories within d",
+    P:86-90 "and corresponding time periods"): for every pair
+    (query trajectory, entry trajectory), the union of the closed intervals of
+    its segment-pair records, as maximal disjoint intervals.  Two intervals
+    merge when the next starts no later than ``gap`` after the current one
+    ends (gap = 0: overlapping or touching).  Plain definition: sort by
+    (q_traj, e_traj, t_in) and sweep.  Returns dict qtraj, etraj, t_in, t_out
+    (ordered by qtraj, etraj, t_in)."""
+    qt = np.asarray(q_traj)[np.asarray(qid, np.int64)]
+    et = np.asarray(e_traj)[np.asarray(eid, np.int64)]
+    ti = np.asarray(t_in, np.float64)
+    to = np.asarray(t_out, np.float64)
+    order = np.lexsort((ti, et, qt))
+    out = {"qtraj": [], "etraj": [], "t_in": [], "t_out": []}
+    cur = None
+    for k in order:
+        key = (int(qt[k]), int(et[k]))
+        if cur is not None and cur[0] == key and ti[k] <= cur[2] + gap:
+            cur[2] = max(cur[2], to[k])
+            continue
+        if cur is not None:
+            for f, v in zip(("qtraj", "etraj", "t_in", "t_out"), (cur[0][0], cur[0][1], cur[1], cur[2])):
+                out[f].append(v)
+        cur = [key, ti[k], to[k]]
+    if cur is not None:
+        for f, v in zip(("qtraj", "etraj", "t_in", "t_out"), (cur[0][0], cur[0][1], cur[1], cur[2])):
+            out[f].append(v)
+    return {"qtraj": np.array(out["qtraj"], np.int64), "etraj": np.array(out["etraj"], np.int64),
+            "t_in": np.array(out["t_in"], np.float64), "t_out": np.array(out["t_out"], np.float64)}

@@ -34,7 +34,7 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 # every symbol include/tds.h declares
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
-               "tds_version", "tds_kernel_launches"]
+               "tds_version", "tds_kernel_launches", "tds_merge_trajectories"]
 
 
 class TdsError(RuntimeError):
@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH):
     lib.tds_search.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, vp, ctypes.POINTER(vp),
                                ctypes.POINTER(u64)]
     lib.tds_fetch_results.argtypes = [vp, u64, u64, vp, vp, vp, vp, i32, i32, vp]
+    lib.tds_merge_trajectories.argtypes = [vp, vp, u64, vp, u64, f32, vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
     lib.tds_result_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
     lib.tds_result_count.argtypes = [vp]
     lib.tds_result_count.restype = u64
@@ -87,7 +88,7 @@ def load_library(path: str = LIB_PATH):
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_uint32)]
     for name in ("tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats",
-                 "tds_index_export", "tds_index_info"):
+                 "tds_index_export", "tds_index_info", "tds_merge_trajectories"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -128,6 +129,21 @@ def _segments(x):
         b = b[off:off + a.size].reshape(-1, 8)
         b[...] = a
         a = b
+    return ctypes.c_void_p(a.ctypes.data), a.shape[0], a
+
+
+def _u32(x):
+    """(pointer, n, keepalive) for a 1-D uint32/int32 array (torch cuda/cpu or numpy)."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if x.dtype not in (torch.int32,) or x.dim() != 1:
+                x = x.to(torch.int32).reshape(-1)
+            x = x.contiguous()
+            return ctypes.c_void_p(x.data_ptr()), x.shape[0], x
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(np.asarray(x).astype(np.uint32).reshape(-1))
     return ctypes.c_void_p(a.ctypes.data), a.shape[0], a
 
 
@@ -217,6 +233,19 @@ class Result:
         _check(lib.tds_fetch_results(self._h, int(first), cnt, *ptrs, 1 if device else 0, 1 if sorted else 0,
                                      _stream_ptr(stream)))
         return q, e, ti, to
+
+    def merge_trajectories(self, q_traj, e_traj, gap: float = 0.0, stream=None) -> "Result":
+        """Trajectory-level answer (tds_merge_trajectories): records become
+        (query trajectory, entry trajectory, t_in, t_out), maximal intervals."""
+        lib = load_library()
+        qp, nq, kq = _u32(q_traj)
+        ep, ne, ke = _u32(e_traj)
+        h = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        _check(lib.tds_merge_trajectories(self._h, qp, nq, ep, ne, float(gap), _stream_ptr(stream), ctypes.byref(h),
+                                          ctypes.byref(n)))
+        del kq, ke
+        return Result(h, n.value)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -209,6 +209,27 @@ static void stage(const tds_seg *src, uint64_t n, cudaStream_t s, Staged &out) {
     out.p = out.own.p;
 }
 
+// device copy of a uint32 array that may live in host memory
+struct StagedU32 {
+    const uint32_t *p = nullptr;
+    DBuf<uint32_t> own;
+};
+
+static void stage_u32(const uint32_t *src, uint64_t n, cudaStream_t s, StagedU32 &out) {
+    if (!src) fail(TDS_EINVAL, "NULL id array");
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, src);
+    if (e != cudaSuccess) cudaGetLastError();
+    bool dev = (e == cudaSuccess) && (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    if (dev) {
+        out.p = src;
+        return;
+    }
+    out.own = DBuf<uint32_t>(n, s);
+    TDS_CUDA(cudaMemcpyAsync(out.own.p, src, n * 4, cudaMemcpyHostToDevice, s));
+    out.p = out.own.p;
+}
+
 }  // namespace tds
 
 using namespace tds;
@@ -309,6 +330,40 @@ int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *qu
     if (!r) fail(TDS_EINVAL, "NULL result");
     tds::fetch(r, first, count, query_id, entry_id, t_in, t_out, dst_is_device != 0, sorted != 0,
                (cudaStream_t)stream);
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_merge_trajectories(tds_result r, const uint32_t *q_traj, uint64_t nq, const uint32_t *e_traj, uint64_t ne,
+                           float gap, void *stream, tds_result *out, uint64_t *n_out) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!r || !out) fail(TDS_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (nq != r->nq) fail(TDS_EINVAL, "q_traj has %llu ids, the search had %llu queries", (unsigned long long)nq,
+                          (unsigned long long)r->nq);
+    if (ne != r->ne) fail(TDS_EINVAL, "e_traj has %llu ids, the index has %llu entries", (unsigned long long)ne,
+                          (unsigned long long)r->ne);
+    if (!(gap >= 0.f) || !isfinite(gap)) fail(TDS_EINVAL, "gap = %g must be finite and >= 0", (double)gap);
+    cudaStream_t s = (cudaStream_t)stream;
+    tds_result_s *m = new tds_result_s();
+    cudaGetDevice(&m->device);
+    try {
+        if (r->n > 0) {
+            StagedU32 qt, et;
+            stage_u32(q_traj, nq, s, qt);
+            stage_u32(e_traj, ne, s, et);
+            tds::merge_trajectories(r, qt.p, nq, et.p, ne, gap, s, m);
+        }
+    } catch (...) {
+        free_result(m);
+        delete m;
+        throw;
+    }
+    m->nq = r->nq;
+    m->ne = r->ne;
+    *out = m;
+    if (n_out) *n_out = m->n;
     return TDS_OK;
     ABI_CATCH
 }

@@ -1266,6 +1266,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     tds_stats &S = res->stats;
     memset(&S, 0, sizeof S);
     res->stream = s;
+    res->nq = nq;
+    res->ne = idx->n;
     res->n = 0;
     res->chunked = false;
     if (nq == 0) return;

@@ -214,6 +214,7 @@ struct tds_result_s {
     tds_stats stats{};
     int device = 0;
     cudaStream_t stream = 0;          // stream of the last operation (frees are ordered after it)
+    uint64_t nq = 0, ne = 0;          // query / entry counts of the search (trajectory merge checks)
 };
 
 namespace tds {
@@ -222,4 +223,6 @@ void search(tds_index_s *idx, int kind, const float4 *q, uint64_t nq, double d, 
 void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint32_t *eid, float *tin,
            float *tout, bool dst_dev, bool sorted, cudaStream_t s);
 void free_result(tds_result_s *r);
+void merge_trajectories(tds_result_s *r, const uint32_t *q_traj, uint64_t nq, const uint32_t *e_traj, uint64_t ne,
+                        float gap, cudaStream_t s, tds_result_s *out);
 }  // namespace tds

@@ -260,3 +260,40 @@ def test_fsg_time_trim_equals_literal(tds, name, monkeypatch):
     assert st["pair_tests"] <= st_l["pair_tests"]
     if name != "tiny":
         assert st["pair_tests"] < st_l["pair_tests"] / 4      # time trimming prunes most of a cell
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("gap", [0.0, 0.75])
+def test_trajectory_merge(tds, tiny, kind, gap):
+    """tds_merge_trajectories equals oracle.merge_trajectories applied to the
+    oracle's segment-level result (pairs in the 1e-5 d band excluded on both
+    sides: their presence may differ)."""
+    w, ref = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    r = idx.search(_cuda(w.Q), w.d, kind=kind)
+    m = r.merge_trajectories(w.traj_Q.astype(np.uint32), w.traj_D.astype(np.uint32), gap=gap)
+    gq, ge, gi, go = m.fetch(sorted=True, device=False)
+    band = np.abs(ref["dmin"] - w.d) <= 1e-5 * w.d
+    if band.any():
+        pytest.skip("band pairs present: trajectory-level comparison would need band handling")
+    h = ref["hit"]
+    om = oracle.merge_trajectories(ref["qid"][h], ref["eid"][h], ref["t_in"][h], ref["t_out"][h],
+                                   w.traj_Q, w.traj_D, gap=gap)
+    order = np.lexsort((gi, ge, gq))
+    assert len(gq) == len(om["qtraj"])
+    assert np.array_equal(gq[order], om["qtraj"]) and np.array_equal(ge[order], om["etraj"])
+    span = np.maximum(1.0, np.abs(om["t_in"]))
+    assert np.all(np.abs(gi[order] - om["t_in"]) <= 1e-5 * span)
+    assert np.all(np.abs(go[order] - om["t_out"]) <= 1e-5 * np.maximum(1.0, np.abs(om["t_out"])))
+    assert len(gq) < r.count                       # trajectory answers merge segment records
+
+
+def test_trajectory_merge_crossing_boundary(tds):
+    Q = np.array([[-5, 0, 0, 0, 0, 0, 0, 5], [0, 0, 0, 5, 5, 0, 0, 10]], np.float32)
+    D = np.array([[0, 0, 0, 0, 0, 0, 0, 5], [0, 0, 0, 5, 0, 0, 0, 10]], np.float32)
+    idx = tds.Index(_cuda(D), kinds=tds.ALL, m=2, v=1, grid=(2, 2, 2))
+    for kind in KINDS:
+        r = idx.search(_cuda(Q), 1.0, kind=kind)
+        m = r.merge_trajectories(np.array([7, 7], np.uint32), np.array([3, 3], np.uint32))
+        q, e, ti, to = m.fetch(device=False)
+        assert (q.tolist(), e.tolist(), ti.tolist(), to.tolist()) == ([7], [3], [4.0], [6.0])
