@@ -94,3 +94,42 @@ def gather_results(qid, eid, t_in, t_out, q_offset: int = 0, dst: int = 0, group
     allp = torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
     return (allp[:, 0].clone(), allp[:, 1].clone(), allp[:, 2].clone().view(torch.float32),
             allp[:, 3].clone().view(torch.float32))
+
+
+# ---------------------------------------------------------------------------
+# Time-partitioned D sharding (the paper's intended scenario of
+# "a number of GPU-equipped compute nodes"): D is split into `world`
+# contiguous t_start ranges of equal entry count; each rank indexes only its
+# slice (memory per GPU ~ |D| / N) and answers every query against it; the
+# union of the ranks' records is the answer (each entry lives on one rank, so
+# the union has no duplicates).  Entry ids are mapped back to rows of D.
+# ---------------------------------------------------------------------------
+def time_partition(t_start: np.ndarray, rank: int, world: int) -> np.ndarray:
+    """Global rows of D owned by ``rank``: the rank-th of ``world`` equal-count
+    slices of D in (t_start, row) order (stable)."""
+    order = np.argsort(np.asarray(t_start), kind="stable")
+    lo, hi = shard_bounds(order.size, rank, world)
+    return np.sort(order[lo:hi])
+
+
+class TimeShardedIndex:
+    """This rank's index over its t_start slice of D."""
+
+    def __init__(self, D, rank: int, world: int, kinds: int = 5, m: int = 1000, v: int = 1,
+                 grid=(50, 50, 50), device=None):
+        import torch
+        import paper_1410_2698_b200 as tds
+        Dn = D.cpu().numpy() if isinstance(D, torch.Tensor) else np.asarray(D)
+        rows = time_partition(Dn[:, 3], rank, world)
+        self.rows = torch.as_tensor(rows.astype(np.int32), device=device or "cuda")
+        self.index = tds.Index(torch.as_tensor(np.ascontiguousarray(Dn[rows]), device=device or "cuda"),
+                               kinds=kinds, m=m, v=v, grid=grid)
+        self.rank, self.world = rank, world
+
+    def search(self, queries, d: float, kind: str = "temporal", window=(-math.inf, math.inf), capacity: int = 0):
+        """(qid, eid, t_in, t_out) device tensors for this slice; eid = rows of D."""
+        r = self.index.search(queries, d, window=window, kind=kind, capacity=capacity)
+        q, e, ti, to = r.fetch(device=True)
+        e = self.rows[e.long()]
+        r.close()
+        return q, e, ti, to

@@ -84,3 +84,17 @@ def test_gather_world2_gloo():
     for k, e, a, b in zip(qid, eid, tin, tout):
         assert e in (3 * k, 3 * k + 1)
         assert a == pytest.approx(0.5 * k) and b == pytest.approx(0.5 * k + 0.25)
+
+
+def test_time_partition_is_a_partition_in_time_order():
+    rng = np.random.default_rng(0)
+    t0 = np.round(rng.uniform(0, 10, 1001), 1)            # ties on purpose
+    from paper_1410_2698_b200.dist import time_partition
+    for world in (1, 2, 3, 8):
+        parts = [time_partition(t0, r, world) for r in range(world)]
+        allr = np.concatenate(parts)
+        assert np.array_equal(np.sort(allr), np.arange(1001))
+        for a, b in zip(parts, parts[1:]):
+            assert t0[a].max() <= t0[b].min()              # contiguous time ranges
+        sizes = [p.size for p in parts]
+        assert max(sizes) - min(sizes) <= 1

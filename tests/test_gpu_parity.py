@@ -297,3 +297,26 @@ def test_trajectory_merge_crossing_boundary(tds):
         m = r.merge_trajectories(np.array([7, 7], np.uint32), np.array([3, 3], np.uint32))
         q, e, ti, to = m.fetch(device=False)
         assert (q.tolist(), e.tolist(), ti.tolist(), to.tolist()) == ([7], [3], [4.0], [6.0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_partitioned_union_equals_single_index(tds, world):
+    """SURVEY §8f-1 on one GPU: the union over `world` time slices of D (each
+    with its own index, every query against every slice) equals the single-index
+    result, without duplicates, with entry ids mapped back to rows of D."""
+    import torch
+    from paper_1410_2698_b200.dist import TimeShardedIndex
+    w = synth.random_1m(n_traj=400)
+    full = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=1000, v=2)
+    for kind in ("temporal", "spatiotemporal"):
+        r = full.search(_cuda(w.Q), 20.0, kind=kind)
+        a = r.fetch(sorted=True, device=False)
+        ka = np.sort(keys(a[0], a[1]))
+        parts = []
+        for rank in range(world):
+            sh = TimeShardedIndex(w.D, rank, world, kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=1000, v=2)
+            q, e, _, _ = sh.search(_cuda(w.Q), 20.0, kind=kind)
+            parts.append(keys(q.cpu().numpy(), e.cpu().numpy()))
+        kb = np.sort(np.concatenate(parts))
+        assert np.unique(kb).size == kb.size
+        assert np.array_equal(ka, kb)
