@@ -156,7 +156,51 @@ __device__ __forceinline__ bool filter_pair(float4 q0, float4 q1, float t0c, flo
     return (a < b) & (h <= thr * thr);
 }
 
-// For a pair that passed filter_pair: 2 = certain hit (fp32 closest approach
+// Absolute-time form of the certified filter ("absolute form"),
+// used by the range kernel's sparse windows.  Times are shifted by a constant
+// origin tc (the middle of the index's time extent): t' = fl(t - tc), monotone
+// in t.  Each segment is written as P(t') = c + v t' with c = P0 - v t0', so
+// the relative motion is C + V t' and the closest approach over the shared span
+// [a', b'] is at clamp(-(C.V)/A, a', b') — no per-pair time offsets.  Its fp32
+// error is <= 12 u (m_q + m_e) with the per-segment magnitude
+// m = |c|_1 + |P1 - P0|_1 + max(|t0'|, |t1'|) |v|_1, so the margin
+// eta = 64 u (m_q + m_e) keeps a factor > 5.  The span test is a' <= b' (a
+// superset of a < b: rounding t - tc may merge a' and b').
+struct FSeg {
+    float cx, cy, cz, m;
+    float vx, vy, vz, t0, t1;        // t0, t1 shifted by tc
+};
+
+__device__ __forceinline__ FSeg make_fseg(float4 a, float4 b, float tc) {
+    FSeg f;
+    const float dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
+    const float r = rcp_approx(b.w - a.w);
+    f.t0 = a.w - tc; f.t1 = b.w - tc;
+    f.vx = dx * r; f.vy = dy * r; f.vz = dz * r;
+    f.cx = fmaf(-f.vx, f.t0, a.x); f.cy = fmaf(-f.vy, f.t0, a.y); f.cz = fmaf(-f.vz, f.t0, a.z);
+    const float T = fmaxf(fabsf(f.t0), fabsf(f.t1));
+    f.m = fmaf(T, fabsf(f.vx) + fabsf(f.vy) + fabsf(f.vz),
+               (fabsf(f.cx) + fabsf(f.cy) + fabsf(f.cz)) + (fabsf(dx) + fabsf(dy) + fabsf(dz)));
+    return f;
+}
+
+// n0 = (c, m), n1 = (v, -) of the query; [t0c, t1c] its window-clipped span
+// shifted by tc; df = the filter threshold (d rounded up, times 1 + 2^-20 to
+// absorb the rounding of thr^2)
+__device__ __forceinline__ bool filter_abs(float4 n0, float4 n1, float t0c, float t1c, const FSeg &e, float df) {
+    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
+    const float Cx = n0.x - e.cx, Cy = n0.y - e.cy, Cz = n0.z - e.cz;
+    const float Vx = n1.x - e.vx, Vy = n1.y - e.vy, Vz = n1.z - e.vz;
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Cx, Vx, fmaf(Cy, Vy, Cz * Vz));
+    const float t = fminf(fmaxf(-B * rcp_approx(A), a), b);
+    const float yx = fmaf(t, Vx, Cx), yy = fmaf(t, Vy, Cy), yz = fmaf(t, Vz, Cz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    const float thr = fmaf(KU, n0.w + e.m, df);
+    return (a <= b) & (h <= thr * thr);
+}
+
+// For a pair that passed a filter: 0 = no shared span (a >= b), 2 = certain hit (fp32 closest approach
 // < d - eta) whose fp32 interval [tin, tout] is within its first-order error
 // bound of the exact one, the bound being <= 1e-6 * max(b - a, min(|a|, |b|))
 // for every end not certainly clamped to a or b (clamped ends are exact);
@@ -180,9 +224,10 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
     const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
     const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
+    if (!(a < b)) return 0;                                     // C5 (filter_abs passes a == b)
     if (CHECK_MISS) {                                           // fused filter (dense windows)
         const float thr = fmaf(KU, M, d);
-        if (!((a < b) & (h <= thr * thr))) return 0;
+        if (!(h <= thr * thr)) return 0;
     }
     const float dl = d - KU * M;
     if (!(dl > 0.f) || !(h < dl * dl)) return 1;
@@ -385,7 +430,7 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
         const int k = hit_kind(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext),
                                qc.t0c, qc.t1c, make_ecand(ea, eb), C->d, tin, tout);
         hit = (k == 2);
-        need64 = !hit;
+        need64 = (k == 1);           // k == 0: no shared span (a, b exact in fp32)
     }
     if (__any_sync(FULL, need64) && need64)
         hit = pair64(qa, qb, ea, eb, C->d64, (double)C->T0, (double)C->T1, tin, tout);
@@ -619,7 +664,21 @@ struct RangeArgs {
     const Tile *tiles;
     const uint32_t *item_start;      // [ntiles+1]
     uint32_t ntiles;
+    float df;                        // filter_abs threshold: d * (1 + 2^-20), rounded up
+    float tc;                        // filter_abs time origin (middle of the index's time extent)
 };
+
+// threshold of filter_abs: d (already rounded up) times 1 + 2^-20, rounded up,
+// so the rounding of thr and thr^2 never turns a pass into a reject
+inline float time_origin(const tds_index_s *idx) {
+    return (float)(0.5 * ((double)idx->ext.t_min + (double)idx->ext.t_max));
+}
+
+inline float filter_threshold(float d) {
+    float df = (float)((double)d * (1.0 + 0x1p-20));
+    if ((double)df < (double)d * (1.0 + 0x1p-20)) df = nextafterf(df, INFINITY);
+    return df;
+}
 
 // Pairs of query qid that passed the fp32 filter (lane's candidates j0, j1):
 // certain hits with an accurate fp32 interval are appended; the rest is queued
@@ -658,7 +717,8 @@ __device__ __forceinline__ uint32_t handle_passed(const PairCtx *C, WarpState *W
 }
 
 struct __align__(16) RangeWarpSmem {
-    float4 q[32][3];                 // group query constants: (p0,t0) (v,ext) (t0c,t1c,lo,hi)
+    float4 q[32][6];                 // group query constants: (p0,t0) (v,ext) (t0c,t1c,lo,hi)
+                                     // and the absolute form (c,m) (v,t0c') (t1c',lo,hi,-)
     WarpState ws;
     uint32_t qn;                     // refine queue fill
 };
@@ -680,6 +740,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     const uint32_t total = A.item_start[A.ntiles];
     const uint32_t CH = st->ch;
     const float d = A.pc.d;
+    const float df = A.df;
     warp_state_init(W.ws, lane);
     if (lane == 0) W.qn = 0;
     __syncwarp();
@@ -710,10 +771,14 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f);
             if (active) { qa = __ldg(A.pc.Q + 2 * (uint64_t)S.qid); qb = __ldg(A.pc.Q + 2 * (uint64_t)S.qid + 1); }
             const QConst qc = make_qconst(qa, qb, A.pc.T0, A.pc.T1);
+            const FSeg qf = make_fseg(qa, qb, A.tc);
             __syncwarp();
             W.q[lane][0] = make_float4(qc.px, qc.py, qc.pz, qc.t0);
             W.q[lane][1] = make_float4(qc.vx, qc.vy, qc.vz, qc.ext);
             W.q[lane][2] = make_float4(qc.t0c, qc.t1c, __uint_as_float(my_lo), __uint_as_float(my_hi));
+            W.q[lane][3] = make_float4(qf.cx, qf.cy, qf.cz, qf.m);
+            W.q[lane][4] = make_float4(qf.vx, qf.vy, qf.vz, qc.t0c - A.tc);
+            W.q[lane][5] = make_float4(qc.t1c - A.tc, __uint_as_float(my_lo), __uint_as_float(my_hi), 0.f);
             __syncwarp();
         }
         uint32_t wlo = my_lo, whi = my_hi;
@@ -754,9 +819,9 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 a1 = __ldg(A.pc.rec + 2 * (uint64_t)j1);
                 b1 = __ldg(A.pc.rec + 2 * (uint64_t)j1 + 1);
             }
-            const ECand e0 = make_ecand(a0, b0), e1 = make_ecand(a1, b1);
             exec += (unsigned long long)(cend - base) * __popc(mask);
             if (dense) {
+                const ECand e0 = make_ecand(a0, b0), e1 = make_ecand(a1, b1);
                 // output-bound regime (last window was dense): fused filter + certain-hit
                 // interval per pair, no recomputation
                 uint32_t passes = 0;
@@ -800,20 +865,26 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 base = cend;
                 continue;
             }
+            const FSeg f0 = make_fseg(a0, b0, A.tc), f1 = make_fseg(a1, b1, A.tc);
             while (mask) {
                 const int g = __ffs(mask) - 1;
                 mask &= mask - 1;
-                const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
+                const float4 n0 = W.q[g][3], n1 = W.q[g][4], n2 = W.q[g][5];
+                const uint32_t glo = __float_as_uint(n2.y), ghi = __float_as_uint(n2.z);
                 // branch-free (bitwise &): no divergent branch around each filter
-                const bool m0 = (v0 & (c0 >= glo) & (c0 < ghi)) & filter_pair(q0, q1, q2.x, q2.y, e0, d);
-                const bool m1 = (v1 & (c1 >= glo) & (c1 < ghi)) & filter_pair(q0, q1, q2.x, q2.y, e1, d);
+                // (c < ghi <= whi implies c < cend: no separate validity test)
+                const bool m0 = (c0 - glo < ghi - glo) & filter_abs(n0, n1, n1.w, n2.x, f0, df);
+                const bool m1 = (c1 - glo < ghi - glo) & filter_abs(n0, n1, n1.w, n2.x, f1, df);
                 if (!__any_sync(FULL, m0 | m1)) continue;
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 if (__popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) >= DIRECT_MIN) {
                     // dense: most lanes passed -> in place (fp32 interval or fp64 queue); the
-                    // following windows use the fused path
+                    // following windows use the fused path.  Candidates are re-read (L1) in
+                    // the relative form the interval needs.
                     dense = true;
+                    const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
+                    const ECand e0 = make_ecand(__ldg(A.pc.rec + 2 * (uint64_t)j0), __ldg(A.pc.rec + 2 * (uint64_t)j0 + 1));
+                    const ECand e1 = make_ecand(__ldg(A.pc.rec + 2 * (uint64_t)j1), __ldg(A.pc.rec + 2 * (uint64_t)j1 + 1));
                     const uint32_t hits_g =
                         handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, m0, m1, q0, q1, q2.x, q2.y, qid, j0, j1, e0, e1);
                     direct_hits += hits_g;
@@ -1421,6 +1492,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     tm.mark(2);
     if (!spatial) {
         RangeArgs a{};
+        a.df = filter_threshold(d);
+        a.tc = time_origin(idx);
         a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
         for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
@@ -1613,6 +1686,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             DBuf<uint32_t> bis;
             uint32_t bnt = plan_items(rsched.p + b0, 0, b1 - b0, bst.p, bt, bis, s);
             RangeArgs a{};
+            a.df = filter_threshold(d);
+            a.tc = time_origin(idx);
             a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
             a.pc.o.st = bst.p;
             for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];

@@ -320,3 +320,25 @@ def test_time_partitioned_union_equals_single_index(tds, world):
         kb = np.sort(np.concatenate(parts))
         assert np.unique(kb).size == kb.size
         assert np.array_equal(ka, kb)
+
+
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal", "spatial"])
+def test_touching_spans_dense_window(tds, kind):
+    """C5 on the in-place (dense window) path: 200 entries whose spans touch the
+    query's span at one instant (t_end = 1 or t_start = 2) sit next to 200 that
+    overlap it, all within d of the stationary query; only the overlapping ones
+    interact.  (The fp32 filter passes touching spans; the later stages decide.)"""
+    import torch
+    rng = np.random.default_rng(7)
+    n = 200
+    pos = rng.uniform(-0.1, 0.1, (3 * n, 3)).astype(np.float32)
+    t0 = np.concatenate([np.full(n, 0.0), np.full(n, 2.0), rng.uniform(0.5, 1.5, n)]).astype(np.float32)
+    t1 = np.concatenate([np.full(n, 1.0), np.full(n, 3.0), t0[2 * n:] + 1.0]).astype(np.float32)
+    order = rng.permutation(3 * n)
+    D = np.concatenate([pos, t0[:, None], pos, t1[:, None]], axis=1)[order].astype(np.float32)
+    Q = np.array([[0, 0, 0, 1.0, 0, 0, 0, 2.0]], np.float32)
+    ref = oracle.search(D, Q, 1.0)
+    idx = tds.Index(_cuda(D), kinds=tds.ALL, m=4, v=1, grid=(4, 4, 4))
+    got = idx.search(_cuda(Q), 1.0, kind=kind).fetch(sorted=True, device=False)
+    rep = check(got, ref, D, Q, 1.0, label=f"touching {kind}")
+    assert rep["pairs"] == n
