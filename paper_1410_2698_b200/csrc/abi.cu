@@ -159,6 +159,8 @@ void Trace::mark(const char *name) {
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
     ev.emplace_back(name, e);
+    host_ms.push_back(std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now().time_since_epoch()).count());
 }
 
 Trace::~Trace() {
@@ -169,8 +171,24 @@ Trace::~Trace() {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
         char b[96];
-        snprintf(b, sizeof b, " %s %.3f", ev[i].first, ms);
+        snprintf(b, sizeof b, " %s %.3f (host %.3f)", ev[i].first, ms, host_ms[i] - host_ms[i - 1]);
         line += b;
+    }
+    {   // pool reservations (GB): default pool, result pool
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pools[2] = {nullptr, big_pool()};
+        cudaDeviceGetDefaultMemPool(&pools[0], dev);
+        for (cudaMemPool_t pool : pools) {
+            uint64_t reserved = 0, used = 0;
+            if (pool) {
+                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+            }
+            char b[64];
+            snprintf(b, sizeof b, " | pool %.2f/%.2f GB", used / 1e9, reserved / 1e9);
+            line += b;
+        }
     }
     fprintf(stderr, "%s\n", line.c_str());
     for (auto &x : ev) cudaEventDestroy(x.second);

@@ -10,6 +10,7 @@
 //                              subbin in (slab, bin) lexicographic order)
 //   A4 FSG                     P:282-361 (rasterise each MBB to cells; lookup array A)
 #include <float.h>
+#include <stdlib.h>
 #include <vector>
 #include <algorithm>
 
@@ -336,9 +337,10 @@ __global__ void k_subbin_offsets(const uint32_t *__restrict__ keys, uint64_t len
 
 // group (key, val) pairs by key with a stable radix sort; vals -> out ids,
 // offsets of the nk buckets -> off[nk+1]
-void group_by_key(uint32_t *keys, uint32_t *vals, uint64_t len, uint64_t nk, uint32_t *off, cudaStream_t s) {
+void group_by_key(DBuf<uint32_t> &keys, DBuf<uint32_t> &vals, uint64_t len, uint64_t nk, uint32_t *off,
+                  cudaStream_t s) {
     radix_sort_pairs(keys, vals, len, 0, bits_for(nk), s);
-    k_bucket_offsets<<<nblk(len + 1), NT, 0, s>>>(keys, len, (uint32_t)nk, off);
+    k_bucket_offsets<<<nblk(len + 1), NT, 0, s>>>(keys.p, len, (uint32_t)nk, off);
     TDS_CHECK_LAUNCH();
 }
 
@@ -478,10 +480,16 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     }
 
     tr.mark("counts+sync");
-    // ---- phase 2: the three subbin arrays and the FSG are independent: build them
-    // concurrently on forked streams (joined before returning)
+    // ---- phase 2: the three subbin arrays and the FSG are independent (optionally
+    // built concurrently on forked streams, joined before returning)
     cudaStream_t side[4];
     side_streams(side);
+    // one stream by default: on B200 the fork/join and cross-stream pool reuse cost
+    // more than the overlap gains (Random-1M build 0.62 vs 0.78 ms; Random-dense
+    // within noise); TDS_BUILD_CONCURRENT=1 forks the four builds onto side streams
+    static const bool concurrent = getenv("TDS_BUILD_CONCURRENT") && getenv("TDS_BUILD_CONCURRENT")[0] == '1';
+    if (!concurrent)
+        for (auto &ss : side) ss = s;
     cudaEvent_t fork = fork_event();
     TDS_CUDA(cudaEventRecord(fork, s));
     for (auto ss : side) TDS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
@@ -498,7 +506,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
             TDS_CHECK_LAUNCH();
             // emitted in sorted-position order, so within a slab the bins are already
             // ascending: a stable sort on the slab bits alone groups the subbins
-            radix_sort_pairs(k2.p, v2.p, len, mbits, mbits + bits_for((uint64_t)v), sc);
+            radix_sort_pairs(k2, v2, len, mbits, mbits + bits_for((uint64_t)v), sc);
             k_subbin_offsets<<<nblk((uint64_t)v * m + 1), NT, 0, sc>>>(k2.p, len, v, m, mbits, off.p);
             TDS_CHECK_LAUNCH();
             st_pos[c].s = sc;                      // free after its last use, on that stream
@@ -517,7 +525,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         DBuf<uint32_t> k2(len, sf), v2(len, sf), off(ncell + 1, sf);
         k_cell_emit<<<nblk(n), NT, 0, sf>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
         TDS_CHECK_LAUNCH();
-        group_by_key(k2.p, v2.p, len, ncell, off.p, sf);
+        group_by_key(k2, v2, len, ncell, off.p, sf);
         DBuf<uint2> ecell(len, sf);
         DBuf<float4> frec(2 * len, sf);
         DBuf<uint32_t> fperm(len, sf);

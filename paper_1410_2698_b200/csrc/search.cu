@@ -494,9 +494,9 @@ struct SchedArgs {
     float st_o[3], st_w[3];
     int use_st;
     Sched *out;
-    uint32_t *keys;                  // sort keys: category << lo_bits | lo
+    uint32_t *keys;                  // sort keys: category << 13 | lo >> lo_shift (16 bits)
     uint32_t *vals;                  // identity (sort payload)
-    int lo_bits;
+    int lo_shift;
     DevStats *st;
 };
 
@@ -567,7 +567,7 @@ __global__ void k_schedule(SchedArgs A) {
             }
         }
         A.out[p] = S;
-        A.keys[p] = ((uint32_t)(S.sel + 1) << A.lo_bits) | S.lo;
+        A.keys[p] = ((uint32_t)(S.sel + 1) << 13) | (S.lo >> A.lo_shift);
         A.vals[p] = p;
         atomicAdd(&A.st->cat_cnt[S.sel + 1], 1u);
     }
@@ -1396,14 +1396,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             for (int c = 0; c < 3; ++c) lo_max = std::max<uint64_t>(lo_max, idx->st_len[c]);
         int lo_bits = 1;
         while ((1ull << lo_bits) <= lo_max) ++lo_bits;
-        if (lo_bits > 29) fail(TDS_EINVAL, "index too large for the 32-bit schedule key (%llu)",
-                               (unsigned long long)lo_max);
-        a.lo_bits = lo_bits;
+        // the order only shapes the groups of 32 (the category must be exact): the
+        // top 13 bits of the range start suffice, so the key has 16 bits = 2 passes
+        a.lo_shift = std::max(0, lo_bits - 13);
         a.st = dst.p;
         k_schedule<<<nblk(n), 256, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
         // sort S by (array selector, range start): one stable radix sort
-        radix_sort_pairs(keys.p, order.p, n, 0, lo_bits + 3, s);
+        radix_sort_pairs(keys.p, order.p, n, 0, 16, s);
         {
             DBuf<Sched> tmp(n, s);
             k_permute_sched<<<nblk(n), 256, 0, s>>>(sched.p, order.p, n, tmp.p);

@@ -461,14 +461,13 @@ void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t 
     exclusive_scan_impl<uint64_t>(in, out, n, d_total, s);
 }
 
-void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit, cudaStream_t s) {
-    if (n <= 1 || end_bit <= begin_bit) return;
-    if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
+// the passes; returns true if the sorted data ended in (k2, v2) (odd pass count)
+static bool radix_sort_passes(uint32_t *keys, uint32_t *vals, uint32_t *k2p, uint32_t *v2p, uint64_t n,
+                              int begin_bit, int end_bit, cudaStream_t s) {
     const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
     const uint32_t os_tiles = (uint32_t)((n + OS_TILE - 1) / OS_TILE);
     const int npass = (end_bit - begin_bit + 7) / 8;
-    DBuf<uint32_t> k2(n, s), v2(n, s);
-    uint32_t *ka = keys, *va = vals, *kb = k2.p, *vb = v2.p;
+    uint32_t *ka = keys, *va = vals, *kb = k2p, *vb = v2p;
     if (n < (1ull << 30)) {
         // onesweep: 1 upsweep + 1 scatter per digit
         const uint64_t status_words = (uint64_t)npass * os_tiles * 256;
@@ -509,9 +508,30 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit,
             std::swap(va, vb);
         }
     }
-    if (npass & 1) {
-        TDS_CUDA(cudaMemcpyAsync(keys, ka, n * 4, cudaMemcpyDeviceToDevice, s));
-        TDS_CUDA(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, s));
+    return (npass & 1) != 0;
+}
+
+void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit, cudaStream_t s) {
+    if (n <= 1 || end_bit <= begin_bit) return;
+    if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
+    DBuf<uint32_t> k2(n, s), v2(n, s);
+    if (radix_sort_passes(keys, vals, k2.p, v2.p, n, begin_bit, end_bit, s)) {
+        TDS_CUDA(cudaMemcpyAsync(keys, k2.p, n * 4, cudaMemcpyDeviceToDevice, s));
+        TDS_CUDA(cudaMemcpyAsync(vals, v2.p, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// same, owning buffers: an odd pass count swaps the buffers instead of copying back
+void radix_sort_pairs(DBuf<uint32_t> &keys, DBuf<uint32_t> &vals, uint64_t n, int begin_bit, int end_bit,
+                      cudaStream_t s) {
+    if (n <= 1 || end_bit <= begin_bit) return;
+    if (n >= (1ull << 32)) fail(TDS_EINVAL, "radix_sort_pairs: n too large");
+    DBuf<uint32_t> k2(keys.n, s), v2(vals.n, s);
+    if (radix_sort_passes(keys.p, vals.p, k2.p, v2.p, n, begin_bit, end_bit, s)) {
+        std::swap(keys.p, k2.p);
+        std::swap(vals.p, v2.p);
+        k2.s = keys.s; v2.s = vals.s;          // free the old buffers on their own streams
+        keys.s = s; vals.s = s;
     }
 }
 

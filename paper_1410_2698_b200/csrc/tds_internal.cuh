@@ -157,6 +157,8 @@ __host__ __device__ __forceinline__ uint32_t pack_cell(int x, int y, int z) {
 // keys/vals are sorted in place (double-buffered with caller-free temporaries).
 void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit,
                       cudaStream_t s);
+void radix_sort_pairs(DBuf<uint32_t> &keys, DBuf<uint32_t> &vals, uint64_t n, int begin_bit, int end_bit,
+                      cudaStream_t s);
 // Exclusive scan of n uint32 values into out (out may alias in); optional
 // total written to *d_total (device pointer, may be null).  64-bit variant too.
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *d_total,
@@ -181,6 +183,7 @@ struct Trace {
     bool on = false;
     cudaStream_t s = 0;
     std::vector<std::pair<const char *, cudaEvent_t>> ev;
+    std::vector<double> host_ms;       // host wall clock at each mark
     explicit Trace(cudaStream_t s_);
     void mark(const char *name);
     ~Trace();

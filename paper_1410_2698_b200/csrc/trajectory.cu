@@ -140,13 +140,13 @@ void merge_trajectories(tds_result_s *r, const uint32_t *q_traj, uint64_t nq, co
     DBuf<uint32_t> keys(n, s), ord(n, s), ord2(n, s);
     k_traj_key<<<nblk(n), 256, 0, s>>>(rs, nullptr, n, 0, q_traj, e_traj, keys.p, ord.p);
     TDS_CHECK_LAUNCH();
-    radix_sort_pairs(keys.p, ord.p, n, 0, 32, s);
+    radix_sort_pairs(keys, ord, n, 0, 32, s);
     k_traj_key<<<nblk(n), 256, 0, s>>>(rs, ord.p, n, 1, q_traj, e_traj, keys.p, ord2.p);
     TDS_CHECK_LAUNCH();
-    radix_sort_pairs(keys.p, ord2.p, n, 0, bits(hmx[1]), s);
+    radix_sort_pairs(keys, ord2, n, 0, bits(hmx[1]), s);
     k_traj_key<<<nblk(n), 256, 0, s>>>(rs, ord2.p, n, 2, q_traj, e_traj, keys.p, ord.p);
     TDS_CHECK_LAUNCH();
-    radix_sort_pairs(keys.p, ord.p, n, 0, bits(hmx[0]), s);
+    radix_sort_pairs(keys, ord, n, 0, bits(hmx[0]), s);
     // sorted records with trajectory ids, group heads, group starts
     DBuf<Rec> srt(n, s, n * sizeof(Rec) > (256ull << 20));
     DBuf<uint32_t> head(n + 1, s), gid(n + 1, s);
