@@ -34,6 +34,7 @@ VARIANTS = ("temporal", "spatiotemporal", "spatial")
 # algorithmic work of one pair test: the certified fp32 filter of DESIGN.md
 # ("Pair test numerics"): 43 FP32 instructions, 16 of them FFMA -> 59 flops
 FLOPS_PER_PAIR = 59
+BYTES_PER_SPATIAL_PAIR = 36          # GPUSpatial: 32-B record + 4-B id streamed per pair test
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -42,6 +43,18 @@ def load_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def ncu_traffic(args, kname, variant):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    ncu --set full capture of the same configuration (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py), else None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        key = f"{args.config}|{args.d if args.d is not None else 'default'}|{kname}|{variant}"
+        return t[key]["dram_bytes"]
+    except Exception:
+        return None
 
 
 def fp32_peak_tflops(peaks, n_sms=148):
@@ -356,17 +369,30 @@ def run_tds(args, ws, rank, local):
     search_ms = searches_ms
     pt_all = pair_tests_step if dist is None else sum_over_ranks(dist, float(pair_tests_step), dev)
     peaks = load_peaks()
-    # roofline of the dominant kernel: the pair kernel with the largest share
+    # roofline of the dominant kernel: the pair kernel with the largest share.  The
+    # range kernels (GPUTemporal / GPUSpatioTemporal) reuse each loaded record for
+    # up to 32 queries and are bound by the FP32 ALUs (59 flops per scheduled pair
+    # test); GPUSpatial streams one record + id per pair test (FSG slices are per
+    # (query, cell)) and is bound by HBM (36 B per pair test).
     dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
     dk = per_kind[dom]
-    achieved = FLOPS_PER_PAIR * dk["pair_tests"] / (dk["pair_kernel_ms"] / 1e3) / 1e12
-    peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
-    roof = {"bound": "alu", "kernel": f"k_pair_{'spatial' if dom == 'spatial' else 'range'} ({dom})",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None,
-            "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
-                           "algorithmic 59 flops per scheduled pair test",
-            "share_of_step": dk["pair_kernel_ms"] / statistics.median(step_ms)}
+    kname = "k_pair_spatial" if dom == "spatial" else "k_pair_range"
+    secs = dk["pair_kernel_ms"] / 1e3
+    if dom == "spatial":
+        achieved = BYTES_PER_SPATIAL_PAIR * dk["pair_tests"] / secs / 1e9
+        peak = float(peaks.get("hbm_gbs", 6537.0))
+        roof = {"bound": "hbm", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); algorithmic 36 B (record + id) per pair test"}
+    else:
+        achieved = FLOPS_PER_PAIR * dk["pair_tests"] / secs / 1e12
+        peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
+        roof = {"bound": "alu", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s",
+                "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
+                               "algorithmic 59 flops per scheduled pair test"}
+    roof["frac"] = achieved / peak
+    roof["traffic"] = ncu_traffic(args, kname, dom)
+    roof["share_of_step"] = dk["pair_kernel_ms"] / statistics.median(step_ms)
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
