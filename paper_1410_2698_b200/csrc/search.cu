@@ -489,6 +489,9 @@ struct PairCtx {                     // what the fp64 path needs
 };
 
 // Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
+// Out of line: called once per 32 queued pairs from several sites of the pair
+// kernels; inlining it (and pair64) at each site bloated the kernels past the
+// instruction cache (ncu: no_instruction stalls on output-bound searches).
 template <bool EXACT>
 __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n) {
     const int lane = threadIdx.x & 31;
@@ -949,8 +952,12 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     load_cand(c2, c2 < cend, j2, a, b);
                     load_cand(c3, c3 < cend, j3, a, b);
                 }
-                uint32_t passes = dense_pair(mask, c0, c1, cend, j0, j1);
-                if (base + 64 < cend) passes += dense_pair(mask, c2, c3, cend, j2, j3);
+                uint32_t passes = 0;
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {      // one copy of the dense code (i-cache)
+                    if (h && base + 64 >= cend) break;
+                    passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
+                }
                 dense = passes >= (uint32_t)DIRECT_MIN * __popc(wmask) * 2u;
                 base = cend;
                 continue;
@@ -990,10 +997,13 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     // the relative form the interval needs.
                     dense = true;
                     const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                    uint32_t hits_g = handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, m0, m1, q0, q1, q2.x, q2.y, qid, j0,
-                                                           j1, ecand_of(j0), ecand_of(j1));
-                    hits_g += handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, m2, m3, q0, q1, q2.x, q2.y, qid, j2, j3,
-                                                   ecand_of(j2), ecand_of(j3));
+                    uint32_t hits_g = 0;
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {  // one copy of the in-place code (i-cache)
+                        const uint32_t ja = h ? j2 : j0, jb = h ? j3 : j1;
+                        hits_g += handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, h ? m2 : m0, h ? m3 : m1, q0, q1, q2.x,
+                                                       q2.y, qid, ja, jb, ecand_of(ja), ecand_of(jb));
+                    }
                     direct_hits += hits_g;
                     if (lane == g) owner_hits += hits_g;
                 } else {
