@@ -340,6 +340,95 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     return (in_ok && out_ok) ? 2 : 1;
 }
 
+// hit_kind<true> for two candidates at once (dense windows): the same arithmetic
+// and the same first-order bound per candidate, with the elementwise work in
+// packed fp32x2 and no early exits (both candidates are resolved together).
+// Returns the kinds through k0 / k1 (0 = miss, 1 = fp64, 2 = certain hit).
+__device__ __forceinline__ void hit_kind2(float4 q0, float4 q1, float t0c, float t1c, const ECand &e0, const ECand &e1,
+                                          float d, int &k0, float &tin0, float &tout0, int &k1, float &tin1,
+                                          float &tout1) {
+    constexpr float U = 1.0f / 16777216.0f;
+    const float a0 = fmaxf(t0c, e0.t0), b0 = fminf(t1c, e0.t1);
+    const float a1 = fmaxf(t0c, e1.t0), b1 = fminf(t1c, e1.t1);
+    const f32x2 a = pk2(a0, a1), et0 = pk2(e0.t0, e1.t0);
+    const f32x2 aq = sub2(a, bc2(q0.w)), nae = sub2(et0, a);          // a - t0q, -(a - t0e) (exact negation)
+    const f32x2 dpx = sub2(bc2(q0.x), pk2(e0.px, e1.px)), dpy = sub2(bc2(q0.y), pk2(e0.py, e1.py)),
+                dpz = sub2(bc2(q0.z), pk2(e0.pz, e1.pz));
+    const f32x2 evx = pk2(e0.vx, e1.vx), evy = pk2(e0.vy, e1.vy), evz = pk2(e0.vz, e1.vz);
+    const f32x2 Dx = fma2(nae, evx, fma2(aq, bc2(q1.x), dpx));
+    const f32x2 Dy = fma2(nae, evy, fma2(aq, bc2(q1.y), dpy));
+    const f32x2 Dz = fma2(nae, evz, fma2(aq, bc2(q1.z), dpz));
+    const f32x2 Vx = sub2(bc2(q1.x), evx), Vy = sub2(bc2(q1.y), evy), Vz = sub2(bc2(q1.z), evz);
+    const f32x2 L = sub2(pk2(b0, b1), a);
+    const f32x2 A = fma2(Vx, Vx, fma2(Vy, Vy, mul2(Vz, Vz)));
+    const f32x2 B = fma2(Dx, Vx, fma2(Dy, Vy, mul2(Dz, Vz)));
+    float A0, A1, L0, L1, P0, P1;
+    upk2(A, A0, A1);
+    upk2(L, L0, L1);
+    const float rA0 = rcp_approx(A0), rA1 = rcp_approx(A1);
+    const f32x2 rA = pk2(rA0, rA1);
+    upk2(mul2(B, rA), P0, P1);
+    const float su0 = -P0, su1 = -P1;
+    const f32x2 su = pk2(su0, su1);
+    const f32x2 s = pk2(fminf(fmaxf(su0, 0.f), L0), fminf(fmaxf(su1, 0.f), L1));
+    const f32x2 yx = fma2(s, Vx, Dx), yy = fma2(s, Vy, Dy), yz = fma2(s, Vz, Dz);
+    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
+    float x0, x1, y0, y1, z0, z1;
+    upk2(dpx, x0, x1);
+    upk2(dpy, y0, y1);
+    upk2(dpz, z0, z1);
+    const f32x2 M = add2(pk2(fabsf(x0) + fabsf(y0) + fabsf(z0), fabsf(x1) + fabsf(y1) + fabsf(z1)),
+                         add2(bc2(q1.w), pk2(e0.ext, e1.ext)));
+    const f32x2 thr = fma2(bc2(KU), M, bc2(d));
+    const f32x2 dl = fma2(bc2(-KU), M, bc2(d));
+    float h0, h1, th0, th1, dl0, dl1;
+    upk2(h, h0, h1);
+    upk2(mul2(thr, thr), th0, th1);
+    upk2(dl, dl0, dl1);
+    const bool pass0 = (a0 < b0) & (h0 <= th0), pass1 = (a1 < b1) & (h1 <= th1);
+    const bool cert0 = (dl0 > 0.f) & (h0 < dl0 * dl0), cert1 = (dl1 > 0.f) & (h1 < dl1 * dl1);
+    // interval and its bound (as hit_kind)
+    const f32x2 ux = fma2(su, Vx, Dx), uy = fma2(su, Vy, Dy), uz = fma2(su, Vz, Dz);
+    const f32x2 hu = fma2(ux, ux, fma2(uy, uy, mul2(uz, uz)));
+    const float d2 = d * d;
+    float r0, r1;
+    upk2(sub2(bc2(d2), hu), r0, r1);
+    const f32x2 rem = pk2(fmaxf(r0, 0.f), fmaxf(r1, 0.f));
+    float wq0, wq1;
+    upk2(mul2(rem, rA), wq0, wq1);
+    const f32x2 w = pk2(sqrt_approx(wq0), sqrt_approx(wq1));
+    const f32x2 V1 = pk2(fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e0.vx) + fabsf(e0.vy) + fabsf(e0.vz),
+                         fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e1.vx) + fabsf(e1.vy) + fabsf(e1.vz));
+    const f32x2 rsA = pk2(rsqrt_approx(A0), rsqrt_approx(A1));
+    const f32x2 asu = pk2(fabsf(su0), fabsf(su1));
+    const f32x2 Su = pk2(fmaxf(fabsf(su0), L0), fmaxf(fabsf(su1), L1));
+    const f32x2 Mu = fma2(Su, V1, M);
+    const f32x2 relA = fma2(mul2(bc2(12.f * U), V1), rsA, bc2(5.f * U));
+    const f32x2 dsu = fma2(asu, relA, fma2(mul2(mul2(bc2(6.f * U), V1), Mu), rA, mul2(mul2(bc2(14.f * U), Mu), rsA)));
+    const f32x2 drem = fma2(bc2(2.f * U), add2(bc2(d2), rem), fma2(mul2(A, dsu), dsu, mul2(bc2(28.f * U * d), Mu)));
+    float rm0, rm1;
+    upk2(rem, rm0, rm1);
+    const f32x2 rr = pk2(rcp_approx(rm0), rcp_approx(rm1));
+    const f32x2 dw = mul2(w, add2(fma2(mul2(bc2(0.5f), drem), rr, mul2(bc2(0.5f), relA)), bc2(4.f * U)));
+    const f32x2 dst = mul2(bc2(2.f), add2(dsu, dw));
+    float w0, w1, ds0, ds1;
+    upk2(w, w0, w1);
+    upk2(dst, ds0, ds1);
+    const float lo0 = su0 - w0, hi0 = su0 + w0, lo1 = su1 - w1, hi1 = su1 + w1;
+    tin0 = a0 + fminf(fmaxf(lo0, 0.f), L0);
+    tout0 = a0 + fminf(fmaxf(hi0, 0.f), L0);
+    tin1 = a1 + fminf(fmaxf(lo1, 0.f), L1);
+    tout1 = a1 + fminf(fmaxf(hi1, 0.f), L1);
+    const float tol0 = 1e-6f * fmaxf(L0, fminf(fabsf(a0), fabsf(b0))) - (4.f * U) * fmaxf(fabsf(a0), fabsf(b0)) -
+                       2.f * U * L0;
+    const float tol1 = 1e-6f * fmaxf(L1, fminf(fabsf(a1), fabsf(b1))) - (4.f * U) * fmaxf(fabsf(a1), fabsf(b1)) -
+                       2.f * U * L1;
+    const bool ok0 = ((lo0 + ds0 < 0.f) | (ds0 <= tol0)) & ((hi0 - ds0 > L0) | (ds0 <= tol0));
+    const bool ok1 = ((lo1 + ds1 < 0.f) | (ds1 <= tol1)) & ((hi1 - ds1 > L1) | (ds1 <= tol1));
+    k0 = pass0 ? ((cert0 & ok0) ? 2 : 1) : 0;
+    k1 = pass1 ? ((cert1 & ok1) ? 2 : 1) : 0;
+}
+
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
 // the sublevel interval of the convex quadratic ||Pq(t)-Pe(t)||^2 <= d^2 on [a,b].
 __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 eb, double d, double T0, double T1,
@@ -896,9 +985,11 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask &= mask - 1;
                 const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
                 const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                float tia = 0.f, toa = 0.f, tib = 0.f, tob = 0.f;
-                const int ka = (va && ca >= glo && ca < ghi) ? hit_kind<true>(q0, q1, q2.x, q2.y, ea, d, tia, toa) : 0;
-                const int kb = (vb && cb >= glo && cb < ghi) ? hit_kind<true>(q0, q1, q2.x, q2.y, eb, d, tib, tob) : 0;
+                float tia, toa, tib, tob;
+                int ka, kb;
+                hit_kind2(q0, q1, q2.x, q2.y, ea, eb, d, ka, tia, toa, kb, tib, tob);
+                if (!(va && ca >= glo && ca < ghi)) ka = 0;
+                if (!(vb && cb >= glo && cb < ghi)) kb = 0;
                 const unsigned pa = __ballot_sync(FULL, ka != 0), pb = __ballot_sync(FULL, kb != 0);
                 passes += __popc(pa) + __popc(pb);
                 if (!(pa | pb)) continue;
@@ -1325,24 +1416,39 @@ __global__ void k_u32_to_u64(const uint32_t *__restrict__ a, uint64_t n, uint64_
 // ---------------------------------------------------------------------------
 // A11: fetch
 // ---------------------------------------------------------------------------
-__global__ void k_fetch_chunked(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+// one warp per chunk; each lane keeps 4 record loads in flight (16 B, streaming:
+// the records are read once) and writes the four SoA columns with streaming
+// stores.  FULL: the whole result is fetched (no per-record range test).
+template <bool FULL>
+__global__ void __launch_bounds__(256) k_fetch_chunked(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
                                 const uint32_t *__restrict__ used, const uint64_t *__restrict__ off, uint64_t first,
                                 uint64_t count, uint32_t *qid, uint32_t *eid, float *tin, float *tout) {
     uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (c >= nchunks) return;
-    uint32_t u = used[c];
-    uint64_t o = off[c];
-    if (o + u <= first || o >= first + count) return;
-    for (uint32_t k = lane; k < u; k += 32) {
-        uint64_t g = o + k;
-        if (g < first || g >= first + count) continue;
-        Rec r = buf[c * CS + k];
-        uint64_t j = g - first;
-        if (qid) qid[j] = r.qid;
-        if (eid) eid[j] = r.eid;
-        if (tin) tin[j] = r.t_in;
-        if (tout) tout[j] = r.t_out;
+    const uint32_t u = used[c];
+    const uint64_t o = off[c];
+    if (!FULL && (o + u <= first || o >= first + count)) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(buf + c * CS);
+    for (uint32_t k0 = 0; k0 < u; k0 += 128) {
+        uint4 r[4];
+        bool v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t k = k0 + lane + 32 * i;
+            v[i] = k < u;
+            if (!FULL) v[i] = v[i] && o + k >= first && o + k < first + count;
+            if (v[i]) r[i] = __ldcs(src + k);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!v[i]) continue;
+            const uint64_t j = o + k0 + lane + 32 * i - first;
+            if (qid) __stcs(qid + j, r[i].x);
+            if (eid) __stcs(eid + j, r[i].y);
+            if (tin) __stcs(reinterpret_cast<uint32_t *>(tin) + j, r[i].z);
+            if (tout) __stcs(reinterpret_cast<uint32_t *>(tout) + j, r[i].w);
+        }
     }
 }
 
@@ -1900,8 +2006,13 @@ void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint3
     }
     if (!sorted) {
         if (r->chunked) {
-            k_fetch_chunked<<<nblk(r->nchunks * 32), 256, 0, s>>>(r->buf, r->CS, r->nchunks, r->chunk_used,
-                                                                  r->chunk_off, first, count, oq, oe, oi, oo);
+            if (first == 0 && count == r->n)
+                k_fetch_chunked<true><<<nblk(r->nchunks * 32), 256, 0, s>>>(r->buf, r->CS, r->nchunks, r->chunk_used,
+                                                                        r->chunk_off, first, count, oq, oe, oi, oo);
+            else
+                k_fetch_chunked<false><<<nblk(r->nchunks * 32), 256, 0, s>>>(r->buf, r->CS, r->nchunks,
+                                                                         r->chunk_used, r->chunk_off, first, count,
+                                                                         oq, oe, oi, oo);
         } else {
             k_fetch_flat<<<nblk(count), 256, 0, s>>>(r->store, nullptr, first, count, oq, oe, oi, oo);
         }
