@@ -342,3 +342,28 @@ def test_touching_spans_dense_window(tds, kind):
     got = idx.search(_cuda(Q), 1.0, kind=kind).fetch(sorted=True, device=False)
     rep = check(got, ref, D, Q, 1.0, label=f"touching {kind}")
     assert rep["pairs"] == n
+
+
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal", "spatial"])
+def test_output_bound_windows(tds, kind):
+    """Output-bound regime (most candidate windows dense: the in-place fp32
+    interval path, hit_kind2, and the fused dense-window mode): 20,000 short
+    random-walk segments in a small box, 300 queries from D, d chosen so that
+    about half of the time-overlapping pairs interact; full comparison."""
+    import torch
+    rng = np.random.default_rng(11)
+    ntraj, nseg = 400, 50
+    start = rng.uniform(0, 4, (ntraj, 1, 3))
+    steps = rng.uniform(-0.2, 0.2, (ntraj, nseg, 3))
+    pos = np.concatenate([start, start + np.cumsum(steps, axis=1)], axis=1)
+    t = np.arange(nseg + 1, dtype=np.float64)[None, :, None] + rng.uniform(0, 3, (ntraj, 1, 1))
+    P = np.concatenate([pos, np.broadcast_to(t, (ntraj, nseg + 1, 1))], axis=2)
+    D = np.concatenate([P[:, :-1, :], P[:, 1:, :]], axis=2).reshape(-1, 8).astype(np.float32)
+    Q = D[rng.choice(D.shape[0], 300, replace=False)]
+    d = 3.0
+    ref = oracle.search(D, Q, d)
+    idx = tds.Index(_cuda(D), kinds=tds.ALL, m=40, v=2, grid=(8, 8, 8))
+    r = idx.search(_cuda(Q), d, kind=kind)
+    got = r.fetch(sorted=True, device=False)
+    rep = check(got, ref, D, Q, d, label=f"output-bound {kind}")
+    assert rep["pairs"] > 90000
