@@ -236,7 +236,8 @@ def config_dict(args, w, ws):
     return {"workload": f"{w.name}-shaped", "n_entries": int(w.D.shape[0]), "n_queries_per_rank": int(w.Q.shape[0]),
             "d": w.d, "m_bins": w.m_bins, "v_subbins": w.v_subbins, "grid": list(w.grid),
             "variants": list(args.variants), "parallelism": f"query-sharded x{ws}, index replicated",
-            "variant_streams": 1 if args.serial else len(args.variants),
+            "variant_streams": 1 if (args.serial and not args.batched) else len(args.variants),
+            "search_api": "tds_search_many" if args.batched else "tds_search",
             "l2": "flushed between steps (256 MiB write); timed steps bracketed by barrier + synchronize",
             "note": w.note}
 
@@ -292,7 +293,28 @@ def run_tds(args, ws, rank, local):
         idx = tds.Index(Dh if host else D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid,
                         stream=stream.cuda_stream)
         ev[1].record(stream)                    # build_index synchronises: the index is ready
-        if args.serial:
+        if args.batched:
+            # one tds_search_many call: the variants run concurrently on side streams
+            # (overlapping their host synchronisations), then each fetches on its stream
+            evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in args.variants]
+            for j in range(len(args.variants)):
+                side[j].wait_stream(stream)
+                evs[j][0].record(side[j])
+            rs = idx.search_many([{"queries": Qh if host else Q, "d": w.d, "kind": k, "capacity": args.capacity,
+                                   "stream": side[j].cuda_stream} for j, k in enumerate(args.variants)])
+            outs = []
+            for j, r in enumerate(rs):
+                with torch.cuda.stream(side[j]):
+                    evs[j][1].record(side[j])
+                    r.fetch(device=not host, stream=side[j].cuda_stream)
+                    evs[j][2].record(side[j])
+                    stt = r.stats()
+                    n = r.count
+                    r.close()
+                outs.append((evs[j], stt, 16 * n))
+            for sj in side:
+                stream.wait_stream(sj)
+        elif args.serial:
             outs = [one_variant(j, k, idx, host) for j, k in enumerate(args.variants)]
         else:
             futs = [pool.submit(one_variant, j, k, idx, host) for j, k in enumerate(args.variants)]
@@ -466,11 +488,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--concurrent", action="store_true",
-                    help="run the variants concurrently (one host thread + stream each)")
+                    help="run the variants concurrently from Python threads (one stream each)")
+    ap.add_argument("--serial-search", action="store_true",
+                    help="one tds_search call per variant, one after another (default: one "
+                         "tds_search_many call running the variants concurrently on side streams)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.variants = VARIANTS if args.variants == "all" else tuple(args.variants.split(","))
     args.serial = not args.concurrent
+    args.batched = not args.concurrent and not args.serial_search
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)

@@ -135,6 +135,35 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
                float t_start, float t_end, uint64_t capacity, void *stream,
                tds_result *out, uint64_t *n_results);
 
+/* one request of tds_search_many: the arguments of tds_search */
+typedef struct tds_search_req {
+    int kind;
+    const tds_seg *queries;
+    uint64_t nq;
+    double d;
+    float t_start, t_end;
+    uint64_t capacity;
+    void *stream;
+} tds_search_req;
+
+/*
+ * tds_search_many — n independent searches of one index (the same operation as
+ * n tds_search calls; serving several query sets, or one set under several
+ * variants).  Requests on distinct streams
+ * run concurrently: each is driven by its own host thread (a persistent
+ * internal pool), so their host synchronisations and launch chains overlap;
+ * requests sharing a stream run one after another in request order.
+ *
+ *   reqs      : n requests (see tds_search for the meaning of each field)
+ *   out       : n result handles (out[i] for reqs[i]; free each with tds_result_free)
+ *   n_results : n counts (may be NULL)
+ * Errors: those of tds_search.  On any failure no result is returned (all are
+ * freed, out[i] = NULL) and the error of the first failing request in request
+ * order is reported.  Synchronises every request stream.
+ */
+int tds_search_many(tds_index idx, int n, const tds_search_req *reqs, tds_result *out,
+                    uint64_t *n_results);
+
 /*
  * tds_fetch_results — copy records [first, first+count) into caller arrays
  * (each `count` long): query_id / entry_id (row numbers of the caller's Q and

@@ -34,7 +34,7 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 # every symbol include/tds.h declares
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
-               "tds_version", "tds_kernel_launches", "tds_merge_trajectories"]
+               "tds_version", "tds_kernel_launches", "tds_merge_trajectories", "tds_search_many"]
 
 
 class TdsError(RuntimeError):
@@ -42,6 +42,13 @@ class TdsError(RuntimeError):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
         self.code = code
         self.status = STATUS.get(code, str(code))
+
+
+class _SearchReq(ctypes.Structure):
+    """tds_search_req (include/tds.h)."""
+    _fields_ = [("kind", ctypes.c_int), ("queries", ctypes.c_void_p), ("nq", ctypes.c_uint64),
+                ("d", ctypes.c_double), ("t_start", ctypes.c_float), ("t_end", ctypes.c_float),
+                ("capacity", ctypes.c_uint64), ("stream", ctypes.c_void_p)]
 
 
 class _Params(ctypes.Structure):
@@ -84,11 +91,12 @@ def load_library(path: str = LIB_PATH):
     lib.tds_version.restype = ctypes.c_char_p
     lib.tds_kernel_launches.restype = ctypes.c_uint64
     lib.tds_index_export.argtypes = [vp, i32, vp, u64, ctypes.POINTER(u64)]
+    lib.tds_search_many.argtypes = [vp, i32, ctypes.POINTER(_SearchReq), ctypes.POINTER(vp), ctypes.POINTER(u64)]
     lib.tds_index_info.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_uint32)]
     for name in ("tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats",
-                 "tds_index_export", "tds_index_info", "tds_merge_trajectories"):
+                 "tds_index_export", "tds_index_info", "tds_merge_trajectories", "tds_search_many"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -172,6 +180,28 @@ class Index:
                               _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
         del keep
         return Result(h, n.value)
+
+    def search_many(self, requests) -> list:
+        """Independent searches of this index in one call (tds_search_many):
+        ``requests`` is a list of dicts with the arguments of ``search`` (queries,
+        d, and optionally window, kind, capacity, stream).  Requests on distinct
+        streams run concurrently; returns one Result per request, in order."""
+        lib = load_library()
+        n = len(requests)
+        reqs = (_SearchReq * max(n, 1))()
+        keep = []
+        for i, r in enumerate(requests):
+            k = r.get("kind", "temporal")
+            ptr, nq, kp = _segments(r["queries"])
+            keep.append(kp)
+            w = r.get("window", (-math.inf, math.inf))
+            reqs[i] = _SearchReq(KINDS[k] if isinstance(k, str) else int(k), ptr, nq, float(r["d"]), float(w[0]),
+                                 float(w[1]), int(r.get("capacity", 0)), _stream_ptr(r.get("stream")))
+        hs = (ctypes.c_void_p * max(n, 1))()
+        ns = (ctypes.c_uint64 * max(n, 1))()
+        _check(lib.tds_search_many(self._h, n, reqs, hs, ns))
+        del keep
+        return [Result(ctypes.c_void_p(hs[i]), ns[i]) for i in range(n)]
 
     def export(self, what: str) -> np.ndarray:
         lib = load_library()

@@ -6,6 +6,12 @@
 #include <new>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "tds_internal.cuh"
 
@@ -39,8 +45,8 @@ void fail(int code, const char *fmt, ...) {
 }
 
 static void init_pool_once() {
-    static bool done = false;
-    if (done) return;
+    static std::atomic<bool> done{false};
+    if (done.load(std::memory_order_acquire)) return;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
@@ -48,7 +54,7 @@ static void init_pool_once() {
         uint64_t thr = UINT64_MAX;   // keep freed memory in the pool (no re-mapping per search)
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    done = true;
+    done.store(true, std::memory_order_release);
 }
 
 void *dalloc(size_t bytes, cudaStream_t s) {
@@ -73,8 +79,10 @@ void dfree(void *p, cudaStream_t s) {
 static cudaMemPool_t big_pool() {
     static cudaMemPool_t pool = nullptr;
     static int dev_of_pool = -1;
+    static std::mutex mu;                     // concurrent searches (tds_search_many)
     int dev = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
     if (pool && dev_of_pool == dev) return pool;
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
@@ -337,6 +345,112 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
     }
     *out = r;
     if (n_results) *n_results = r->n;
+    return TDS_OK;
+    ABI_CATCH
+}
+
+}  // extern "C"
+
+namespace {
+
+// persistent worker threads for tds_search_many (detached; they wait on a queue)
+class SearchPool {
+  public:
+    void run(std::vector<std::function<void()>> &tasks) {
+        if (tasks.empty()) return;
+        std::mutex m;
+        std::condition_variable cv;
+        size_t left = tasks.size() - 1;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while (idle_ < (int)left) {
+                std::thread(&SearchPool::loop, this).detach();
+                ++idle_;
+            }
+            idle_ -= (int)left;
+            for (size_t i = 1; i < tasks.size(); ++i)
+                q_.push_back([&, i] {
+                    tasks[i]();
+                    std::lock_guard<std::mutex> l2(m);
+                    if (--left == 0) cv.notify_one();
+                });
+        }
+        cv_.notify_all();
+        tasks[0]();                           // the caller drives the first request
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return left == 0; });
+    }
+
+  private:
+    void loop() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !q_.empty(); });
+                f = std::move(q_.front());
+                q_.pop_front();
+            }
+            f();
+            std::lock_guard<std::mutex> lk(mu_);
+            ++idle_;
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    int idle_ = 0;
+};
+
+SearchPool &search_pool() {
+    static SearchPool *p = new SearchPool();  // never destroyed: workers are detached
+    return *p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tds_search_many(tds_index idx, int n, const tds_search_req *reqs, tds_result *out, uint64_t *n_results) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (n < 0 || (n > 0 && (!reqs || !out))) fail(TDS_EINVAL, "bad request list");
+    for (int i = 0; i < n; ++i) out[i] = nullptr;
+    if (n == 0) return TDS_OK;
+    // requests sharing a stream form one serial lane (request order kept)
+    std::vector<std::vector<int>> lanes;
+    for (int i = 0; i < n; ++i) {
+        size_t k = 0;
+        while (k < lanes.size() && reqs[lanes[k][0]].stream != reqs[i].stream) ++k;
+        if (k == lanes.size()) lanes.emplace_back();
+        lanes[k].push_back(i);
+    }
+    std::vector<int> code(n, TDS_OK);
+    std::vector<std::string> msg(n);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::vector<std::function<void()>> tasks;
+    for (auto &lane : lanes)
+        tasks.push_back([&, lane] {
+            cudaSetDevice(dev);
+            for (int i : lane) {
+                const tds_search_req &r = reqs[i];
+                code[i] = tds_search(idx, r.kind, r.queries, r.nq, r.d, r.t_start, r.t_end, r.capacity, r.stream,
+                                     &out[i], n_results ? &n_results[i] : nullptr);
+                if (code[i] != TDS_OK) {
+                    msg[i] = tds_last_error();
+                    break;
+                }
+            }
+        });
+    search_pool().run(tasks);
+    for (int i = 0; i < n; ++i)
+        if (code[i] != TDS_OK) {
+            for (int j = 0; j < n; ++j)
+                if (out[j]) { tds_result_free(out[j]); out[j] = nullptr; }
+            tds::set_error(code[i], "%s", msg[i].c_str());
+            return code[i];
+        }
     return TDS_OK;
     ABI_CATCH
 }

@@ -367,3 +367,39 @@ def test_output_bound_windows(tds, kind):
     got = r.fetch(sorted=True, device=False)
     rep = check(got, ref, D, Q, d, label=f"output-bound {kind}")
     assert rep["pairs"] > 90000
+
+
+def test_search_many_equals_single_searches(tds):
+    """tds_search_many: the three variants concurrently on three streams, plus two
+    requests sharing a stream (a serial lane), give exactly the single searches'
+    records (same pair sets, same endpoints bit for bit)."""
+    import torch
+    w = synth.random_1m(n_traj=300)
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=1000, v=2)
+    Q = _cuda(w.Q)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    reqs = [{"queries": Q, "d": 25.0, "kind": k, "stream": streams[j].cuda_stream}
+            for j, k in enumerate(("temporal", "spatiotemporal", "spatial"))]
+    reqs.append({"queries": Q[: Q.shape[0] // 2], "d": 10.0, "kind": "temporal", "window": (20.0, 60.0),
+                 "stream": streams[0].cuda_stream})
+    many = idx.search_many(reqs)
+    torch.cuda.synchronize()
+    for r, res in zip(reqs, many):
+        one = idx.search(r["queries"], r["d"], kind=r["kind"], window=r.get("window", (-np.inf, np.inf)))
+        a = res.fetch(sorted=True, device=False)
+        b = one.fetch(sorted=True, device=False)
+        assert len(a[0]) == len(b[0]) > 0
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+def test_search_many_error_frees_all(tds):
+    import torch
+    w = synth.tiny()
+    idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL, m=10)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with pytest.raises(tds.TdsError) as ei:
+        idx.search_many([{"queries": _cuda(w.Q), "d": w.d, "kind": "temporal", "stream": s1.cuda_stream},
+                         {"queries": _cuda(w.Q), "d": w.d, "kind": "spatial", "stream": s2.cuda_stream}])
+    assert "not built" in str(ei.value)
+    assert idx.search_many([]) == []
