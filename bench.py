@@ -179,23 +179,33 @@ def make_workload(args, rank):
 # ---------------------------------------------------------------------------
 # reference arm: the CPU oracle (all-pairs, fp64)
 # ---------------------------------------------------------------------------
+def host_cores():
+    """The box's host cores available to this process (torchrun sets
+    OMP_NUM_THREADS=1 per rank; the oracle is given the cores explicitly)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def oracle_rate(w, seconds, seed=0, max_q=None):
     """Time the oracle as it stands on a bounded query sample of the workload."""
     import oracle
     rng = np.random.default_rng(seed)
     nq = w.Q.shape[0]
+    cores = host_cores()
     cal = np.sort(rng.choice(nq, min(8, nq), replace=False))
     t = time.perf_counter()
-    oracle.search(w.D, w.Q, w.d, qsel=cal)
+    oracle.search(w.D, w.Q, w.d, qsel=cal, nthreads=cores)
     dt = max(time.perf_counter() - t, 1e-6)
     n = int(min(nq, max(8, seconds * len(cal) / dt)))
     if max_q:
         n = min(n, max_q)
     sel = np.sort(rng.choice(nq, n, replace=False))
     t = time.perf_counter()
-    r = oracle.search(w.D, w.Q, w.d, qsel=sel)
+    r = oracle.search(w.D, w.Q, w.d, qsel=sel, nthreads=cores)
     dt = time.perf_counter() - t
-    return n, dt, int(r["hit"].sum()), oracle.max_threads()
+    return n, dt, int(r["hit"].sum()), cores
 
 
 def run_reference(args, ws, rank):
@@ -212,7 +222,7 @@ def run_reference(args, ws, rank):
     for k in range(args.warmup + args.steps):
         sel = np.sort(rng.choice(w.Q.shape[0], n, replace=False))
         t = time.perf_counter()
-        oracle.search(w.D, w.Q, w.d, qsel=sel)
+        oracle.search(w.D, w.Q, w.d, qsel=sel, nthreads=cores)
         el = time.perf_counter() - t
         if k >= args.warmup:
             times.append(el)
