@@ -509,6 +509,16 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
             radix_sort_pairs(k2, v2, len, mbits, mbits + bits_for((uint64_t)v), sc);
             k_subbin_offsets<<<nblk((uint64_t)v * m + 1), NT, 0, sc>>>(k2.p, len, v, m, mbits, off.p);
             TDS_CHECK_LAUNCH();
+            // optional materialised records in X/Y/Z order (ablation): the
+            // range kernel then streams them instead of gathering rec[X[i]]
+            if (!st_indirect()) {
+                DBuf<float4> srec(2 * len, sc, 2 * len * sizeof(float4) > (256ull << 20));
+                if (len) {
+                    k_gather_records<<<nblk(2 * len), NT, 0, sc>>>(rec.p, v2.p, len, srec.p);
+                    TDS_CHECK_LAUNCH();
+                }
+                idx->st_rec[c] = srec.release();
+            }
             st_pos[c].s = sc;                      // free after its last use, on that stream
             idx->st_arr[c] = v2.release();
             idx->st_len[c] = len;
@@ -557,11 +567,20 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     TDS_CUDA(cudaStreamSynchronize(s));
 }
 
+// GPUSpatioTemporal reads candidates through X/Y/Z as in the paper; the
+// materialised X/Y/Z-ordered record copies are an ablation,
+// TDS_ST_MATERIALISE=1: on B200 they measured no faster (the range kernel is
+// issue-bound and L1/L2 absorb the gather) and cost build time
+bool st_indirect() {
+    const char *e = getenv("TDS_ST_MATERIALISE");
+    return !(e && e[0] == '1');
+}
+
 void free_index(tds_index_s *idx) {
     cudaStream_t s = 0;
     auto f = [&](void *p) { if (p) dfree(p, s); };
     f(idx->rec); f(idx->perm); f(idx->bin_off); f(idx->bin_lo); f(idx->bin_hi); f(idx->bin_pmhi);
-    for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); }
+    for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); f(idx->st_rec[c]); }
     f(idx->cell_off); f(idx->fsg_A); f(idx->fsg_ecell); f(idx->fsg_rec); f(idx->fsg_perm);
     cudaStreamSynchronize(s);
 }

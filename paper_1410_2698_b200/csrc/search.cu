@@ -830,6 +830,7 @@ __global__ void k_tile_chunks(uint32_t *len_to_chunks, uint32_t ntiles, const un
 struct RangeArgs {
     PairCtx pc;                      // Q, rec, perm, d, window, output
     const uint32_t *arr[3];          // X, Y, Z
+    const float4 *srec[3];           // records in X/Y/Z order (null: gather rec[X[i]])
     const Sched *sched;
     const Tile *tiles;
     const uint32_t *item_start;      // [ntiles+1]
@@ -961,14 +962,18 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         uint32_t owner_hits = 0;             // hits of this lane's query found on the dense path
         // windows of WIN = 128 candidates: lane handles cand + 32k, k = 0..3, as two
         // packed pairs (two independent FFMA2 chains per query load)
+        // records: sorted entries (temporal), the materialised X/Y/Z-ordered copy
+        // (TDS_ST_MATERIALISE=1: streamed, independent of the id load), or rec[X[i]]
+        const float4 *srec = (T.sel >= 0) ? A.srec[T.sel] : nullptr;
         auto load_cand = [&](uint32_t c, bool v, uint32_t &j, float4 &a, float4 &b) {
             j = 0;
             a = make_float4(0.f, 0.f, 0.f, 0.f);
             b = make_float4(0.f, 0.f, 0.f, 1.f);
             if (v) {
                 j = arr ? __ldg(arr + c) : c;
-                a = __ldg(A.pc.rec + 2 * (uint64_t)j);
-                b = __ldg(A.pc.rec + 2 * (uint64_t)j + 1);
+                const float4 *src = srec ? srec + 2 * (uint64_t)c : A.pc.rec + 2 * (uint64_t)j;
+                a = __ldg(src);
+                b = __ldg(src + 1);
             }
         };
         auto ecand_of = [&](uint32_t j) {
@@ -1720,7 +1725,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.df = filter_threshold(d);
         a.tc = time_origin(idx);
         a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
-        for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
+        for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
         k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
@@ -1915,7 +1920,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.tc = time_origin(idx);
             a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
             a.pc.o.st = bst.p;
-            for (int c = 0; c < 3; ++c) a.arr[c] = idx->st_arr[c];
+            for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
             a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
             k_pair_range<true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
             TDS_CHECK_LAUNCH();

@@ -106,6 +106,7 @@ struct tds_index_s {
     uint32_t *st_arr[3] = {nullptr, nullptr, nullptr};   // X, Y, Z (sorted positions)
     uint64_t st_len[3] = {0, 0, 0};
     uint32_t *st_off[3] = {nullptr, nullptr, nullptr};   // [v*m+1], subbin (slab j, bin i) at j*m+i
+    float4 *st_rec[3] = {nullptr, nullptr, nullptr};     // [2*len] records in X/Y/Z order (ablation; null by default)
     // FSG as a dense CSR over all cells + lookup array A
     uint32_t *cell_off = nullptr;   // [gx*gy*gz+1]
     uint32_t *fsg_A = nullptr;      // [A_len] sorted positions
@@ -155,6 +156,7 @@ __host__ __device__ __forceinline__ uint32_t pack_cell(int x, int y, int z) {
 // ---------------------------------------------------------------------------
 // Stable LSD radix sort of (key, value) pairs on bits [begin_bit, end_bit).
 // keys/vals are sorted in place (double-buffered with caller-free temporaries).
+bool st_indirect();                 // no materialised X/Y/Z records unless TDS_ST_MATERIALISE=1 (ablation)
 void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint64_t n, int begin_bit, int end_bit,
                       cudaStream_t s);
 void radix_sort_pairs(DBuf<uint32_t> &keys, DBuf<uint32_t> &vals, uint64_t n, int begin_bit, int end_bit,
