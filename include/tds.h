@@ -53,7 +53,11 @@ enum {
     TDS_TEMPORAL = 1,          /* temporal bins */
     TDS_SPATIAL = 2,           /* flatly structured grid */
     TDS_SPATIOTEMPORAL = 4,    /* temporal bins split into spatial subbins */
-    TDS_ALL = 7
+    TDS_ALL = 7,
+    TDS_AUTO = 8               /* tds_search only: per batch, GPUSpatioTemporal or GPUTemporal,
+                                  whichever has the lower estimated cost = scheduled pair tests x
+                                  measured cost per pair test (the index choice of P:776-777,
+                                  P:1693-1696); needs both built, else GPUTemporal */
 };
 
 typedef enum {
@@ -92,6 +96,9 @@ typedef struct {
     float ms_pairs;             /* device time of the pair kernel passes */
     float ms_compact;           /* device time of overflow compaction / re-planning */
     float ms_total;             /* tds_search device time */
+    int32_t kind;               /* the variant that ran (TDS_TEMPORAL / TDS_SPATIAL / TDS_SPATIOTEMPORAL) */
+    int32_t reserved;
+    uint64_t pair_tests_alt;    /* TDS_AUTO: scheduled pair tests of the variant not chosen (else 0) */
 } tds_stats;
 
 /*
@@ -116,7 +123,8 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
  * tds_search — the distance threshold search of Q against the index
  * (Alg. 1 / 2 / 3).
  *
- *   kind      : TDS_TEMPORAL, TDS_SPATIAL or TDS_SPATIOTEMPORAL (must have been built)
+ *   kind      : TDS_TEMPORAL, TDS_SPATIAL or TDS_SPATIOTEMPORAL (must have been built), or
+ *               TDS_AUTO (see above; the chosen variant is reported in tds_stats.kind)
  *   queries   : nq segments (device or host memory); nq == 0 gives an empty result
  *   d         : distance threshold, finite and > 0 ("within d" is <= d, reading C4); a double:
  *               the hit decision and interval are exact for this d (fp32 filters use d

@@ -23,8 +23,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TDS_LIB", os.path.join(_HERE, "libtds.so"))
 
-TEMPORAL, SPATIAL, SPATIOTEMPORAL, ALL = 1, 2, 4, 7
-KINDS = {"temporal": TEMPORAL, "spatial": SPATIAL, "spatiotemporal": SPATIOTEMPORAL}
+TEMPORAL, SPATIAL, SPATIOTEMPORAL, ALL, AUTO = 1, 2, 4, 7, 8
+KINDS = {"temporal": TEMPORAL, "spatial": SPATIAL, "spatiotemporal": SPATIOTEMPORAL, "auto": AUTO}
 STATUS = {0: "TDS_OK", 1: "TDS_EINVAL", 2: "TDS_EDATA", 3: "TDS_ENOMEM", 4: "TDS_ECAPACITY", 5: "TDS_ECUDA"}
 
 EXPORT = {"perm": 0, "bin_off": 1, "bin_hi": 2, "st_x": 3, "st_y": 4, "st_z": 5, "st_off_x": 6,
@@ -59,7 +59,8 @@ class _Params(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in ("n_results", "n_queries", "pair_tests", "pairs_executed",
                                                "refined_pairs", "passes", "spilled", "fallback_queries")] + \
-               [(k, ctypes.c_float) for k in ("ms_schedule", "ms_pairs", "ms_compact", "ms_total")]
+               [(k, ctypes.c_float) for k in ("ms_schedule", "ms_pairs", "ms_compact", "ms_total")] + \
+               [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("pair_tests_alt", ctypes.c_uint64)]
 
 
 _lib = None

@@ -323,9 +323,10 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
     tds::set_error(0, "");
     if (!idx || !out) fail(TDS_EINVAL, "NULL argument");
     *out = nullptr;
-    if (kind != TDS_TEMPORAL && kind != TDS_SPATIAL && kind != TDS_SPATIOTEMPORAL)
-        fail(TDS_EINVAL, "kind = %d is not one of TDS_TEMPORAL/SPATIAL/SPATIOTEMPORAL", kind);
-    if (!(idx->kinds & (uint32_t)kind)) fail(TDS_EINVAL, "index was not built for kind %d", kind);
+    if (kind != TDS_TEMPORAL && kind != TDS_SPATIAL && kind != TDS_SPATIOTEMPORAL && kind != TDS_AUTO)
+        fail(TDS_EINVAL, "kind = %d is not one of TDS_TEMPORAL/SPATIAL/SPATIOTEMPORAL/AUTO", kind);
+    if (kind != TDS_AUTO && !(idx->kinds & (uint32_t)kind))
+        fail(TDS_EINVAL, "index was not built for kind %d", kind);
     if (!(d > 0.0) || !isfinite(d) || d > 3.0e38) fail(TDS_EINVAL, "d = %g must be finite and > 0", d);
     if (isnan(t_start) || isnan(t_end) || t_start > t_end) fail(TDS_EINVAL, "bad window [%g, %g]",
                                                                (double)t_start, (double)t_end);

@@ -36,6 +36,7 @@ constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range 
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 constexpr int DIRECT_MIN = 16;           // filter passes per 64-candidate window for the in-place path
+constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
@@ -53,6 +54,7 @@ struct DevStats {
     unsigned long long total_slots;  // spatial: flattened slots
     unsigned long long bad;          // ~(first invalid query row), 0 = none (atomicMax)
     unsigned long long union_total;  // sum of tile union lengths (chunk sizing)
+    unsigned long long pair_tests_t; // TDS_AUTO: the GPUTemporal plan's pair tests
     unsigned int work_ctr;           // dynamic work distribution
     unsigned int total_items;
     unsigned int ch;                 // candidates per work item
@@ -667,6 +669,7 @@ struct SchedArgs {
     uint32_t *keys;                  // sort keys: category << 13 | lo >> lo_shift (16 bits)
     uint32_t *vals;                  // identity (sort payload)
     int lo_shift;
+    int count_t;                     // TDS_AUTO: also sum the temporal ranges (pair_tests_t)
     DevStats *st;
 };
 
@@ -691,7 +694,7 @@ __device__ __forceinline__ int lower_bound_f(const float *a, int m, float x) {
 
 __global__ void k_schedule(SchedArgs A) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long work = 0, fb = 0;
+    unsigned long long work = 0, fb = 0, work_t = 0;
     if (p < A.nq) {
         uint32_t k = A.order ? A.order[p] : p;
         float4 a = A.Q[2 * (uint64_t)k], b = A.Q[2 * (uint64_t)k + 1];
@@ -708,6 +711,7 @@ __global__ void k_schedule(SchedArgs A) {
                 S.lo = A.bin_off[jlo];
                 S.hi = A.bin_off[jhe];
                 S.sel = S.lo < S.hi ? -1 : 3;
+                work_t = S.hi - S.lo;
                 if (A.use_st && S.sel == -1) {
                     // per dimension, the subbins (slabs) the d-inflated MBB
                     // overlaps; a dimension is usable only with a single slab
@@ -745,10 +749,12 @@ __global__ void k_schedule(SchedArgs A) {
     for (int o = 16; o > 0; o >>= 1) {
         work += __shfl_xor_sync(FULL, work, o);
         fb += __shfl_xor_sync(FULL, fb, o);
+        work_t += __shfl_xor_sync(FULL, work_t, o);
     }
     if ((threadIdx.x & 31) == 0) {
         if (work) atomicAdd(&A.st->pair_tests, work);
         if (fb) atomicAdd(&A.st->fallback, fb);
+        if (A.count_t && work_t) atomicAdd(&A.st->pair_tests_t, work_t);
     }
 }
 
@@ -1592,6 +1598,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // GPUSpatioTemporal order them by (selector, range start) below, which subsumes
     // the t_start sort of P:681-682 (range starts are monotone in t_start); FSG
     // keeps input order
+    // TDS_AUTO: schedule GPUSpatioTemporal (counting the GPUTemporal ranges too),
+    // then keep whichever plan has the lower estimated cost (below)
+    const int req_kind = kind;
+    if (kind == TDS_AUTO) kind = (idx->kinds & TDS_SPATIOTEMPORAL) ? TDS_SPATIOTEMPORAL : TDS_TEMPORAL;
     const bool spatial = (kind == TDS_SPATIAL);
     DBuf<uint32_t> keys, order;
     if (!spatial) { keys = DBuf<uint32_t>(n, s); order = DBuf<uint32_t>(n, s); }
@@ -1630,8 +1640,29 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         // top 13 bits of the range start suffice, so the key has 16 bits = 2 passes
         a.lo_shift = std::max(0, lo_bits - 13);
         a.st = dst.p;
+        a.count_t = (req_kind == TDS_AUTO && a.use_st) ? 1 : 0;
         k_schedule<<<nblk(n), 256, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
+        if (a.count_t) {
+            // index choice per batch: estimated cost = scheduled
+            // pair tests x cost per pair test; GPUSpatioTemporal's indirect candidates
+            // measured ST_PAIR_COST x GPUTemporal's per pair test
+            DevStats &h0 = *pinned_stats();
+            TDS_CUDA(cudaMemcpyAsync(&h0, dst.p, sizeof h0, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            const unsigned long long p_st = h0.pair_tests, p_t = h0.pair_tests_t;
+            if ((double)p_t < ST_PAIR_COST * (double)p_st) {
+                TDS_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(DevStats), s));
+                a.use_st = 0;
+                a.count_t = 0;
+                kind = TDS_TEMPORAL;
+                k_schedule<<<nblk(n), 256, 0, s>>>(a);
+                TDS_CHECK_LAUNCH();
+                S.pair_tests_alt = p_st;
+            } else {
+                S.pair_tests_alt = p_t;
+            }
+        }
         // sort S by (array selector, range start): one stable radix sort
         radix_sort_pairs(keys.p, order.p, n, 0, 16, s);
         {
@@ -1683,6 +1714,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     tm.mark(1);
     S.pair_tests = hs.pair_tests;
     S.fallback_queries = hs.fallback;
+    S.kind = kind;
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
 
     uint64_t cap = capacity;

@@ -3,6 +3,7 @@ GPU, and exports every entry point include/tds.h declares.  No compute calls."""
 import ctypes
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -66,3 +67,22 @@ def test_no_oracle_import_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "tds_oracle" not in txt, f
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of tds_stats / tds_search_req /
+    tds_index_params have the header's sizes and field offsets (gcc)."""
+    import ctypes
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "tds.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(tds_stats), offsetof(tds_stats, ms_schedule),'
+        ' offsetof(tds_stats, kind), offsetof(tds_stats, pair_tests_alt), sizeof(tds_search_req),'
+        ' offsetof(tds_search_req, stream), sizeof(tds_index_params)); return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    S, R, P = tds._Stats, tds._SearchReq, tds._Params
+    want = [ctypes.sizeof(S), S.ms_schedule.offset, S.kind.offset, S.pair_tests_alt.offset, ctypes.sizeof(R),
+            R.stream.offset, ctypes.sizeof(P)]
+    assert got == want

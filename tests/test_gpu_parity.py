@@ -403,3 +403,39 @@ def test_search_many_error_frees_all(tds):
                          {"queries": _cuda(w.Q), "d": w.d, "kind": "spatial", "stream": s2.cuda_stream}])
     assert "not built" in str(ei.value)
     assert idx.search_many([]) == []
+
+
+def test_st_materialised_ablation_same_result(tds, monkeypatch):
+    """TDS_ST_MATERIALISE=1 (records copied in X/Y/Z order) gives
+    exactly the default (indirect) GPUSpatioTemporal records."""
+    w = synth.random_1m(n_traj=300)
+    base = tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=1000, v=4)
+    a = base.search(_cuda(w.Q), 30.0, kind="spatiotemporal").fetch(sorted=True, device=False)
+    monkeypatch.setenv("TDS_ST_MATERIALISE", "1")
+    mat = tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=1000, v=4)
+    b = mat.search(_cuda(w.Q), 30.0, kind="spatiotemporal").fetch(sorted=True, device=False)
+    assert len(a[0]) > 0
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("v, expect", [(4, "spatiotemporal"), (1, "temporal")])
+def test_auto_kind_choice(tds, v, expect):
+    """TDS_AUTO: with v = 4 and a small d
+    the subbins cut the pair tests far below GPUTemporal's, so GPUSpatioTemporal
+    runs; with v = 1 every subbin range equals the temporal range, so the
+    cheaper-per-pair GPUTemporal runs.  The records equal that variant's."""
+    w = synth.random_1m(n_traj=300)
+    idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=1000, v=v)
+    r = idx.search(_cuda(w.Q), 5.0, kind="auto")
+    st = r.stats()
+    assert st["kind"] == tds.KINDS[expect]
+    assert st["pair_tests_alt"] > 0
+    if expect == "spatiotemporal":
+        assert st["pair_tests"] * 1.5 <= st["pair_tests_alt"]
+    else:
+        assert st["pair_tests_alt"] * 1.5 >= st["pair_tests"]
+    a = r.fetch(sorted=True, device=False)
+    b = idx.search(_cuda(w.Q), 5.0, kind=expect).fetch(sorted=True, device=False)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
