@@ -188,33 +188,6 @@ __global__ void __launch_bounds__(1024) k_prefix_max(const float *__restrict__ i
 }
 
 // A5 / A4: number of slabs (cells) of each entry in dimension c / in 3-D
-__global__ void k_slab_count(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v,
-                             uint32_t *__restrict__ cnt) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float4 a = rec[2 * i], b = rec[2 * i + 1];
-    float p0 = c == 0 ? a.x : (c == 1 ? a.y : a.z);
-    float p1 = c == 0 ? b.x : (c == 1 ? b.y : b.z);
-    int s0 = cell_of(fminf(p0, p1), o, w, v), s1 = cell_of(fmaxf(p0, p1), o, w, v);
-    cnt[i] = (uint32_t)(s1 - s0 + 1);
-}
-
-__global__ void k_slab_emit(const float4 *__restrict__ rec, uint64_t n, int c, float o, float w, int v, int mbits,
-                            const uint32_t *__restrict__ bin, const uint32_t *__restrict__ pos,
-                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float4 a = rec[2 * i], b = rec[2 * i + 1];
-    float p0 = c == 0 ? a.x : (c == 1 ? a.y : a.z);
-    float p1 = c == 0 ? b.x : (c == 1 ? b.y : b.z);
-    int s0 = cell_of(fminf(p0, p1), o, w, v), s1 = cell_of(fmaxf(p0, p1), o, w, v);
-    uint32_t k = pos[i];
-    for (int s = s0; s <= s1; ++s, ++k) {
-        keys[k] = ((uint32_t)s << mbits) | bin[i];      // subbin (slab j, bin i)
-        vals[k] = (uint32_t)i;
-    }
-}
-
 struct Grid3 {
     float o[3], w[3];
     int g[3];
@@ -227,21 +200,6 @@ __device__ __forceinline__ void cell_box(const float4 &a, const float4 &b, const
         lo[c] = cell_of(fminf(p0[c], p1[c]), G.o[c], G.w[c], G.g[c]);
         hi[c] = cell_of(fmaxf(p0[c], p1[c]), G.o[c], G.w[c], G.g[c]);
     }
-}
-
-__global__ void k_cell_count(const float4 *__restrict__ rec, uint64_t n, Grid3 G, uint32_t *__restrict__ cnt,
-                             unsigned long long *__restrict__ total) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long c = 0;
-    if (i < n) {
-        int lo[3], hi[3];
-        cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
-        c = (unsigned long long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
-        cnt[i] = (uint32_t)c;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
 // cell-ordered copies for the GPUSpatial pair kernel: record, original row and
@@ -261,57 +219,86 @@ __global__ void k_fsg_materialise(const float4 *__restrict__ rec, const uint32_t
     ecell[i] = make_uint2(pack_cell(lo[0], lo[1], lo[2]), pack_cell(hi[0], hi[1], hi[2]));
 }
 
-__global__ void k_cell_emit(const float4 *__restrict__ rec, uint64_t n, Grid3 G, const uint32_t *__restrict__ pos,
-                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+// A5 + A4 phase 1 in one pass over the records: per entry, the number of slabs
+// it overlaps in x / y / z and the number of FSG cells
+struct StGeom {
+    float o[3], w[3];
+    int v;
+};
+
+__global__ void k_count_all(const float4 *__restrict__ rec, uint64_t n, int want_st, StGeom S, int want_fsg,
+                            Grid3 G, uint32_t *__restrict__ cx, uint32_t *__restrict__ cy,
+                            uint32_t *__restrict__ cz, uint32_t *__restrict__ cf,
+                            unsigned long long *__restrict__ fsg_total) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c = 0;
+    if (i < n) {
+        const float4 a = rec[2 * i], b = rec[2 * i + 1];
+        if (want_st) {
+            const float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+            uint32_t *outs[3] = {cx, cy, cz};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int s0 = cell_of(fminf(p0[d], p1[d]), S.o[d], S.w[d], S.v);
+                const int s1 = cell_of(fmaxf(p0[d], p1[d]), S.o[d], S.w[d], S.v);
+                outs[d][i] = (uint32_t)(s1 - s0 + 1);
+            }
+        }
+        if (want_fsg) {
+            int lo[3], hi[3];
+            cell_box(a, b, G, lo, hi);
+            c = (unsigned long long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+            cf[i] = (uint32_t)c;
+        }
+    }
+    if (want_fsg) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(fsg_total, c);
+    }
+}
+
+// A5 + A4 phase 2 emission in one pass: (subbin key, entry) pairs of the three
+// subbin arrays and (cell key, entry) pairs of the FSG
+struct EmitOut {
+    const uint32_t *pos[4];          // x, y, z, fsg
+    uint32_t *keys[4], *vals[4];
+};
+
+__global__ void k_emit_all(const float4 *__restrict__ rec, uint64_t n, int want_st, StGeom S, int mbits,
+                           const uint32_t *__restrict__ bin, int want_fsg, Grid3 G, EmitOut E) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int lo[3], hi[3];
-    cell_box(rec[2 * i], rec[2 * i + 1], G, lo, hi);
-    uint32_t k = pos[i];
-    for (int x = lo[0]; x <= hi[0]; ++x)
-        for (int y = lo[1]; y <= hi[1]; ++y)
-            for (int z = lo[2]; z <= hi[2]; ++z, ++k) {
-                keys[k] = (uint32_t)(((uint64_t)x * G.g[1] + y) * G.g[2] + z);   // row-major h
-                vals[k] = (uint32_t)i;
+    const float4 a = rec[2 * i], b = rec[2 * i + 1];
+    if (want_st) {
+        const float p0[3] = {a.x, a.y, a.z}, p1[3] = {b.x, b.y, b.z};
+        const uint32_t bi = bin[i];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int s0 = cell_of(fminf(p0[d], p1[d]), S.o[d], S.w[d], S.v);
+            const int s1 = cell_of(fmaxf(p0[d], p1[d]), S.o[d], S.w[d], S.v);
+            uint32_t k = E.pos[d][i];
+            for (int sl = s0; sl <= s1; ++sl, ++k) {
+                E.keys[d][k] = ((uint32_t)sl << mbits) | bi;     // subbin (slab j, bin i)
+                E.vals[d][k] = (uint32_t)i;
             }
+        }
+    }
+    if (want_fsg) {
+        int lo[3], hi[3];
+        cell_box(a, b, G, lo, hi);
+        uint32_t k = E.pos[3][i];
+        for (int x = lo[0]; x <= hi[0]; ++x)
+            for (int y = lo[1]; y <= hi[1]; ++y)
+                for (int z = lo[2]; z <= hi[2]; ++z, ++k) {
+                    E.keys[3][k] = (uint32_t)(((uint64_t)x * G.g[1] + y) * G.g[2] + z);   // row-major h
+                    E.vals[3][k] = (uint32_t)i;
+                }
+    }
 }
 
 inline unsigned nblk(uint64_t n, int nt = NT) { return (unsigned)((n + nt - 1) / nt); }
 
-// per-thread side streams and events used to overlap independent build phases
-void side_streams(cudaStream_t out[4]) {
-    static thread_local cudaStream_t ss[4] = {nullptr, nullptr, nullptr, nullptr};
-    static thread_local int dev_of = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev_of != dev) {
-        for (auto &x : ss) TDS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-        dev_of = dev;
-    }
-    for (int i = 0; i < 4; ++i) out[i] = ss[i];
-}
-
-cudaEvent_t fork_event() {
-    static thread_local cudaEvent_t e = nullptr;
-    if (!e) TDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return e;
-}
-
-cudaEvent_t join_event(cudaStream_t s) {
-    static thread_local cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
-    static thread_local cudaStream_t owner[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int i = 0; i < 4; ++i) {
-        if (owner[i] == s && e[i]) return e[i];
-        if (!owner[i]) {
-            TDS_CUDA(cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming));
-            owner[i] = s;
-            return e[i];
-        }
-    }
-    cudaEvent_t x;
-    TDS_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
-    return x;
-}
 
 int bits_for(uint64_t nk) {
     int b = 0;
@@ -451,27 +438,44 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
             fail(TDS_EINVAL, "grid %d x %d x %d exceeds %d x %d x %d", idx->grid[0], idx->grid[1], idx->grid[2],
                  FSG_MAX_X, FSG_MAX_Y, FSG_MAX_Z);
     }
+    // one pass over the records counts the slab memberships of x / y / z and the
+    // FSG cells of every entry; one batched scan turns them into emit positions
     DBuf<uint32_t> st_pos[3];
     DBuf<uint32_t> fsg_pos;
     DBuf<unsigned long long> totals(4, s);       // ST x, y, z lengths; FSG length
     TDS_CUDA(cudaMemsetAsync(totals.p, 0, 32, s));
-    if (want_st) {
-        for (int c = 0; c < 3; ++c) {
-            float ext = E.hi[c] - E.lo[c];
-            E.w_st[c] = ext > 0.f ? ext / (float)v : 1.0f;
-            DBuf<uint32_t> cnt(n, s);
-            st_pos[c] = DBuf<uint32_t>(n, s);
-            k_slab_count<<<nblk(n), NT, 0, s>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, cnt.p);
-            TDS_CHECK_LAUNCH();
-            exclusive_scan_u32(cnt.p, st_pos[c].p, n, (uint32_t *)(totals.p + c), s);
-        }
+    StGeom SG{};
+    SG.v = v;
+    for (int c = 0; c < 3; ++c) {
+        float ext = E.hi[c] - E.lo[c];
+        E.w_st[c] = ext > 0.f ? ext / (float)v : 1.0f;
+        SG.o[c] = E.lo[c];
+        SG.w[c] = E.w_st[c];
     }
-    if (want_fsg) {
-        DBuf<uint32_t> cnt(n, s);
-        fsg_pos = DBuf<uint32_t>(n, s);
-        k_cell_count<<<nblk(n), NT, 0, s>>>(rec.p, n, G, cnt.p, totals.p + 3);
+    if (want_st || want_fsg) {
+        DBuf<uint32_t> cnt(4 * n, s);
+        if (want_st)
+            for (int c = 0; c < 3; ++c) st_pos[c] = DBuf<uint32_t>(n, s);
+        if (want_fsg) fsg_pos = DBuf<uint32_t>(n, s);
+        k_count_all<<<nblk(n), NT, 0, s>>>(rec.p, n, want_st, SG, want_fsg, G, cnt.p, cnt.p + n, cnt.p + 2 * n,
+                                           cnt.p + 3 * n, totals.p + 3);
         TDS_CHECK_LAUNCH();
-        exclusive_scan_u32(cnt.p, fsg_pos.p, n, nullptr, s);
+        const uint32_t *in[4];
+        uint32_t *out[4], *tot32[4];
+        int k = 0;
+        if (want_st)
+            for (int c = 0; c < 3; ++c, ++k) {
+                in[k] = cnt.p + (uint64_t)c * n;
+                out[k] = st_pos[c].p;
+                tot32[k] = (uint32_t *)(totals.p + c);
+            }
+        if (want_fsg) {
+            in[k] = cnt.p + 3 * n;
+            out[k] = fsg_pos.p;
+            tot32[k] = nullptr;                     // the FSG total is summed in 64 bits above
+            ++k;
+        }
+        exclusive_scan_u32_batch(k, in, out, tot32, n, s);
     }
     unsigned long long tot[4] = {0, 0, 0, 0};
     if (want_st || want_fsg) {
@@ -480,47 +484,58 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     }
 
     tr.mark("counts+sync");
-    // ---- phase 2: the three subbin arrays and the FSG are independent (optionally
-    // built concurrently on forked streams, joined before returning)
-    cudaStream_t side[4];
-    side_streams(side);
-    // one stream by default: on B200 the fork/join and cross-stream pool reuse cost
-    // more than the overlap gains (Random-1M build 0.62 vs 0.78 ms; Random-dense
-    // within noise); TDS_BUILD_CONCURRENT=1 forks the four builds onto side streams
-    static const bool concurrent = getenv("TDS_BUILD_CONCURRENT") && getenv("TDS_BUILD_CONCURRENT")[0] == '1';
-    if (!concurrent)
-        for (auto &ss : side) ss = s;
-    cudaEvent_t fork = fork_event();
-    TDS_CUDA(cudaEventRecord(fork, s));
-    for (auto ss : side) TDS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+    // ---- phase 2: emission of all four structures in one pass over the records,
+    // then per structure the grouping sort and its offsets
+    const int mbits = bits_for((uint64_t)m);
+    DBuf<uint32_t> sk[3], sv[3], fk, fv;
+    EmitOut EO{};
+    if (want_st)
+        for (int c = 0; c < 3; ++c) {
+            const uint64_t len = tot[c] & 0xffffffffull;
+            sk[c] = DBuf<uint32_t>(len, s);
+            sv[c] = DBuf<uint32_t>(len, s);
+            EO.pos[c] = st_pos[c].p;
+            EO.keys[c] = sk[c].p;
+            EO.vals[c] = sv[c].p;
+        }
+    if (want_fsg) {
+        if (tot[3] >= (1ull << 32) - 1)
+            fail(TDS_EINVAL, "FSG lookup array would hold %llu ids (limit 2^32); use a coarser grid", tot[3]);
+        fk = DBuf<uint32_t>(tot[3], s);
+        fv = DBuf<uint32_t>(tot[3], s);
+        EO.pos[3] = fsg_pos.p;
+        EO.keys[3] = fk.p;
+        EO.vals[3] = fv.p;
+    }
+    if (want_st || want_fsg) {
+        k_emit_all<<<nblk(n), NT, 0, s>>>(rec.p, n, want_st, SG, mbits, bin.p, want_fsg, G, EO);
+        TDS_CHECK_LAUNCH();
+    }
+    for (int c = 0; c < 3; ++c) st_pos[c].reset();
+    fsg_pos.reset();
 
     // ---- A5, phase 2: spatiotemporal subbin arrays ------------------
     if (want_st) {
         for (int c = 0; c < 3; ++c) {
-            cudaStream_t sc = side[c];
             const uint64_t len = tot[c] & 0xffffffffull;
-            DBuf<uint32_t> k2(len, sc), v2(len, sc), off((uint64_t)v * m + 1, sc);
-            const int mbits = bits_for((uint64_t)m);
-            k_slab_emit<<<nblk(n), NT, 0, sc>>>(rec.p, n, c, E.lo[c], E.w_st[c], v, mbits, bin.p, st_pos[c].p,
-                                               k2.p, v2.p);
-            TDS_CHECK_LAUNCH();
+            DBuf<uint32_t> off((uint64_t)v * m + 1, s);
             // emitted in sorted-position order, so within a slab the bins are already
             // ascending: a stable sort on the slab bits alone groups the subbins
-            radix_sort_pairs(k2, v2, len, mbits, mbits + bits_for((uint64_t)v), sc);
-            k_subbin_offsets<<<nblk((uint64_t)v * m + 1), NT, 0, sc>>>(k2.p, len, v, m, mbits, off.p);
+            radix_sort_pairs(sk[c], sv[c], len, mbits, mbits + bits_for((uint64_t)v), s);
+            k_subbin_offsets<<<nblk((uint64_t)v * m + 1), NT, 0, s>>>(sk[c].p, len, v, m, mbits, off.p);
             TDS_CHECK_LAUNCH();
             // optional materialised records in X/Y/Z order (ablation): the
             // range kernel then streams them instead of gathering rec[X[i]]
             if (!st_indirect()) {
-                DBuf<float4> srec(2 * len, sc, 2 * len * sizeof(float4) > (256ull << 20));
+                DBuf<float4> srec(2 * len, s, 2 * len * sizeof(float4) > (256ull << 20));
                 if (len) {
-                    k_gather_records<<<nblk(2 * len), NT, 0, sc>>>(rec.p, v2.p, len, srec.p);
+                    k_gather_records<<<nblk(2 * len), NT, 0, s>>>(rec.p, sv[c].p, len, srec.p);
                     TDS_CHECK_LAUNCH();
                 }
                 idx->st_rec[c] = srec.release();
             }
-            st_pos[c].s = sc;                      // free after its last use, on that stream
-            idx->st_arr[c] = v2.release();
+            sk[c].reset();
+            idx->st_arr[c] = sv[c].release();
             idx->st_len[c] = len;
             idx->st_off[c] = off.release();
         }
@@ -528,32 +543,22 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
 
     // ---- A4, phase 2: FSG (dense CSR over all cells) -----------------
     if (want_fsg) {
-        cudaStream_t sf = side[3];
         const unsigned long long len = tot[3];
-        if (len >= (1ull << 32) - 1)
-            fail(TDS_EINVAL, "FSG lookup array would hold %llu ids (limit 2^32); use a coarser grid", len);
-        DBuf<uint32_t> k2(len, sf), v2(len, sf), off(ncell + 1, sf);
-        k_cell_emit<<<nblk(n), NT, 0, sf>>>(rec.p, n, G, fsg_pos.p, k2.p, v2.p);
+        DBuf<uint32_t> off(ncell + 1, s);
+        group_by_key(fk, fv, len, ncell, off.p, s);
+        fk.reset();
+        DBuf<uint2> ecell(len, s);
+        DBuf<float4> frec(2 * len, s);
+        DBuf<uint32_t> fperm(len, s);
+        k_fsg_materialise<<<nblk(len), NT, 0, s>>>(rec.p, perm.p, fv.p, len, G, frec.p, fperm.p, ecell.p);
         TDS_CHECK_LAUNCH();
-        group_by_key(k2, v2, len, ncell, off.p, sf);
-        DBuf<uint2> ecell(len, sf);
-        DBuf<float4> frec(2 * len, sf);
-        DBuf<uint32_t> fperm(len, sf);
-        k_fsg_materialise<<<nblk(len), NT, 0, sf>>>(rec.p, perm.p, v2.p, len, G, frec.p, fperm.p, ecell.p);
-        TDS_CHECK_LAUNCH();
-        fsg_pos.s = sf;
         idx->fsg_ecell = ecell.release();
         idx->fsg_rec = frec.release();
         idx->fsg_perm = fperm.release();
-        idx->fsg_A = v2.release();
+        idx->fsg_A = fv.release();
         idx->A_len = len;
         idx->cell_off = off.release();
         idx->n_cells = ncell;
-    }
-    for (auto ss : side) {                         // join
-        cudaEvent_t ev = join_event(ss);
-        TDS_CUDA(cudaEventRecord(ev, ss));
-        TDS_CUDA(cudaStreamWaitEvent(s, ev, 0));
     }
     bin.s = s;
     tr.mark("st+fsg");

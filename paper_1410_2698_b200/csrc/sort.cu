@@ -235,9 +235,9 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long *statu
 }
 
 template <class T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chained(const T *__restrict__ in, T *out, uint64_t n,
-                                                               unsigned long long *status, unsigned *tile_ctr,
-                                                               T *d_total, uint64_t ntiles) {
+__device__ __forceinline__ void scan_chained_tile(const T *__restrict__ in, T *out, uint64_t n,
+                                                  unsigned long long *status, unsigned *tile_ctr, T *d_total,
+                                                  uint64_t ntiles) {
     __shared__ T buf[SCAN_TILE];
     __shared__ T tot;
     __shared__ unsigned long long s_prefix;
@@ -292,6 +292,28 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chained(const T *__restri
         if (k < n) out[k] = buf[j];
     }
 }
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chained(const T *__restrict__ in, T *out, uint64_t n,
+                                                               unsigned long long *status, unsigned *tile_ctr,
+                                                               T *d_total, uint64_t ntiles) {
+    scan_chained_tile<T>(in, out, n, status, tile_ctr, d_total, ntiles);
+}
+
+// up to 4 independent scans of n elements in one launch (blockIdx.y = scan)
+struct ScanBatch {
+    const uint32_t *in[4];
+    uint32_t *out[4];
+    uint32_t *total[4];
+};
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chained_batch(ScanBatch B, uint64_t n,
+                                                                     unsigned long long *status, uint64_t ntiles) {
+    const int y = blockIdx.y;
+    unsigned long long *st = status + (uint64_t)y * (ntiles + 1);
+    scan_chained_tile<uint32_t>(B.in[y], B.out[y], n, st, (unsigned *)(st + ntiles), B.total[y], ntiles);
+}
+
 
 // ---------------------------------------------------------------------------
 // onesweep radix sort: one histogram pass for all digits, then one
@@ -459,6 +481,23 @@ void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t 
 
 void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *d_total, cudaStream_t s) {
     exclusive_scan_impl<uint64_t>(in, out, n, d_total, s);
+}
+
+void exclusive_scan_u32_batch(int k, const uint32_t *const *in, uint32_t *const *out, uint32_t *const *d_total,
+                              uint64_t n, cudaStream_t s) {
+    if (k < 1 || k > 4) fail(TDS_EINVAL, "exclusive_scan_u32_batch: k = %d", k);
+    if (n == 0) {
+        for (int y = 0; y < k; ++y)
+            if (d_total[y]) TDS_CUDA(cudaMemsetAsync(d_total[y], 0, 4, s));
+        return;
+    }
+    ScanBatch B{};
+    for (int y = 0; y < k; ++y) { B.in[y] = in[y]; B.out[y] = out[y]; B.total[y] = d_total[y]; }
+    const uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DBuf<unsigned long long> status((uint64_t)k * (nb + 1), s);   // per scan: tile states + tile counter
+    TDS_CUDA(cudaMemsetAsync(status.p, 0, 8 * (uint64_t)k * (nb + 1), s));
+    k_scan_chained_batch<<<dim3((unsigned)nb, (unsigned)k), SCAN_THREADS, 0, s>>>(B, n, status.p, nb);
+    TDS_CHECK_LAUNCH();
 }
 
 // the passes; returns true if the sorted data ended in (k2, v2) (odd pass count)

@@ -163,6 +163,9 @@ void radix_sort_pairs(DBuf<uint32_t> &keys, DBuf<uint32_t> &vals, uint64_t n, in
                       cudaStream_t s);
 // Exclusive scan of n uint32 values into out (out may alias in); optional
 // total written to *d_total (device pointer, may be null).  64-bit variant too.
+// k (<= 4) independent exclusive scans of n uint32 in one launch (totals optional)
+void exclusive_scan_u32_batch(int k, const uint32_t *const *in, uint32_t *const *out, uint32_t *const *d_total,
+                              uint64_t n, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *d_total,
                         cudaStream_t s);
 void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *d_total,
