@@ -340,8 +340,16 @@ def run_tds(args, ws, rank, local):
             collect.append((ev + [end], per, d2h, [o[0] for o in outs]))
         return per
 
-    # warm-up
-    for _ in range(args.warmup):
+    # warm-up.  The first warm-up step runs the variants one after another and
+    # measures their output: tds_search_many holds every variant's result at once,
+    # so it is used only when the outputs are small (< 10 % of device memory);
+    # output-bound runs (e.g. Random-dense d = 0.09, 40 GB per variant) stay serial.
+    want_batched = args.batched
+    args.batched = False
+    per0 = step()
+    out_bytes = 16 * sum(int(v["n_results"]) for v in per0.values())
+    args.batched = want_batched and out_bytes < 0.1 * torch.cuda.get_device_properties(dev).total_memory
+    for _ in range(args.warmup - 1):
         step()
     torch.cuda.synchronize(dev)
 

@@ -104,6 +104,14 @@ void *dalloc_big(size_t bytes, cudaStream_t s);
 
 static uint64_t device_budget_bytes_now();
 
+// uncached budget, and the lock under which searches size and allocate result
+// buffers above 1 GB (concurrent searches then see each other's allocations)
+uint64_t device_budget_bytes_fresh() { return device_budget_bytes_now(); }
+std::mutex &big_alloc_mutex() {
+    static std::mutex m;
+    return m;
+}
+
 // cached: cudaMemGetInfo costs up to milliseconds, so refresh at most every 0.5 s
 // (allocation failures fall back to smaller buffers)
 uint64_t device_budget_bytes() {

@@ -1706,11 +1706,19 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
 
     uint64_t cap = capacity;
+    std::unique_lock<std::mutex> big_lock;
     if (cap == 0) {
-        // budget: free device memory plus memory the pools hold unused, measured at
-        // index build (cudaMemGetInfo costs up to milliseconds: not per search)
-        uint64_t budget = (uint64_t)(device_budget_bytes() * 0.45) / sizeof(Rec);
-        cap = std::min<uint64_t>(hs.pair_tests + 64, budget);
+        // budget: free device memory plus memory the pools hold unused (cached:
+        // cudaMemGetInfo costs up to milliseconds).  A buffer above 1 GB is sized from
+        // a fresh budget under a process-wide lock held until it is allocated, so
+        // concurrent searches (tds_search_many) do not over-commit the device.
+        const uint64_t want = hs.pair_tests + 64;
+        uint64_t budget_bytes = device_budget_bytes();
+        if (want * sizeof(Rec) > (1ull << 30)) {
+            big_lock = std::unique_lock<std::mutex>(big_alloc_mutex());
+            budget_bytes = device_budget_bytes_fresh();
+        }
+        cap = std::min<uint64_t>(want, (uint64_t)(budget_bytes * 0.45) / sizeof(Rec));
         cap = std::max<uint64_t>(cap, 1024);
     }
     cap = std::min<uint64_t>(cap, (1ull << 40));
@@ -1729,6 +1737,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             cap /= 2;                     // auto capacity: retry smaller (overflow re-plan covers the rest)
             set_error(0, "");
         }
+    }
+    if (big_lock.owns_lock()) {
+        TDS_CUDA(cudaStreamSynchronize(s));     // the allocation is visible to the next budget query
+        big_lock.unlock();
     }
     DBuf<uint32_t> chunk_used(nchunks, s);
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));

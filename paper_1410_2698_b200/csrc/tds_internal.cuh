@@ -8,6 +8,7 @@
 #include <math.h>
 #include <string>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/tds.h"
@@ -195,6 +196,8 @@ struct Trace {
 };
 // free device memory + memory reserved but unused in the default mempool (bytes)
 uint64_t device_budget_bytes();
+uint64_t device_budget_bytes_fresh();
+std::mutex &big_alloc_mutex();
 
 // ---------------------------------------------------------------------------
 // result records (16 B): (query row, entry row, t_in, t_out)
