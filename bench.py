@@ -341,15 +341,20 @@ def run_tds(args, ws, rank, local):
         return per
 
     # warm-up.  The first warm-up step runs the variants one after another and
-    # measures their output: tds_search_many holds every variant's result at once,
-    # so it is used only when the outputs are small (< 10 % of device memory);
-    # output-bound runs (e.g. Random-dense d = 0.09, 40 GB per variant) stay serial.
+    # measures them: tds_search_many overlaps the searches' host synchronisations
+    # and launch chains, which pays only when the searches are short (each under
+    # 1 ms of device time, e.g. Random-1M); long pair kernels just compete for the
+    # SMs (Random-dense d = 0.01: 26 vs 21 ms per step), and it holds every
+    # variant's result at once (Random-dense d = 0.09: 40 GB each), so those stay serial.
     want_batched = args.batched
     args.batched = False
+    step()                                   # cold (first-touch, pool growth): not measured
     per0 = step()
     out_bytes = 16 * sum(int(v["n_results"]) for v in per0.values())
-    args.batched = want_batched and out_bytes < 0.1 * torch.cuda.get_device_properties(dev).total_memory
-    for _ in range(args.warmup - 1):
+    short = all(float(v["ms_total"]) < 1.0 for v in per0.values())
+    args.batched = (want_batched and short
+                    and out_bytes < 0.1 * torch.cuda.get_device_properties(dev).total_memory)
+    for _ in range(args.warmup - 2):
         step()
     torch.cuda.synchronize(dev)
 
@@ -477,7 +482,8 @@ def run_tds(args, ws, rank, local):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,
             "breakdown": {"build_index_ms": build_ms, "variants": per_kind,
-                          "step_ms_median": statistics.median(step_ms)},
+                          "step_ms_median": statistics.median(step_ms),
+                          "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
             "search_only": {"value": ws * nvar * nq / (search_ms / 1e3), "unit": "query segments/s",
                             "ranks": "rank 0's time, scaled by the rank count",
                             "note": "per-step median of the three variants' tds_search + tds_fetch_results "
