@@ -484,12 +484,15 @@ struct WarpState {
     unsigned long long ap_base;
     uint32_t ap_used, ap_size, ap_full;
     uint32_t refined, hits;
-    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: query row, sorted entry position
+    uint32_t fn;                     // fp64 queue fill (< 32 between flushes)
+    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: query row (| F64_FLAG), sorted entry position
+    uint32_t fq[64], fj[64];         // fp64 queue: pairs the fp32 stages could not decide
 };
+constexpr uint32_t F64_FLAG = 0x80000000u;   // refine-queue entry already known to need fp64
 
 __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
     if (lane == 0) {
-        W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0;
+        W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0; W.fn = 0;
     }
     __syncwarp();
 }
@@ -571,41 +574,82 @@ struct PairCtx {                     // what the fp64 path needs
 // Out of line: called once per 32 queued pairs from several sites of the pair
 // kernels; inlining it (and pair64) at each site bloated the kernels past the
 // instruction cache (ncu: no_instruction stalls on output-bound searches).
+// Evaluate the first n (<= 32) pairs of the fp64 queue (lane k takes pair k, all
+// lanes busy) and append the hits; the rest moves to the front.
 template <bool EXACT>
-__device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n) {
+__device__ __forceinline__ void flush64(const PairCtx *C, WarpState *W, uint32_t n) {
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
-    const uint32_t q = v ? W->rq[lane] : 0u, j = v ? W->rj[lane] : 0u;
-    __syncwarp();                    // queue slots read: later queue_add may reuse them
+    const uint32_t q = v ? W->fq[lane] : 0u, j = v ? W->fj[lane] : 0u;
+    const uint32_t fn = W->fn;
+    const uint32_t t1 = (uint32_t)lane + n < fn ? W->fq[n + lane] : 0u;
+    const uint32_t t2 = (uint32_t)lane + n < fn ? W->fj[n + lane] : 0u;
+    __syncwarp();
+    if ((uint32_t)lane + n < fn) { W->fq[lane] = t1; W->fj[lane] = t2; }
     float tin = 0.f, tout = 0.f;
-    bool hit = false, need64 = false;
-    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = make_float4(0.f, 0.f, 0.f, 1.f), ea = qa, eb = qb;
+    bool hit = false;
     if (v) {
-        qa = __ldg(C->Q + 2 * (uint64_t)q);
-        qb = __ldg(C->Q + 2 * (uint64_t)q + 1);
-        ea = __ldg(C->rec + 2 * (uint64_t)j);
-        eb = __ldg(C->rec + 2 * (uint64_t)j + 1);
-        // certain hit with an accurate fp32 interval, else fp64
-        const QConst qc = make_qconst(qa, qb, C->T0, C->T1);
-        const int k = hit_kind(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext),
-                               qc.t0c, qc.t1c, make_ecand(ea, eb), C->d, tin, tout);
-        hit = (k == 2);
-        need64 = (k == 1);           // k == 0: no shared span (a, b exact in fp32)
+        hit = pair64(__ldg(C->Q + 2 * (uint64_t)q), __ldg(C->Q + 2 * (uint64_t)q + 1), __ldg(C->rec + 2 * (uint64_t)j),
+                     __ldg(C->rec + 2 * (uint64_t)j + 1), C->d64, (double)C->T0, (double)C->T1, tin, tout);
     }
-    if (__any_sync(FULL, need64) && need64)
-        hit = pair64(qa, qb, ea, eb, C->d64, (double)C->T0, (double)C->T1, tin, tout);
     const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
     Rec r{q, eid, tin, tout};
     append<EXACT>(C->o, *W, hit, r, lane);
     const unsigned hm = __ballot_sync(FULL, hit);
-    const unsigned m64 = __ballot_sync(FULL, need64);
     if (hit) {   // per-query counts, aggregated over the lanes of the same query
         const unsigned peers = __match_any_sync(hm, q);
         if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&C->o.qcount[q], (uint32_t)__popc(peers));
     }
     __syncwarp();
-    if (lane == 0) { W->refined += __popc(m64); W->hits += __popc(hm); }
+    if (lane == 0) { W->refined += n; W->hits += __popc(hm); W->fn = fn - n; }
     __syncwarp();
+}
+
+// Evaluate queued pairs [base, base + n), n <= 32 (lane k takes pair k): certain
+// hits with an accurate fp32 interval are appended; the undecided go to the fp64
+// queue, which is evaluated 32 at a time (a warp-wide fp64 pass per 32 pairs that
+// need it, not per flush).  Entries flagged F64_FLAG skip the fp32 stage.
+template <bool EXACT>
+__device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n, uint32_t base = 0) {
+    const int lane = threadIdx.x & 31;
+    const bool v = (uint32_t)lane < n;
+    const uint32_t qraw = v ? W->rq[base + lane] : 0u, j = v ? W->rj[base + lane] : 0u;
+    const uint32_t q = qraw & ~F64_FLAG;
+    __syncwarp();                    // queue slots read: later queue_add may reuse them
+    float tin = 0.f, tout = 0.f;
+    int k = 0;
+    if (v) {
+        if (qraw & F64_FLAG) {
+            k = 1;
+        } else {
+            const float4 qa = __ldg(C->Q + 2 * (uint64_t)q), qb = __ldg(C->Q + 2 * (uint64_t)q + 1);
+            const float4 ea = __ldg(C->rec + 2 * (uint64_t)j), eb = __ldg(C->rec + 2 * (uint64_t)j + 1);
+            const QConst qc = make_qconst(qa, qb, C->T0, C->T1);
+            k = hit_kind(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext), qc.t0c,
+                         qc.t1c, make_ecand(ea, eb), C->d, tin, tout);   // k == 0: no shared span
+        }
+    }
+    const bool hit = (k == 2), need64 = (k == 1);
+    const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
+    Rec r{q, eid, tin, tout};
+    append<EXACT>(C->o, *W, hit, r, lane);
+    const unsigned hm = __ballot_sync(FULL, hit);
+    if (hit) {   // per-query counts, aggregated over the lanes of the same query
+        const unsigned peers = __match_any_sync(hm, q);
+        if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&C->o.qcount[q], (uint32_t)__popc(peers));
+    }
+    // undecided pairs -> fp64 queue
+    const unsigned m64 = __ballot_sync(FULL, need64);
+    const uint32_t fn = W->fn;
+    if (need64) {
+        const uint32_t pos = fn + __popc(m64 & ((1u << lane) - 1u));
+        W->fq[pos] = q;
+        W->fj[pos] = j;
+    }
+    __syncwarp();
+    if (lane == 0) { W->hits += __popc(hm); W->fn = fn + __popc(m64); }
+    __syncwarp();
+    if (fn + __popc(m64) >= 32) flush64<EXACT>(C, W, 32);
 }
 
 // warp-wide: queue the pairs whose fp32 filter passed (no flush here)
@@ -617,23 +661,36 @@ __device__ __forceinline__ void queue_add(WarpState &W, uint32_t &qn, bool maybe
     qn += __popc(mb);
 }
 
+// warp-wide: queue four candidate slots at once (branch-free; the queue holds
+// < 32 entries before, so at most 32 + 4 x 32 after, within RQ_CAP)
+__device__ __forceinline__ void queue_add4(WarpState &W, uint32_t &qn, bool m0, bool m1, bool m2, bool m3,
+                                           uint32_t qid, uint32_t j0, uint32_t j1, uint32_t j2, uint32_t j3,
+                                           int lane) {
+    const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
+    const unsigned b2 = __ballot_sync(FULL, m2), b3 = __ballot_sync(FULL, m3);
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t p = qn;
+    if (m0) { const uint32_t k = p + __popc(b0 & lt); W.rq[k] = qid; W.rj[k] = j0; }
+    p += __popc(b0);
+    if (m1) { const uint32_t k = p + __popc(b1 & lt); W.rq[k] = qid; W.rj[k] = j1; }
+    p += __popc(b1);
+    if (m2) { const uint32_t k = p + __popc(b2 & lt); W.rq[k] = qid; W.rj[k] = j2; }
+    p += __popc(b2);
+    if (m3) { const uint32_t k = p + __popc(b3 & lt); W.rq[k] = qid; W.rj[k] = j3; }
+    qn = p + __popc(b3);
+}
+
 // warp-wide: evaluate queued pairs in fp64, 32 at a time, while >= 32 are queued
 template <bool EXACT>
 __device__ __forceinline__ void queue_drain(const PairCtx *C, WarpState &W, uint32_t &qn, int lane) {
     if (qn < 32) return;
     __syncwarp();
     uint32_t head = 0;
-    do {
-        if (head) {                      // move the next 32 to the front
-            uint32_t t1 = W.rq[head + lane], t2 = W.rj[head + lane];
-            __syncwarp();
-            W.rq[lane] = t1; W.rj[lane] = t2;
-            __syncwarp();
-        }
-        flush_refine<EXACT>(C, &W, 32);
+    do {                                 // flush 32 at a time in place
+        flush_refine<EXACT>(C, &W, 32, head);
         head += 32;
     } while (qn - head >= 32);
-    const uint32_t rest = qn - head;
+    const uint32_t rest = qn - head;     // move the remainder to the front
     uint32_t t1 = 0, t2 = 0;
     if ((uint32_t)lane < rest) { t1 = W.rq[head + lane]; t2 = W.rj[head + lane]; }
     __syncwarp();
@@ -872,8 +929,8 @@ __device__ __forceinline__ uint32_t handle_passed(const PairCtx *C, WarpState *W
         hits += __popc(hm1);
     }
     uint32_t qn = *qn_io;
-    queue_add(*W, qn, k0 == 1, qid, j0, lane);
-    queue_add(*W, qn, k1 == 1, qid, j1, lane);
+    queue_add(*W, qn, k0 == 1, qid | F64_FLAG, j0, lane);      // known undecided: straight to fp64
+    queue_add(*W, qn, k1 == 1, qid | F64_FLAG, j1, lane);
     queue_drain<EXACT>(C, *W, qn, lane);
     __syncwarp();
     if (lane == 0) *qn_io = qn;
@@ -1008,8 +1065,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 direct_hits += hits_g;
                 if (lane == g) owner_hits += hits_g;
                 uint32_t qn = W.qn;
-                queue_add(W.ws, qn, ka == 1, qid, ja, lane);
-                queue_add(W.ws, qn, kb == 1, qid, jb, lane);
+                queue_add(W.ws, qn, ka == 1, qid | F64_FLAG, ja, lane);   // known undecided: straight to fp64
+                queue_add(W.ws, qn, kb == 1, qid | F64_FLAG, jb, lane);
                 queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
                 __syncwarp();
                 if (lane == 0) W.qn = qn;
@@ -1099,10 +1156,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 } else {
                     // sparse: queue; the flush evaluates 32 at a time with every lane busy
                     uint32_t qn = W.qn;
-                    queue_add(W.ws, qn, m0, qid, j0, lane);
-                    queue_add(W.ws, qn, m1, qid, j1, lane);
-                    queue_add(W.ws, qn, m2, qid, j2, lane);
-                    queue_add(W.ws, qn, m3, qid, j3, lane);
+                    queue_add4(W.ws, qn, m0, m1, m2, m3, qid, j0, j1, j2, j3, lane);
                     queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
                     __syncwarp();
                     if (lane == 0) W.qn = qn;
@@ -1115,6 +1169,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     }
     __syncwarp();
     if (W.qn) flush_refine<EXACT>(&A.pc, &W.ws, W.qn);
+    if (W.ws.fn) flush64<EXACT>(&A.pc, &W.ws, W.ws.fn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
     if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
@@ -1330,6 +1385,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     }
     __syncwarp();                    // last queue_add writes -> flush reads
     if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
+    if (W.fn) flush64<EXACT>(&A.pc, &W, W.fn);
     warp_state_finish<EXACT>(A.pc.o, W, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
     if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
