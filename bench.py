@@ -414,27 +414,42 @@ def run_tds(args, ws, rank, local):
     search_ms = searches_ms
     pt_all = pair_tests_step if dist is None else sum_over_ranks(dist, float(pair_tests_step), dev)
     peaks = load_peaks()
-    # roofline of the dominant kernel: the pair kernel with the largest share.  The
-    # range kernels (GPUTemporal / GPUSpatioTemporal) reuse each loaded record for
-    # up to 32 queries and are bound by the FP32 ALUs (59 flops per scheduled pair
-    # test); GPUSpatial streams one record + id per pair test (FSG slices are per
-    # (query, cell)) and is bound by HBM (36 B per pair test).
+    # roofline of the dominant kernel: the pair kernel with the largest share.
+    # GPUSpatial streams one record + id per pair test (FSG slices are per (query,
+    # cell)) and is bound by HBM (36 B per pair test).  The range
+    # kernels (GPUTemporal / GPUSpatioTemporal) reuse each loaded record for up to
+    # 32 queries: their roof is the larger of the FP32 time (59 flops per scheduled
+    # pair test) and the HBM time of their algorithmic bytes (SURVEY 8(d):
+    # 36 B per entry of D + 48 B per query + 16 B per result record written), i.e.
+    # FP32 on sparse outputs and HBM on output-bound searches (Random-dense d=0.09).
     dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
     dk = per_kind[dom]
     kname = "k_pair_spatial" if dom == "spatial" else "k_pair_range"
     secs = dk["pair_kernel_ms"] / 1e3
+    hbm_peak = float(peaks.get("hbm_gbs", 6537.0))
+    alu_peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
     if dom == "spatial":
         achieved = BYTES_PER_SPATIAL_PAIR * dk["pair_tests"] / secs / 1e9
-        peak = float(peaks.get("hbm_gbs", 6537.0))
+        peak = hbm_peak
         roof = {"bound": "hbm", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); algorithmic 36 B (record + id) per pair test"}
     else:
-        achieved = FLOPS_PER_PAIR * dk["pair_tests"] / secs / 1e12
-        peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
-        roof = {"bound": "alu", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s",
-                "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
-                               "algorithmic 59 flops per scheduled pair test"}
+        flops = FLOPS_PER_PAIR * dk["pair_tests"]
+        nbytes = 36 * w.D.shape[0] + 48 * w.Q.shape[0] + 16 * dk["results"]
+        if nbytes / (hbm_peak * 1e9) > flops / (alu_peak * 1e12):
+            achieved = nbytes / secs / 1e9
+            peak = hbm_peak
+            roof = {"bound": "hbm", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); algorithmic bytes 36 B x |D| + 48 B x |Q| "
+                                   "+ 16 B x results (output-bound: the HBM time exceeds the FP32 time)"}
+        else:
+            achieved = flops / secs / 1e12
+            peak = alu_peak
+            roof = {"bound": "alu", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s",
+                    "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
+                                   "algorithmic 59 flops per scheduled pair test"}
     roof["frac"] = achieved / peak
     roof["traffic"] = ncu_traffic(args, kname, dom)
     roof["share_of_step"] = dk["pair_kernel_ms"] / statistics.median(step_ms)

@@ -551,6 +551,59 @@ __device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit,
     __syncwarp();
 }
 
+// Two appends of one warp step (a lane's two candidates of one query) with one
+// chunk reservation and one warp-state update: records of the first set take
+// slots used + rank, those of the second follow them.
+template <bool EXACT>
+__device__ __forceinline__ void append2(const OutArgs &o, WarpState &W, bool ha, bool hb, unsigned hma, unsigned hmb,
+                                        const Rec &ra, const Rec &rb, int lane) {
+    const uint32_t ka = __popc(hma), k = ka + __popc(hmb);
+    if (EXACT) {                     // (k <= 64 <= CS: one chunk refresh always makes room)
+        append<EXACT>(o, W, ha, ra, lane);
+        append<EXACT>(o, W, hb, rb, lane);
+        return;
+    }
+    unsigned long long base = W.ap_base;
+    uint32_t used = W.ap_used, size = W.ap_size, full = W.ap_full;
+    if (!full && used + k > size) {
+        if (size && lane == 0) o.chunk_used[base / o.CS] = used;
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(&o.st->reserved, (unsigned long long)o.CS);
+        nb = __shfl_sync(FULL, nb, 0);
+        if (nb >= o.cap) {
+            full = 1; size = 0; used = 0;
+        } else {
+            base = nb;
+            used = 0;
+            unsigned long long room = o.cap - nb;
+            size = room < o.CS ? (uint32_t)room : o.CS;
+        }
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t rka = __popc(hma & lt), rkb = ka + __popc(hmb & lt);
+    uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base;
+    if (ha) {
+        if (!full && used + rka < size) {
+            out[used + rka] = make_uint4(ra.qid, ra.eid, __float_as_uint(ra.t_in), __float_as_uint(ra.t_out));
+        } else {
+            o.redo[ra.qid] = 1;
+            atomicAdd(&o.st->dropped, 1ull);
+        }
+    }
+    if (hb) {
+        if (!full && used + rkb < size) {
+            out[used + rkb] = make_uint4(rb.qid, rb.eid, __float_as_uint(rb.t_in), __float_as_uint(rb.t_out));
+        } else {
+            o.redo[rb.qid] = 1;
+            atomicAdd(&o.st->dropped, 1ull);
+        }
+    }
+    if (!full) used = min(used + k, size);
+    __syncwarp();
+    if (lane == 0) { W.ap_base = base; W.ap_used = used; W.ap_size = size; W.ap_full = full; }
+    __syncwarp();
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void warp_state_finish(const OutArgs &o, WarpState &W, int lane) {
     __syncwarp();
@@ -918,15 +971,10 @@ __device__ __forceinline__ uint32_t handle_passed(const PairCtx *C, WarpState *W
     if (m1) k1 = hit_kind(q0, q1, t0c, t1c, e1, d, ti1, to1);
     uint32_t hits = 0;
     const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
-    if (hm0) {
-        Rec r{qid, k0 == 2 ? __ldg(C->perm + j0) : 0u, ti0, to0};
-        append<EXACT>(C->o, *W, k0 == 2, r, lane);
-        hits += __popc(hm0);
-    }
-    if (hm1) {
-        Rec r{qid, k1 == 2 ? __ldg(C->perm + j1) : 0u, ti1, to1};
-        append<EXACT>(C->o, *W, k1 == 2, r, lane);
-        hits += __popc(hm1);
+    if (hm0 | hm1) {
+        append2<EXACT>(C->o, *W, k0 == 2, k1 == 2, hm0, hm1, Rec{qid, k0 == 2 ? __ldg(C->perm + j0) : 0u, ti0, to0},
+                       Rec{qid, k1 == 2 ? __ldg(C->perm + j1) : 0u, ti1, to1}, lane);
+        hits = __popc(hm0) + __popc(hm1);
     }
     uint32_t qn = *qn_io;
     queue_add(*W, qn, k0 == 1, qid | F64_FLAG, j0, lane);      // known undecided: straight to fp64
@@ -1035,6 +1083,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         auto dense_pair = [&](unsigned mask, uint32_t ca, uint32_t cb, uint32_t cend, uint32_t ja, uint32_t jb) {
             const ECand ea = ecand_of(ja), eb = ecand_of(jb);
             const bool va = ca < cend, vb = cb < cend;
+            // entry rows of the lane's two candidates: loaded once per window (not per hit)
+            const uint32_t ida = va ? __ldg(A.pc.perm + ja) : 0u, idb = vb ? __ldg(A.pc.perm + jb) : 0u;
             uint32_t passes = 0;
             while (mask) {
                 const int g = __ffs(mask) - 1;
@@ -1047,30 +1097,26 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 if (!(va && ca >= glo && ca < ghi)) ka = 0;
                 if (!(vb && cb >= glo && cb < ghi)) kb = 0;
                 const unsigned pa = __ballot_sync(FULL, ka != 0), pb = __ballot_sync(FULL, kb != 0);
-                passes += __popc(pa) + __popc(pb);
                 if (!(pa | pb)) continue;
+                passes += __popc(pa) + __popc(pb);
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                uint32_t hits_g = 0;
                 const unsigned hma = __ballot_sync(FULL, ka == 2), hmb = __ballot_sync(FULL, kb == 2);
-                if (hma) {
-                    Rec r{qid, ka == 2 ? __ldg(A.pc.perm + ja) : 0u, tia, toa};
-                    append<EXACT>(A.pc.o, W.ws, ka == 2, r, lane);
-                    hits_g += __popc(hma);
+                if (hma | hmb) {
+                    append2<EXACT>(A.pc.o, W.ws, ka == 2, kb == 2, hma, hmb, Rec{qid, ida, tia, toa},
+                                   Rec{qid, idb, tib, tob}, lane);
+                    const uint32_t hits_g = __popc(hma) + __popc(hmb);
+                    direct_hits += hits_g;
+                    if (lane == g) owner_hits += hits_g;
                 }
-                if (hmb) {
-                    Rec r{qid, kb == 2 ? __ldg(A.pc.perm + jb) : 0u, tib, tob};
-                    append<EXACT>(A.pc.o, W.ws, kb == 2, r, lane);
-                    hits_g += __popc(hmb);
+                if ((pa & ~hma) | (pb & ~hmb)) {     // undecided in fp32: known fp64 pairs
+                    uint32_t qn = W.qn;
+                    queue_add(W.ws, qn, ka == 1, qid | F64_FLAG, ja, lane);
+                    queue_add(W.ws, qn, kb == 1, qid | F64_FLAG, jb, lane);
+                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
+                    __syncwarp();
+                    if (lane == 0) W.qn = qn;
+                    __syncwarp();
                 }
-                direct_hits += hits_g;
-                if (lane == g) owner_hits += hits_g;
-                uint32_t qn = W.qn;
-                queue_add(W.ws, qn, ka == 1, qid | F64_FLAG, ja, lane);   // known undecided: straight to fp64
-                queue_add(W.ws, qn, kb == 1, qid | F64_FLAG, jb, lane);
-                queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
-                __syncwarp();
-                if (lane == 0) W.qn = qn;
-                __syncwarp();
             }
             return passes;
         };
@@ -1780,7 +1826,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     cap = std::min<uint64_t>(cap, (1ull << 40));
     const int bps = spatial ? SPATIAL_BPS : RANGE_BPS;
     const uint64_t nwarps = (uint64_t)persistent_blocks(bps) * (PT / 32);
-    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(32, cap / (16 * nwarps)));
+    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(64, cap / (16 * nwarps)));  // >= 64: append2
     CS = (CS + 31) / 32 * 32;
     const uint64_t nchunks = (cap + CS - 1) / CS;
     DBuf<Rec> buf;
