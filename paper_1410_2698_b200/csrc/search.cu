@@ -551,18 +551,20 @@ __device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit,
     __syncwarp();
 }
 
-// Two appends of one warp step (a lane's two candidates of one query) with one
-// chunk reservation and one warp-state update: records of the first set take
-// slots used + rank, those of the second follow them.
-template <bool EXACT>
-__device__ __forceinline__ void append2(const OutArgs &o, WarpState &W, bool ha, bool hb, unsigned hma, unsigned hmb,
-                                        const Rec &ra, const Rec &rb, int lane) {
-    const uint32_t ka = __popc(hma), k = ka + __popc(hmb);
-    if (EXACT) {                     // (k <= 64 <= CS: one chunk refresh always makes room)
-        append<EXACT>(o, W, ha, ra, lane);
-        append<EXACT>(o, W, hb, rb, lane);
+// K appends of one warp step (a lane's K candidates of one query) with one chunk
+// reservation and one warp-state update: the records of set i follow those of
+// sets 0..i-1 (k <= 32 K <= CS, so one chunk refresh always makes room).
+template <bool EXACT, int K>
+__device__ __forceinline__ void appendK(const OutArgs &o, WarpState &W, const bool (&h)[K], const unsigned (&hm)[K],
+                                        const Rec (&r)[K], int lane) {
+    if (EXACT) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) append<EXACT>(o, W, h[i], r[i], lane);
         return;
     }
+    uint32_t k = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) k += __popc(hm[i]);
     unsigned long long base = W.ap_base;
     uint32_t used = W.ap_used, size = W.ap_size, full = W.ap_full;
     if (!full && used + k > size) {
@@ -580,28 +582,34 @@ __device__ __forceinline__ void append2(const OutArgs &o, WarpState &W, bool ha,
         }
     }
     const unsigned lt = (1u << lane) - 1u;
-    const uint32_t rka = __popc(hma & lt), rkb = ka + __popc(hmb & lt);
     uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base;
-    if (ha) {
-        if (!full && used + rka < size) {
-            out[used + rka] = make_uint4(ra.qid, ra.eid, __float_as_uint(ra.t_in), __float_as_uint(ra.t_out));
-        } else {
-            o.redo[ra.qid] = 1;
-            atomicAdd(&o.st->dropped, 1ull);
+    uint32_t pre = used;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const uint32_t slot = pre + __popc(hm[i] & lt);
+        if (h[i]) {
+            if (!full && slot < size) {
+                out[slot] = make_uint4(r[i].qid, r[i].eid, __float_as_uint(r[i].t_in), __float_as_uint(r[i].t_out));
+            } else {
+                o.redo[r[i].qid] = 1;
+                atomicAdd(&o.st->dropped, 1ull);
+            }
         }
-    }
-    if (hb) {
-        if (!full && used + rkb < size) {
-            out[used + rkb] = make_uint4(rb.qid, rb.eid, __float_as_uint(rb.t_in), __float_as_uint(rb.t_out));
-        } else {
-            o.redo[rb.qid] = 1;
-            atomicAdd(&o.st->dropped, 1ull);
-        }
+        pre += __popc(hm[i]);
     }
     if (!full) used = min(used + k, size);
     __syncwarp();
     if (lane == 0) { W.ap_base = base; W.ap_used = used; W.ap_size = size; W.ap_full = full; }
     __syncwarp();
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void append2(const OutArgs &o, WarpState &W, bool ha, bool hb, unsigned hma, unsigned hmb,
+                                        const Rec &ra, const Rec &rb, int lane) {
+    const bool h[2] = {ha, hb};
+    const unsigned hm[2] = {hma, hmb};
+    const Rec r[2] = {ra, rb};
+    appendK<EXACT, 2>(o, W, h, hm, r, lane);
 }
 
 template <bool EXACT>
@@ -1102,8 +1110,10 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 const unsigned hma = __ballot_sync(FULL, ka == 2), hmb = __ballot_sync(FULL, kb == 2);
                 if (hma | hmb) {
-                    append2<EXACT>(A.pc.o, W.ws, ka == 2, kb == 2, hma, hmb, Rec{qid, ida, tia, toa},
-                                   Rec{qid, idb, tib, tob}, lane);
+                    const bool h[2] = {ka == 2, kb == 2};
+                    const unsigned hm[2] = {hma, hmb};
+                    const Rec r[2] = {Rec{qid, ida, tia, toa}, Rec{qid, idb, tib, tob}};
+                    appendK<EXACT, 2>(A.pc.o, W.ws, h, hm, r, lane);
                     const uint32_t hits_g = __popc(hma) + __popc(hmb);
                     direct_hits += hits_g;
                     if (lane == g) owner_hits += hits_g;
@@ -1826,7 +1836,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     cap = std::min<uint64_t>(cap, (1ull << 40));
     const int bps = spatial ? SPATIAL_BPS : RANGE_BPS;
     const uint64_t nwarps = (uint64_t)persistent_blocks(bps) * (PT / 32);
-    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(64, cap / (16 * nwarps)));  // >= 64: append2
+    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(128, cap / (16 * nwarps)));  // >= 128: appendK
     CS = (CS + 31) / 32 * 32;
     const uint64_t nchunks = (cap + CS - 1) / CS;
     DBuf<Rec> buf;
