@@ -378,6 +378,11 @@ def run_tds(args, ws, rank, local):
         torch.cuda.synchronize(dev)
         barrier()
         step_ms.append(e0.elapsed_time(e1))
+        if os.environ.get("TDS_BENCH_STEPS") == "1":
+            free_b, _ = torch.cuda.mem_get_info(dev)
+            print(f"[bench] step {len(step_ms) - 1}: {step_ms[-1]:.3f} ms; torch reserved "
+                  f"{torch.cuda.memory_reserved(dev) / 1e9:.1f} GB, device free {free_b / 1e9:.1f} GB",
+                  file=sys.stderr, flush=True)
     sampler.mark(1)
     clocks = sampler.stop()
     launches = tds.kernel_launches() - launches0

@@ -104,29 +104,55 @@ void *dalloc_big(size_t bytes, cudaStream_t s);
 
 static uint64_t device_budget_bytes_now();
 
-// uncached budget, and the lock under which searches size and allocate result
-// buffers above 1 GB (concurrent searches then see each other's allocations)
-uint64_t device_budget_bytes_fresh() { return device_budget_bytes_now(); }
+// Memory budget for result buffers.  cudaMemGetInfo is slow (measured 2-80 ms per
+// call on B200 between large searches), so it is called once per device (and
+// again after an allocation failure): the budget is that snapshot (free memory +
+// memory the two pools held unused) minus what the pools hand out since, read
+// from their cheap used-memory counters.  Concurrent searches therefore see each
+// other's buffers; allocations by other libraries after the snapshot are not
+// tracked (the 0.45 factor and the halving retry on ENOMEM cover them).
+static uint64_t pools_used_bytes(int dev) {
+    cudaMemPool_t pools[2] = {nullptr, big_pool()};
+    cudaDeviceGetDefaultMemPool(&pools[0], dev);
+    uint64_t tot = 0;
+    for (cudaMemPool_t pool : pools) {
+        uint64_t used = 0;
+        if (pool && cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess) tot += used;
+    }
+    return tot;
+}
+
+static std::mutex g_budget_mu;
+static int g_budget_dev = -1;
+static uint64_t g_budget_avail0 = 0, g_budget_used0 = 0;
+
+static void budget_snapshot_locked(int dev) {
+    g_budget_avail0 = device_budget_bytes_now();
+    g_budget_used0 = pools_used_bytes(dev);
+    g_budget_dev = dev;
+}
+
+void device_budget_refresh() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_budget_mu);
+    budget_snapshot_locked(dev);
+}
+
+uint64_t device_budget_bytes() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_budget_mu);
+    if (dev != g_budget_dev || g_budget_avail0 == 0) budget_snapshot_locked(dev);
+    const uint64_t cap = g_budget_avail0 + g_budget_used0, used = pools_used_bytes(dev);
+    return used < cap ? cap - used : 0;
+}
+
+// the lock under which searches size and allocate result buffers above 1 GB
+// (concurrent searches then see each other's allocations in the pool counters)
 std::mutex &big_alloc_mutex() {
     static std::mutex m;
     return m;
-}
-
-// cached: cudaMemGetInfo costs up to milliseconds, so refresh at most every 0.5 s
-// (allocation failures fall back to smaller buffers)
-uint64_t device_budget_bytes() {
-    static thread_local uint64_t cached = 0;
-    static thread_local std::chrono::steady_clock::time_point when{};
-    static thread_local int dev_of = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto now = std::chrono::steady_clock::now();
-    if (dev != dev_of || cached == 0 || now - when > std::chrono::milliseconds(500)) {
-        cached = device_budget_bytes_now();
-        when = now;
-        dev_of = dev;
-    }
-    return cached;
 }
 
 static uint64_t device_budget_bytes_now() {
@@ -190,6 +216,7 @@ Trace::~Trace() {
         snprintf(b, sizeof b, " %s %.3f (host %.3f)", ev[i].first, ms, host_ms[i] - host_ms[i - 1]);
         line += b;
     }
+    line += notes;
     {   // pool reservations (GB): default pool, result pool
         int dev = 0;
         cudaGetDevice(&dev);

@@ -1812,6 +1812,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     TDS_CUDA(cudaStreamSynchronize(s));
     if (hs.bad) fail(TDS_EDATA, "query segment %llu has a non-finite value or t_end <= t_start", ~hs.bad);
     tm.mark(1);
+    tr.mark("sync");
     S.pair_tests = hs.pair_tests;
     S.fallback_queries = hs.fallback;
     S.kind = kind;
@@ -1820,18 +1821,16 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     uint64_t cap = capacity;
     std::unique_lock<std::mutex> big_lock;
     if (cap == 0) {
-        // budget: free device memory plus memory the pools hold unused (cached:
-        // cudaMemGetInfo costs up to milliseconds).  A buffer above 1 GB is sized from
-        // a fresh budget under a process-wide lock held until it is allocated, so
-        // concurrent searches (tds_search_many) do not over-commit the device.
+        // budget: the device memory available at the last snapshot minus what the
+        // pools hand out since (abi.cu; no cudaMemGetInfo per search).  Buffers above
+        // 1 GB are sized and allocated under a process-wide lock, so concurrent
+        // searches (tds_search_many) do not over-commit the device.
         const uint64_t want = hs.pair_tests + 64;
-        uint64_t budget_bytes = device_budget_bytes();
-        if (want * sizeof(Rec) > (1ull << 30)) {
-            big_lock = std::unique_lock<std::mutex>(big_alloc_mutex());
-            budget_bytes = device_budget_bytes_fresh();
-        }
+        if (want * sizeof(Rec) > (1ull << 30)) big_lock = std::unique_lock<std::mutex>(big_alloc_mutex());
+        const uint64_t budget_bytes = device_budget_bytes();
         cap = std::min<uint64_t>(want, (uint64_t)(budget_bytes * 0.45) / sizeof(Rec));
         cap = std::max<uint64_t>(cap, 1024);
+        tr.mark(big_lock.owns_lock() ? "budget(locked)" : "budget");
     }
     cap = std::min<uint64_t>(cap, (1ull << 40));
     const int bps = spatial ? SPATIAL_BPS : RANGE_BPS;
@@ -1847,13 +1846,13 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         } catch (const Error &e) {
             if (e.code != TDS_ENOMEM || capacity != 0 || cap <= (1ull << 20)) throw;
             cap /= 2;                     // auto capacity: retry smaller (overflow re-plan covers the rest)
+            device_budget_refresh();      // memory use changed outside the pools
             set_error(0, "");
         }
     }
-    if (big_lock.owns_lock()) {
-        TDS_CUDA(cudaStreamSynchronize(s));     // the allocation is visible to the next budget query
-        big_lock.unlock();
-    }
+    tr.mark("alloc");
+    tr.note("cap_GB", cap * sizeof(Rec) / 1e9);
+    if (big_lock.owns_lock()) big_lock.unlock();   // the pool counts the buffer from here on
     DBuf<uint32_t> chunk_used(nchunks, s);
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
 

@@ -192,11 +192,18 @@ struct Trace {
     std::vector<double> host_ms;       // host wall clock at each mark
     explicit Trace(cudaStream_t s_);
     void mark(const char *name);
+    std::string notes;                 // extra key=value pairs printed with the trace
+    void note(const char *key, double v) {
+        if (!on) return;
+        char b[64];
+        snprintf(b, sizeof b, " %s=%.3f", key, v);
+        notes += b;
+    }
     ~Trace();
 };
 // free device memory + memory reserved but unused in the default mempool (bytes)
-uint64_t device_budget_bytes();
-uint64_t device_budget_bytes_fresh();
+uint64_t device_budget_bytes();        // snapshot minus pool use since (cheap)
+void device_budget_refresh();          // new snapshot (cudaMemGetInfo), after ENOMEM
 std::mutex &big_alloc_mutex();
 
 // ---------------------------------------------------------------------------

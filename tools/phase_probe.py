@@ -41,4 +41,6 @@ for step in range(a.steps):
                    f"sched {st['ms_schedule']:.3f} pairs {st['ms_pairs']:.3f} compact {st['ms_compact']:.3f}")
     idx.close()
     torch.cuda.synchronize()
-    print(step, f"build {1e3*(t1-t0):.3f}", " || ".join(out), flush=True)
+    free, total = torch.cuda.mem_get_info()
+    print(step, f"build {1e3*(t1-t0):.3f}", " || ".join(out),
+          f"| torch reserved {torch.cuda.memory_reserved() / 1e9:.1f} GB, device free {free / 1e9:.1f} GB", flush=True)
