@@ -203,10 +203,11 @@ __device__ __forceinline__ void cell_box(const float4 &a, const float4 &b, const
 }
 
 // cell-ordered copies for the GPUSpatial pair kernel: record, original row and
-// min / max cell of entry A[i] at position i
+// min cell of entry A[i] at position i (the duplicate-avoidance test needs only
+// the min corner: 4 B per pair test instead of 8 for min / max)
 __global__ void k_fsg_materialise(const float4 *__restrict__ rec, const uint32_t *__restrict__ perm,
                                   const uint32_t *__restrict__ A, uint64_t len, Grid3 G, float4 *__restrict__ frec,
-                                  uint32_t *__restrict__ fperm, uint2 *__restrict__ ecell) {
+                                  uint32_t *__restrict__ fperm, uint32_t *__restrict__ ecell) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= len) return;
     const uint32_t e = A[i];
@@ -216,7 +217,7 @@ __global__ void k_fsg_materialise(const float4 *__restrict__ rec, const uint32_t
     frec[2 * i] = a;
     frec[2 * i + 1] = b;
     fperm[i] = perm[e];
-    ecell[i] = make_uint2(pack_cell(lo[0], lo[1], lo[2]), pack_cell(hi[0], hi[1], hi[2]));
+    ecell[i] = pack_cell(lo[0], lo[1], lo[2]);
 }
 
 // A5 + A4 phase 1 in one pass over the records: per entry, the number of slabs
@@ -547,7 +548,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         DBuf<uint32_t> off(ncell + 1, s);
         group_by_key(fk, fv, len, ncell, off.p, s);
         fk.reset();
-        DBuf<uint2> ecell(len, s);
+        DBuf<uint32_t> ecell(len, s);
         DBuf<float4> frec(2 * len, s);
         DBuf<uint32_t> fperm(len, s);
         k_fsg_materialise<<<nblk(len), NT, 0, s>>>(rec.p, perm.p, fv.p, len, G, frec.p, fperm.p, ecell.p);

@@ -1322,7 +1322,7 @@ __global__ void k_fsg_items(const uint32_t *__restrict__ item_start, uint32_t n,
 
 struct SpatialArgs {
     PairCtx pc;                      // rec / perm = the cell-ordered copies (indexed by A position)
-    const uint2 *ecell;              // packed min / max cell of entry A[i]
+    const uint32_t *ecell;           // packed min cell of entry A[i]
     const uint32_t *grab_row;        // [ngrab + 1] row of the first slot of each grab
     const uint32_t *cell_off;
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
@@ -1405,7 +1405,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                 pp[u] = r_p;
             }
             float4 ea[SB], eb[SB];
-            uint2 ec[SB];
+            uint32_t ec[SB];
 #pragma unroll
             for (int u = 0; u < SB; ++u) {          // coalesced: consecutive slots, consecutive i
                 ea[u] = __ldg(A.pc.rec + 2 * (uint64_t)ii[u]);
@@ -1425,7 +1425,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                     }
                     // duplicate avoidance: test (q, e) only in the first cell (index-space
                     // min corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
-                    const uint32_t m0 = ec[u].x;
+                    const uint32_t m0 = ec[u];
                     const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
                     const int rz = max((int)(m0 & 0x3ffu), qlo.z);
                     const bool first = pack_cell(rx, ry, rz) == cxy[u];

@@ -111,7 +111,7 @@ struct tds_index_s {
     // FSG as a dense CSR over all cells + lookup array A
     uint32_t *cell_off = nullptr;   // [gx*gy*gz+1]
     uint32_t *fsg_A = nullptr;      // [A_len] sorted positions
-    uint2 *fsg_ecell = nullptr;     // [A_len] min / max cell of entry A[i]'s MBB, packed x<<21 | y<<10 | z
+    uint32_t *fsg_ecell = nullptr;  // [A_len] min cell of entry A[i]'s MBB, packed x<<21 | y<<10 | z
     float4 *fsg_rec = nullptr;      // [2 A_len] record of entry A[i] (cell-ordered copy, coalesced streaming)
     uint32_t *fsg_perm = nullptr;   // [A_len] original row of entry A[i]
     uint64_t A_len = 0;
