@@ -30,7 +30,7 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #define TDS_RANGE_BPS 2
 #endif
 #ifndef TDS_SPATIAL_BPS
-#define TDS_SPATIAL_BPS 2
+#define TDS_SPATIAL_BPS 3
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
