@@ -1328,9 +1328,17 @@ struct SpatialArgs {
     const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
     const uint32_t *row_q, *row_alo, *row_cxy;   // work items (query, cell): query, slice start, packed cell
     const unsigned long long *slot_start;   // [nrows + 1]
+    const uint32_t *slot_row;        // [slots] row of each slot (small searches), else nullptr
     uint32_t nrows;
     FsgGrid G;
 };
+
+// Small searches (<= SLOT_ROW_MAX slots): the row of every slot, found by one
+// thread per slot in parallel, so the pair kernel needs one load per row change
+// instead of a dependent binary search (most (query, cell-row) items of a small
+// search are empty after time trimming: on Random-1M-shaped data a row change
+// per slot, each a ~10-level chain of L2 loads, set the kernel time).
+constexpr unsigned long long SLOT_ROW_MAX = 1ull << 22;
 
 __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint32_t lo, uint32_t hi,
                                              unsigned long long s) {
@@ -1340,6 +1348,12 @@ __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint3
         if (ss[mid] <= s) lo = mid; else hi = mid;
     }
     return lo;
+}
+
+__global__ void k_slot_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, uint64_t nslots,
+                            uint32_t *__restrict__ slot_row) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nslots) slot_row[k] = find_row(ss, 0, nrows, k);
 }
 
 __global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, uint64_t ngrab,
@@ -1379,7 +1393,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
         const uint32_t rlo = A.grab_row[gi], rhi = A.grab_row[gi + 1] + 1;
         // row of this lane's first slot (small search inside the grab's row range);
         // later slots advance the row linearly (rows are consecutive in slot order)
-        uint32_t r = find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
+        uint32_t r = A.slot_row ? A.slot_row[min(B + lane, Bend - 1)] : find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
         unsigned long long r_start = A.slot_start[r], r_next = A.slot_start[r + 1];
         uint32_t r_alo = A.row_alo[r], r_cxy = A.row_cxy[r], r_p = A.row_q[r];
         exec += Bend - B;
@@ -1393,7 +1407,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                 vv[u] = s < Bend;
                 if (vv[u] && s >= r_next) {
                     // next item holding slot s (binary search: many (query, cell) items are empty)
-                    r = find_row(A.slot_start, r + 1, rhi, s);
+                    r = A.slot_row ? A.slot_row[s] : find_row(A.slot_start, r + 1, rhi, s);
                     r_start = A.slot_start[r];
                     r_next = A.slot_start[r + 1];
                     r_alo = A.row_alo[r];
@@ -1877,7 +1891,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         DBuf<uint32_t> grab_row(ngrab + 1, s);
         k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, ngrab, grab_row.p);
         TDS_CHECK_LAUNCH();
+        DBuf<uint32_t> slot_row;
+        if (hs.pair_tests <= SLOT_ROW_MAX) {
+            slot_row = DBuf<uint32_t>(hs.pair_tests, s);
+            k_slot_rows<<<nblk(hs.pair_tests), 256, 0, s>>>(slot_start.p, nrows, hs.pair_tests, slot_row.p);
+            TDS_CHECK_LAUNCH();
+        }
         SpatialArgs a{};
+        a.slot_row = slot_row.p;
         a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
         a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
@@ -2104,7 +2125,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             DBuf<uint32_t> grab_row(ngrab + 1, s);
             k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, ngrab, grab_row.p);
             TDS_CHECK_LAUNCH();
+            DBuf<uint32_t> slot_row;
+            if (bslots && bslots <= SLOT_ROW_MAX) {
+                slot_row = DBuf<uint32_t>(bslots, s);
+                k_slot_rows<<<nblk(bslots), 256, 0, s>>>(ss.p, bnrows, bslots, slot_row.p);
+                TDS_CHECK_LAUNCH();
+            }
             SpatialArgs a{};
+            a.slot_row = slot_row.p;
             a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
             a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;

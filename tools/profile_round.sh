@@ -24,4 +24,11 @@ for spec in "random1m_temporal --variants temporal" "rdense01_temporal --config 
   ncu -i $out/ncu_$name.ncu-rep --page raw --csv > $out/ncu_$name.raw.csv 2>/dev/null
   rm -f $out/ncu_$name.ncu-rep
 done
+# output-bound range kernel on a query subsample (tools/prof_dense.py), with the source page
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pair_range -c 1 --launch-skip 3 \
+    -o $out/ncu_rdense09_temporal -f python tools/prof_dense.py 0.09 5000 temporal > $out/ncu_rdense09_temporal.log 2>&1
+ncu -i $out/ncu_rdense09_temporal.ncu-rep --page details --csv > $out/ncu_rdense09_temporal.details.csv 2>/dev/null
+ncu -i $out/ncu_rdense09_temporal.ncu-rep --page raw --csv > $out/ncu_rdense09_temporal.raw.csv 2>/dev/null
+ncu -i $out/ncu_rdense09_temporal.ncu-rep --page source --csv > $out/ncu_rdense09_temporal.source.csv 2>/dev/null
+rm -f $out/ncu_rdense09_temporal.ncu-rep
 ls $out
