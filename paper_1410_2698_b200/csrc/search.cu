@@ -776,6 +776,8 @@ struct SchedArgs {
     uint32_t *vals;                  // identity (sort payload)
     int lo_shift;
     int count_t;                     // TDS_AUTO: also sum the temporal ranges (pair_tests_t)
+    const float4 *rec;               // sorted entries (tight ranges)
+    int tight;                       // trim the bin hull to entry-exact ends
     DevStats *st;
 };
 
@@ -816,6 +818,26 @@ __global__ void k_schedule(SchedArgs A) {
             if (jlo < jhe) {
                 S.lo = A.bin_off[jlo];
                 S.hi = A.bin_off[jhe];
+                if (A.tight && S.lo < S.hi) {
+                    // entry-exact ends (bin-free tight range).  hi: only bin
+                    // jhe-1 can hold entries with t_start >= t1c (every earlier bin ends
+                    // before the next bin's first t_start < t1c); t_start is sorted, so a
+                    // binary search there gives the first one.  lo: the prefix max of t_end
+                    // before bin jlo is <= t0c, so entries of bin jlo are skipped while
+                    // their own t_end <= t0c (at most 64 tested; the skipped ones cannot
+                    // overlap under C5, so stopping early stays complete).
+                    uint32_t b = max(S.lo, A.bin_off[jhe - 1]), e = S.hi;
+                    while (b < e) {
+                        const uint32_t mid = (b + e) >> 1;
+                        if (__ldg(&A.rec[2 * (uint64_t)mid].w) < t1c) b = mid + 1; else e = mid;
+                    }
+                    S.hi = b;
+                    const uint32_t cap = min(S.hi, S.lo + 64u);
+                    uint32_t l = S.lo;
+                    while (l < cap && !(__ldg(&A.rec[2 * (uint64_t)l + 1].w) > t0c)) ++l;
+                    S.lo = l;
+                    if (S.lo > S.hi) S.lo = S.hi;
+                }
                 S.sel = S.lo < S.hi ? -1 : 3;
                 work_t = S.hi - S.lo;
                 if (A.use_st && S.sel == -1) {
@@ -1644,6 +1666,16 @@ DevStats *pinned_stats() {
 
 // TDS_FSG_LITERAL=1: GPUSpatial candidates are whole cells, as in the paper
 // (no per-cell time trimming) — for ablation
+// TDS_TIGHT_RANGE=1: entry-exact candidate range ends instead of the hull of the
+// overlapping bins (the paper's granularity).  An ablation, off by default: on
+// Random-1M-shaped data it removes < 1 bin of slack per side and measured within
+// noise, while its extra schedule loads shift the overlap of the concurrent
+// searches of a bench step
+int tight_ranges() {
+    const char *e = getenv("TDS_TIGHT_RANGE");
+    return (e && e[0] == '1') ? 1 : 0;
+}
+
 int fsg_literal() {
     const char *e = getenv("TDS_FSG_LITERAL");
     return (e && e[0] == '1') ? 1 : 0;
@@ -1755,6 +1787,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.lo_shift = std::max(0, lo_bits - 13);
         a.st = dst.p;
         a.count_t = (req_kind == TDS_AUTO && a.use_st) ? 1 : 0;
+        a.rec = idx->rec;
+        a.tight = tight_ranges();
         k_schedule<<<nblk(n), 256, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
         if (a.count_t) {
@@ -1903,7 +1937,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
-        k_pair_spatial<false><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
+        // persistent grid, but no more blocks than grabs / warps per block: a small
+        // search (Random-1M-shaped: a few hundred grabs) does not launch 444 blocks
+        // that mostly find no work
+        const int sp_blocks = (int)std::min<uint64_t>(persistent_blocks(SPATIAL_BPS), (ngrab + PT / 32 - 1) / (PT / 32));
+        k_pair_spatial<false><<<sp_blocks, PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
     }
     tm.mark(3);
@@ -2138,7 +2176,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;
             if (bnrows && bslots) {
-                k_pair_spatial<true><<<persistent_blocks(SPATIAL_BPS), PT, 0, s>>>(a);
+                const int sp_blocks =
+                    (int)std::min<uint64_t>(persistent_blocks(SPATIAL_BPS), (ngrab + PT / 32 - 1) / (PT / 32));
+                k_pair_spatial<true><<<sp_blocks, PT, 0, s>>>(a);
                 TDS_CHECK_LAUNCH();
             }
             TDS_CUDA(cudaStreamSynchronize(s));

@@ -439,3 +439,26 @@ def test_auto_kind_choice(tds, v, expect):
     b = idx.search(_cuda(w.Q), 5.0, kind=expect).fetch(sorted=True, device=False)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", ["tiny", "random-1m-small"])
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
+def test_tight_range_equals_bin_hull(tds, name, kind, monkeypatch):
+    """Entry-exact candidate ranges (TDS_TIGHT_RANGE=1) return
+    exactly the result of the paper-granularity bin hull (default)
+    with no more pair tests."""
+    if name == "tiny":
+        w = synth.tiny()
+        d = w.d
+    else:
+        w = synth.random_1m(n_traj=300, query_frac_stride=10)
+        d = 20.0
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    hull, st_h = _run(idx, w.Q, d, kind)
+    monkeypatch.setenv("TDS_TIGHT_RANGE", "1")
+    got, st = _run(idx, w.Q, d, kind)
+    monkeypatch.delenv("TDS_TIGHT_RANGE")
+    assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(hull[0], hull[1])))
+    assert st["pair_tests"] <= st_h["pair_tests"]
+    if name != "tiny" and kind == "temporal":
+        assert st["pair_tests"] < st_h["pair_tests"]
