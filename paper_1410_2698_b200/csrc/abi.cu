@@ -13,7 +13,15 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (CUDA toolkit): ranges for profilers
 #include "tds_internal.cuh"
+
+// NVTX range over one C-ABI call (visible in nsys / ncu timelines; a few ns
+// when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace tds {
 
@@ -196,6 +204,7 @@ Trace::Trace(cudaStream_t s_) : s(s_) {
 }
 
 void Trace::mark(const char *name) {
+    nvtxMarkA(name);                   // phase ends as NVTX markers (always)
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -320,6 +329,7 @@ uint64_t tds_kernel_launches(void) { return tds::g_launches.load(); }
 
 int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *params, void *stream,
                     tds_index *out) {
+    NvtxRange nvtx_range("tds_build_index");
     ABI_TRY
     tds::set_error(0, "");
     if (!out || !params) fail(TDS_EINVAL, "NULL argument");
@@ -354,6 +364,7 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
 
 int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
                uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results) {
+    NvtxRange nvtx_range("tds_search");
     ABI_TRY
     tds::set_error(0, "");
     if (!idx || !out) fail(TDS_EINVAL, "NULL argument");
@@ -448,6 +459,7 @@ SearchPool &search_pool() {
 extern "C" {
 
 int tds_search_many(tds_index idx, int n, const tds_search_req *reqs, tds_result *out, uint64_t *n_results) {
+    NvtxRange nvtx_range("tds_search_many");
     ABI_TRY
     tds::set_error(0, "");
     if (n < 0 || (n > 0 && (!reqs || !out))) fail(TDS_EINVAL, "bad request list");
@@ -493,6 +505,7 @@ int tds_search_many(tds_index idx, int n, const tds_search_req *reqs, tds_result
 
 int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *query_id, uint32_t *entry_id,
                       float *t_in, float *t_out, int dst_is_device, int sorted, void *stream) {
+    NvtxRange nvtx_range("tds_fetch_results");
     ABI_TRY
     tds::set_error(0, "");
     if (!r) fail(TDS_EINVAL, "NULL result");
@@ -504,6 +517,7 @@ int tds_fetch_results(tds_result r, uint64_t first, uint64_t count, uint32_t *qu
 
 int tds_merge_trajectories(tds_result r, const uint32_t *q_traj, uint64_t nq, const uint32_t *e_traj, uint64_t ne,
                            float gap, void *stream, tds_result *out, uint64_t *n_out) {
+    NvtxRange nvtx_range("tds_merge_trajectories");
     ABI_TRY
     tds::set_error(0, "");
     if (!r || !out) fail(TDS_EINVAL, "NULL argument");
