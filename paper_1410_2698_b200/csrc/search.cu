@@ -35,7 +35,10 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
-constexpr int DIRECT_MIN = 16;           // filter passes per 64-candidate window for the in-place path
+#ifndef TDS_DIRECT_MIN
+#define TDS_DIRECT_MIN 16
+#endif
+constexpr int DIRECT_MIN = TDS_DIRECT_MIN;  // filter passes per 64-candidate window for the in-place path
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
