@@ -35,9 +35,19 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
+#ifndef TDS_HYST
+#define TDS_HYST 1            // dense/sparse window choice with hysteresis (HYST_HI / HYST_LO)
+#endif
+#ifndef TDS_HYST_HI
+#define TDS_HYST_HI 50
+#endif
+#ifndef TDS_HYST_LO
+#define TDS_HYST_LO 25
+#endif
 #ifndef TDS_DIRECT_MIN
 #define TDS_DIRECT_MIN 16
 #endif
+constexpr int HYST_HI = TDS_HYST_HI, HYST_LO = TDS_HYST_LO;   // % of a window's pairs passing the filter
 constexpr int DIRECT_MIN = TDS_DIRECT_MIN;  // filter passes per 64-candidate window for the in-place path
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
@@ -1186,10 +1196,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     if (h && base + 64 >= cend) break;
                     passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
                 }
+#if TDS_HYST
+                // stay dense while >= HYST_LO % of the window's (query, slot) pairs pass
+                dense = 100u * passes >= (uint32_t)HYST_LO * __popc(wmask) * (cend - base);
+#else
                 dense = passes >= (uint32_t)DIRECT_MIN * __popc(wmask) * 2u;
+#endif
                 base = cend;
                 continue;
             }
+            uint32_t wpass = 0;                // filter passes of this window (all queries)
             FSeg2 f01, f23;
             {
                 float4 a0, b0, a1, b1;
@@ -1219,7 +1235,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 const uint32_t qid = __shfl_sync(FULL, S.qid, g);
                 const uint32_t npass = __popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) +
                                        __popc(__ballot_sync(FULL, m2)) + __popc(__ballot_sync(FULL, m3));
-                if (npass >= 2u * DIRECT_MIN) {
+                wpass += npass;
+                if (!TDS_HYST && npass >= 2u * DIRECT_MIN) {
                     // dense: most lanes passed -> in place (fp32 interval or fp64 queue); the
                     // following windows use the fused path.  Candidates are re-read (L1) in
                     // the relative form the interval needs.
@@ -1244,6 +1261,12 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     __syncwarp();
                 }
             }
+#if TDS_HYST
+            // switch to the fused dense path once >= HYST_HI % of the window's pairs pass
+            // (two thresholds: a window mix near one threshold toggled between the
+            // paths, and the in-place transition was slower than either)
+            dense = 100u * wpass >= (uint32_t)HYST_HI * __popc(wmask) * (cend - base);
+#endif
             base = cend;
         }
         if (owner_hits) atomicAdd(&A.pc.o.qcount[S.qid], owner_hits);
