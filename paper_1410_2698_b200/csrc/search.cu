@@ -35,6 +35,9 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
+#ifndef TDS_DENSE4
+#define TDS_DENSE4 0          // dense windows: four candidates per query step (two chains)
+#endif
 #ifndef TDS_HYST
 #define TDS_HYST 1            // dense/sparse window choice with hysteresis (HYST_HI / HYST_LO)
 #endif
@@ -1165,6 +1168,58 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             }
             return passes;
         };
+#if TDS_DENSE4
+        // dense windows: per query, the lane's four candidates as two independent packed
+        // hit_kind2 chains (one chain per query step is latency-bound), one append
+        auto dense_quad = [&](unsigned mask, uint32_t c0, uint32_t cend, uint32_t j0, uint32_t j1, uint32_t j2,
+                              uint32_t j3) {
+            const ECand e0 = ecand_of(j0), e1 = ecand_of(j1), e2 = ecand_of(j2), e3 = ecand_of(j3);
+            const uint32_t id0 = c0 < cend ? __ldg(A.pc.perm + j0) : 0u, id1 = c0 + 32 < cend ? __ldg(A.pc.perm + j1) : 0u,
+                           id2 = c0 + 64 < cend ? __ldg(A.pc.perm + j2) : 0u, id3 = c0 + 96 < cend ? __ldg(A.pc.perm + j3) : 0u;
+            uint32_t passes = 0;
+            while (mask) {
+                const int g = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
+                const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
+                float ti[4], to[4];
+                int kk[4];
+                hit_kind2(q0, q1, q2.x, q2.y, e0, e1, d, kk[0], ti[0], to[0], kk[1], ti[1], to[1]);
+                hit_kind2(q0, q1, q2.x, q2.y, e2, e3, d, kk[2], ti[2], to[2], kk[3], ti[3], to[3]);
+                // slot c valid for query g iff glo <= c < ghi (ghi <= whi) and c < cend
+                const uint32_t gw = ghi - glo, o0 = c0 - glo;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (!(o0 + 32u * i < gw) || !(c0 + 32u * i < cend)) kk[i] = 0;
+                unsigned pm[4], hm[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pm[i] = __ballot_sync(FULL, kk[i] != 0);
+                if (!((pm[0] | pm[1]) | (pm[2] | pm[3]))) continue;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) { passes += __popc(pm[i]); hm[i] = __ballot_sync(FULL, kk[i] == 2); }
+                const uint32_t qid = __shfl_sync(FULL, S.qid, g);
+                if ((hm[0] | hm[1]) | (hm[2] | hm[3])) {
+                    const bool h[4] = {kk[0] == 2, kk[1] == 2, kk[2] == 2, kk[3] == 2};
+                    const Rec r[4] = {Rec{qid, id0, ti[0], to[0]}, Rec{qid, id1, ti[1], to[1]},
+                                      Rec{qid, id2, ti[2], to[2]}, Rec{qid, id3, ti[3], to[3]}};
+                    appendK<EXACT, 4>(A.pc.o, W.ws, h, hm, r, lane);
+                    const uint32_t hits_g = __popc(hm[0]) + __popc(hm[1]) + __popc(hm[2]) + __popc(hm[3]);
+                    direct_hits += hits_g;
+                    if (lane == g) owner_hits += hits_g;
+                }
+                if (((pm[0] & ~hm[0]) | (pm[1] & ~hm[1])) | ((pm[2] & ~hm[2]) | (pm[3] & ~hm[3]))) {
+                    uint32_t qn = W.qn;          // undecided in fp32: known fp64 pairs
+                    queue_add4(W.ws, qn, kk[0] == 1, kk[1] == 1, kk[2] == 1, kk[3] == 1, qid | F64_FLAG, j0, j1, j2,
+                               j3, lane);
+                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
+                    __syncwarp();
+                    if (lane == 0) W.qn = qn;
+                    __syncwarp();
+                }
+            }
+            return passes;
+        };
+#endif
         uint32_t base = wlo;
         while (base < whi) {
             const uint32_t cend = min(base + WIN, whi);
@@ -1190,12 +1245,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     load_cand(c2, c2 < cend, j2, a, b);
                     load_cand(c3, c3 < cend, j3, a, b);
                 }
+#if TDS_DENSE4
+                const uint32_t passes = dense_quad(mask, c0, cend, j0, j1, j2, j3);
+#else
                 uint32_t passes = 0;
 #pragma unroll 1
                 for (int h = 0; h < 2; ++h) {      // one copy of the dense code (i-cache)
                     if (h && base + 64 >= cend) break;
                     passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
                 }
+#endif
 #if TDS_HYST
                 // stay dense while >= HYST_LO % of the window's (query, slot) pairs pass
                 dense = 100u * passes >= (uint32_t)HYST_LO * __popc(wmask) * (cend - base);
