@@ -36,7 +36,7 @@ constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range 
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 #ifndef TDS_DENSE4
-#define TDS_DENSE4 0          // dense windows: four candidates per query step (two chains)
+#define TDS_DENSE4 2          // dense windows, four candidates per query step: 0 never, 1 always, 2 by probe
 #endif
 #ifndef TDS_HYST
 #define TDS_HYST 1            // dense/sparse window choice with hysteresis (HYST_HI / HYST_LO)
@@ -50,7 +50,8 @@ constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial ker
 #ifndef TDS_DIRECT_MIN
 #define TDS_DIRECT_MIN 16
 #endif
-constexpr int HYST_HI = TDS_HYST_HI, HYST_LO = TDS_HYST_LO;   // % of a window's pairs passing the filter
+constexpr int HYST_HI = TDS_HYST_HI, HYST_LO = TDS_HYST_LO;
+constexpr unsigned long long PROBE_MIN_PAIRS = 1ull << 28;   // density probe only above this many pair tests   // % of a window's pairs passing the filter
 constexpr int DIRECT_MIN = TDS_DIRECT_MIN;  // filter passes per 64-candidate window for the in-place path
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
@@ -75,7 +76,8 @@ struct DevStats {
     unsigned int total_items;
     unsigned int ch;                 // candidates per work item
     unsigned int cat_cnt[5];         // schedule entries per category
-    unsigned int pad[5];
+    unsigned int probe_pass, probe_total;   // density probe (k_density_probe)
+    unsigned int pad[3];
 };
 
 struct Sched {                       // 16 B schedule entry
@@ -1039,6 +1041,40 @@ struct __align__(16) RangeWarpSmem {
     uint32_t qn;                     // refine queue fill
 };
 
+// Density probe (per search, before the pair kernel): the fraction of filter
+// passes on up to 64 sampled schedule entries x 128 candidates from the middle of
+// their ranges, with the relative-form filter; decides whether the dense-heavy
+// D4 instantiation of k_pair_range runs.  One warp per sampled entry.
+__global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const float4 *__restrict__ Q,
+                                const float4 *__restrict__ rec, const uint32_t *__restrict__ arr0,
+                                const uint32_t *__restrict__ arr1, const uint32_t *__restrict__ arr2, float d, float T0,
+                                float T1, DevStats *st) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    if (n == 0) return;
+    const uint32_t p = (uint32_t)(((uint64_t)w * n) / nw + n / (2 * nw));
+    if (p >= n) return;
+    const Sched e = S[p];
+    if (e.sel == 3 || e.hi <= e.lo) return;
+    const uint32_t *arr = e.sel == 0 ? arr0 : e.sel == 1 ? arr1 : e.sel == 2 ? arr2 : nullptr;
+    const QConst qc = make_qconst(__ldg(Q + 2 * (uint64_t)e.qid), __ldg(Q + 2 * (uint64_t)e.qid + 1), T0, T1);
+    const float4 q0 = make_float4(qc.px, qc.py, qc.pz, qc.t0), q1 = make_float4(qc.vx, qc.vy, qc.vz, qc.ext);
+    const uint32_t len = e.hi - e.lo, m = min(len, 128u);
+    const uint32_t c0 = e.lo + (len - m) / 2;
+    uint32_t pass = 0;
+    for (uint32_t k = lane; k < m; k += 32) {
+        const uint32_t c = c0 + k, j = arr ? __ldg(arr + c) : c;
+        const ECand ec = make_ecand(__ldg(rec + 2 * (uint64_t)j), __ldg(rec + 2 * (uint64_t)j + 1));
+        pass += filter_pair(q0, q1, qc.t0c, qc.t1c, ec, d) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pass += __shfl_xor_sync(FULL, pass, o);
+    if (lane == 0) {
+        atomicAdd(&st->probe_pass, pass);
+        atomicAdd(&st->probe_total, m);
+    }
+}
+
 // Mapping: a work item is a group of <= 32
 // consecutive schedule entries (one category) and a chunk of the union of their
 // candidate ranges.  Lane g owns query g of the group (its constants are staged
@@ -1047,7 +1083,10 @@ struct __align__(16) RangeWarpSmem {
 // meets the current 32 candidates, so each loaded candidate is tested against
 // every query that needs it and gaps between ranges are skipped.  Pairs that
 // pass the fp32 filter are queued and evaluated 32 at a time in fp64.
-template <bool EXACT>
+// D4: the dense-window step takes four candidates per query (two hit_kind2
+// chains); its registers slow the sparse loop, so it is a separate instantiation
+// chosen per search by the density probe (k_density_probe).
+template <bool EXACT, bool D4 = false>
 __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_constant__ RangeArgs A) {
     __shared__ RangeWarpSmem sm[PT / 32];
     const int lane = threadIdx.x & 31;
@@ -1168,9 +1207,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             }
             return passes;
         };
-#if TDS_DENSE4
-        // dense windows: per query, the lane's four candidates as two independent packed
-        // hit_kind2 chains (one chain per query step is latency-bound), one append
+        // dense windows (D4 instantiation): per query, the lane's four candidates as two
+        // independent packed hit_kind2 chains (one chain per query step is latency-bound)
         auto dense_quad = [&](unsigned mask, uint32_t c0, uint32_t cend, uint32_t j0, uint32_t j1, uint32_t j2,
                               uint32_t j3) {
             const ECand e0 = ecand_of(j0), e1 = ecand_of(j1), e2 = ecand_of(j2), e3 = ecand_of(j3);
@@ -1219,7 +1257,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             }
             return passes;
         };
-#endif
         uint32_t base = wlo;
         while (base < whi) {
             const uint32_t cend = min(base + WIN, whi);
@@ -1245,16 +1282,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     load_cand(c2, c2 < cend, j2, a, b);
                     load_cand(c3, c3 < cend, j3, a, b);
                 }
-#if TDS_DENSE4
-                const uint32_t passes = dense_quad(mask, c0, cend, j0, j1, j2, j3);
-#else
                 uint32_t passes = 0;
+                if (D4) {
+                    passes = dense_quad(mask, c0, cend, j0, j1, j2, j3);
+                } else {
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {      // one copy of the dense code (i-cache)
-                    if (h && base + 64 >= cend) break;
-                    passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
+                    for (int h = 0; h < 2; ++h) {      // one copy of the dense code (i-cache)
+                        if (h && base + 64 >= cend) break;
+                        passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
+                    }
                 }
-#endif
 #if TDS_HYST
                 // stay dense while >= HYST_LO % of the window's (query, slot) pairs pass
                 dense = 100u * passes >= (uint32_t)HYST_LO * __popc(wmask) * (cend - base);
@@ -1950,6 +1987,19 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     S.fallback_queries = hs.fallback;
     S.kind = kind;
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
+    // density probe, on large range searches only (one small kernel + a read-back):
+    // dense-heavy searches (>= HYST_HI % of the probed pairs pass the filter) run the
+    // four-candidate dense step (the D4 instantiation of k_pair_range)
+    bool d4 = !spatial && TDS_DENSE4 == 1;
+    if (!spatial && TDS_DENSE4 == 2 && hs.pair_tests >= PROBE_MIN_PAIRS) {
+        k_density_probe<<<8, 256, 0, s>>>(sched.p, n, Q, idx->rec, idx->st_arr[0], idx->st_arr[1], idx->st_arr[2], d,
+                                          T0, T1, dst.p);
+        TDS_CHECK_LAUNCH();
+        TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        d4 = hs.probe_total && 100ull * hs.probe_pass >= (uint64_t)HYST_HI * hs.probe_total;
+        tr.note("probe_pass_frac", hs.probe_total ? (double)hs.probe_pass / hs.probe_total : -1.0);
+    }
 
     uint64_t cap = capacity;
     std::unique_lock<std::mutex> big_lock;
@@ -2003,8 +2053,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
         for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
-        k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+        if (d4) k_pair_range<false, true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+        else k_pair_range<false, false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
+        tr.note("dense4", d4 ? 1.0 : 0.0);
     } else if (nrows > 0 && hs.pair_tests > 0) {
         const uint64_t ngrab = (hs.pair_tests + SP_GRAB - 1) / SP_GRAB;
         DBuf<uint32_t> grab_row(ngrab + 1, s);
