@@ -1990,8 +1990,13 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // density probe, on large range searches only (one small kernel + a read-back):
     // dense-heavy searches (>= HYST_HI % of the probed pairs pass the filter) run the
     // four-candidate dense step (the D4 instantiation of k_pair_range)
-    bool d4 = !spatial && TDS_DENSE4 == 1;
-    if (!spatial && TDS_DENSE4 == 2 && hs.pair_tests >= PROBE_MIN_PAIRS) {
+    // TDS_DENSE4 (environment) = 0 / 1 overrides the build default (tests, ablation)
+    const int d4_mode = [] {
+        const char *e = getenv("TDS_DENSE4");
+        return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : TDS_DENSE4;
+    }();
+    bool d4 = !spatial && d4_mode == 1;
+    if (!spatial && d4_mode == 2 && hs.pair_tests >= PROBE_MIN_PAIRS) {
         k_density_probe<<<8, 256, 0, s>>>(sched.p, n, Q, idx->rec, idx->st_arr[0], idx->st_arr[1], idx->st_arr[2], d,
                                           T0, T1, dst.p);
         TDS_CHECK_LAUNCH();

@@ -462,3 +462,28 @@ def test_tight_range_equals_bin_hull(tds, name, kind, monkeypatch):
     assert st["pair_tests"] <= st_h["pair_tests"]
     if name != "tiny" and kind == "temporal":
         assert st["pair_tests"] < st_h["pair_tests"]
+
+
+@pytest.mark.parametrize("name", ["tiny", "random-dense-1m"])
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
+def test_dense4_instantiation_matches_oracle(tds, name, kind, monkeypatch):
+    """The four-candidate dense-window instantiation (chosen by the density probe
+    on large dense searches; forced here with TDS_DENSE4=1 on small ones, with
+    ragged and partial windows) returns the oracle's pair set and intervals."""
+    if name == "tiny":
+        w = synth.tiny()
+        d = w.d * 3.0
+        qsel = np.arange(w.Q.shape[0])
+    else:
+        w = synth.make_workload("random-dense-1m")
+        d = 0.09
+        qsel = np.arange(0, w.Q.shape[0], 97)[:64]
+    Q = w.Q[qsel]
+    ref = oracle.search(w.D, Q, d)
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    monkeypatch.setenv("TDS_DENSE4", "1")
+    got, st = _run(idx, Q, d, kind)
+    monkeypatch.delenv("TDS_DENSE4")
+    base, _ = _run(idx, Q, d, kind)
+    assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(base[0], base[1])))
+    check(got, ref, w.D, Q, d, label=f"{kind} dense4")
