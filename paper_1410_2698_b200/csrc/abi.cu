@@ -11,6 +11,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <string>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (CUDA toolkit): ranges for profilers
@@ -184,7 +185,26 @@ static uint64_t device_budget_bytes_now() {
     return (uint64_t)fr + extra;
 }
 
+// Fault injection (tests): TDS_INJECT_ENOMEM="k[:tag]" makes the next k large
+// allocations fail with TDS_ENOMEM; a new value (another tag) re-arms it.
+static bool inject_enomem() {
+    const char *e = getenv("TDS_INJECT_ENOMEM");
+    if (!e || !*e) return false;
+    static std::mutex mu;
+    static std::string armed;
+    static int left = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (armed != e) {
+        armed = e;
+        left = atoi(e);
+    }
+    if (left <= 0) return false;
+    --left;
+    return true;
+}
+
 void *dalloc_big(size_t bytes, cudaStream_t s) {
+    if (inject_enomem()) fail(TDS_ENOMEM, "injected allocation failure (TDS_INJECT_ENOMEM), %zu bytes", bytes);
     cudaMemPool_t pool = big_pool();
     if (!pool) return dalloc(bytes, s);
     void *p = nullptr;

@@ -487,3 +487,46 @@ def test_dense4_instantiation_matches_oracle(tds, name, kind, monkeypatch):
     base, _ = _run(idx, Q, d, kind)
     assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(base[0], base[1])))
     check(got, ref, w.D, Q, d, label=f"{kind} dense4")
+
+
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
+def test_enomem_fallback_injected(tds, kind, monkeypatch):
+    """Fault injection: the automatic result capacity survives failed
+    allocations of its pass buffer (TDS_INJECT_ENOMEM) by
+    halving the capacity and re-taking the memory budget (one or two injected
+    failures, as far as the floor allows); the result is the same pair set as
+    without failures.  A single failure with capacity at the floor
+    surfaces as TDS_ENOMEM."""
+    w = synth.random_1m(n_traj=300, query_frac_stride=10)
+    d = 20.0
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
+    base, st = _run(idx, w.Q, d, kind)
+    assert st["pair_tests"] > (1 << 20)              # above the halving floor
+    nfail = 2 if st["pair_tests"] > 4 * (1 << 20) else 1
+    monkeypatch.setenv("TDS_INJECT_ENOMEM", f"{nfail}:{kind}")
+    got, _ = _run(idx, w.Q, d, kind)
+    monkeypatch.delenv("TDS_INJECT_ENOMEM")
+    assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(base[0], base[1])))
+    ref = oracle.search(w.D, w.Q[:400], d)
+    sel = got[0] < 400
+    check(tuple(x[sel] for x in got), ref, w.D, w.Q[:400], d, label=f"{kind} enomem")
+    small = w.Q[:50]
+    monkeypatch.setenv("TDS_INJECT_ENOMEM", f"1:{kind}-floor")
+    with pytest.raises(tds.TdsError):
+        _run(idx, small, d, kind)
+    monkeypatch.delenv("TDS_INJECT_ENOMEM")
+
+
+def test_enomem_injected_spatial_surfaces(tds, monkeypatch):
+    """GPUSpatial with a small automatic capacity (below the halving floor): an
+    injected pass-buffer allocation failure surfaces as TDS_ENOMEM, and the next
+    search succeeds."""
+    w = synth.tiny()
+    idx = tds.Index(_cuda(w.D), kinds=tds.SPATIAL, m=w.m_bins, grid=w.grid)
+    monkeypatch.setenv("TDS_INJECT_ENOMEM", "1:spatial-floor")
+    with pytest.raises(tds.TdsError) as ei:
+        _run(idx, w.Q, w.d, "spatial")
+    assert ei.value.status == "TDS_ENOMEM"
+    got, _ = _run(idx, w.Q, w.d, "spatial")
+    monkeypatch.delenv("TDS_INJECT_ENOMEM")
+    check(got, oracle.search(w.D, w.Q, w.d), w.D, w.Q, w.d, label="spatial after injected ENOMEM")
