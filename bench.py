@@ -1,22 +1,31 @@
 """Benchmark of the B200 distance threshold search (driver contract in DESIGN.md "Measurement").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config random-1m] [--d 50]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config random-dense] [--d 0.03]
+                    [--variants spatiotemporal,temporal]
     python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
 
-One step = one pass of the whole hot path over the workload, device-resident
-inputs: tds_build_index (validate, t_start radix sort, bins, subbin arrays,
-FSG) + for each index variant (GPUTemporal, GPUSpatioTemporal, GPUSpatial)
-tds_search + tds_fetch_results into device buffers.  ``value`` counts query
-segments answered per second over all ranks (3 x |Q| per step per rank: each
-query is answered once per variant).  Multi-GPU: one process per GPU, every
-rank holds D and answers its own query trajectories (weak scaling; results
-stay sharded, no data-path collective); timing is max over ranks.
+The workload is the one BASELINE.json's metric and north-star target are
+quoted on: Random-dense-shaped, 65,536 x 192 = 12,582,912 segments, the S3
+query set of 50,880 segments (Table 1),
+GPUSpatioTemporal (m = 1,000, v = 2) at d = 0.03 kpc, with GPUTemporal
+beside it.  The index is built once, before the timed region: the paper's
+response time excludes the index build and the upload of D.
+
+One step = tds_search of the full query set with each listed variant (the
+first is the headline), inputs resident in HBM; the results stay
+device-resident (T_search, T_fetch and T_gather are reported
+separately).  ``value`` = #Q / T_search of the headline variant, query
+segments per second over all ranks.  N GPUs (one process each): every rank
+holds D and its index and the full query set and runs its work-balanced part
+of each search (tds_search_part: equal shares of the exact pair tests); the
+union of the parts is the answer, left sharded (strong scaling); T_search is
+the max over ranks.  T_gather (the records to rank 0 over NCCL) is measured
+after the timed region and reported separately.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -30,11 +39,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "query segments/s & segment-pair tests/s vs HBM roofline at 1/2/4/8 B200"
-VARIANTS = ("temporal", "spatiotemporal", "spatial")
-# algorithmic work of one pair test: the certified fp32 filter of DESIGN.md
-# ("Pair test numerics"): 43 FP32 instructions, 16 of them FFMA -> 59 flops
-FLOPS_PER_PAIR = 59
-BYTES_PER_SPATIAL_PAIR = 36          # GPUSpatial: 32-B record + 4-B id streamed per pair test
+DEFAULT_D = {"random-dense": 0.03, "random-dense-1m": 0.03, "merger": 1.0, "random-1m": 50.0,
+             "scale-out": 50.0, "tiny": 2.0}
+DEFAULT_VARIANTS = {"merger": "spatiotemporal,temporal,spatial", "random-1m": "temporal,spatiotemporal,spatial",
+                    "tiny": "spatiotemporal,temporal,spatial"}
+# SURVEY §8(d) algorithmic work: 42 FP32 operations per pair test, 25 more per
+# hit; bytes: 36 per entry of D touched (32-B record + 4-B id), 48 per query
+# (32-B record + 16-B schedule entry), 16 per result record, + 4 per entry
+# id read from X/Y/Z (GPUSpatioTemporal)
+OPS_PER_PAIR, OPS_PER_HIT = 42, 25
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -45,22 +58,14 @@ def load_peaks():
         return {}
 
 
-def ncu_traffic(args, kname, variant):
+def ncu_traffic(config, d, kname, variant):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed
-    ncu --set full capture of the same configuration (profiles/ncu_traffic.json,
-    written by tools/ncu_traffic.py), else None."""
+    ncu capture of the same configuration (profiles/ncu_traffic.json), else None."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        key = f"{args.config}|{args.d if args.d is not None else 'default'}|{kname}|{variant}"
-        return t[key]["dram_bytes"]
+        return t[f"{config}|{d:g}|{kname}|{variant}"]
     except Exception:
         return None
-
-
-def fp32_peak_tflops(peaks, n_sms=148):
-    # 128 FP32 lanes per SM, FFMA = 2 flops, at the maximum SM clock (DESIGN.md "Roofline")
-    mhz = peaks.get("sm_max_mhz", 1965.0)
-    return n_sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
 class ClockSampler:
@@ -122,7 +127,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup(args):
+def dist_setup():
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -140,33 +145,21 @@ def dist_setup(args):
     return ws, rank, local
 
 
-def max_over_ranks(dist, x, dev):
-    """Max of a host float over ranks (NCCL needs a CUDA tensor, gloo a CPU one)."""
+def reduce_over_ranks(dist, x, dev, op):
+    """Max / sum of a host float over ranks (NCCL needs a CUDA tensor, gloo a CPU one)."""
     import torch
+    if dist is None:
+        return x
     on_gpu = dist.get_backend() == "nccl"
     t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
 
-def sum_over_ranks(dist, x, dev):
-    import torch
-    on_gpu = dist.get_backend() == "nccl"
-    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
-
-
-def make_workload(args, rank):
+def make_workload(args):
     import synth
-    kw = {}
-    if args.config in ("random-1m", "random-dense", "random-dense-1m", "merger"):
-        kw["offset"] = rank                       # weak scaling: each rank its own query set
-    elif args.config == "scale-out":
-        kw["shard"] = (rank, int(os.environ.get("WORLD_SIZE", "1")))   # strong: one query set, sharded
-    w = synth.make_workload(args.config, **kw)
-    if args.d is not None:
-        w.d = args.d
+    w = synth.make_workload(args.config)
+    w.d = args.d
     if args.m is not None:
         w.m_bins = args.m
     if args.v is not None:
@@ -174,6 +167,18 @@ def make_workload(args, rank):
     if args.grid is not None:
         w.grid = (args.grid,) * 3
     return w
+
+
+def config_dict(args, w, ws):
+    return {"workload": f"{w.name}-shaped", "n_entries": int(w.D.shape[0]), "n_queries": int(w.Q.shape[0]),
+            "d": w.d, "m_bins": w.m_bins, "v_subbins": w.v_subbins, "grid": list(w.grid),
+            "variants": list(args.variants), "headline_variant": args.variants[0],
+            "parallelism": (f"query-sharded x{ws}: work-balanced parts of the sorted schedule "
+                            f"(tds_search_part), D + index replicated") if ws > 1 else "1 GPU",
+            "index": "built once before the timed region (excluded, P:1301-1304)",
+            "l2": "inputs (D 403 MB at Random-dense) exceed L2, and L2 is flushed (256 MiB write) before "
+                  "every timed search, outside its events",
+            "note": w.note}
 
 
 # ---------------------------------------------------------------------------
@@ -188,42 +193,39 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def oracle_rate(w, seconds, seed=0, max_q=None):
-    """Time the oracle as it stands on a bounded query sample of the workload."""
+def oracle_sample_size(w, seconds, cores, seed=0):
+    """Queries of the workload the oracle answers in about ``seconds``."""
     import oracle
     rng = np.random.default_rng(seed)
     nq = w.Q.shape[0]
-    cores = host_cores()
-    cal = np.sort(rng.choice(nq, min(8, nq), replace=False))
+    cal = np.sort(rng.choice(nq, min(max(cores, 8), nq), replace=False))
     t = time.perf_counter()
     oracle.search(w.D, w.Q, w.d, qsel=cal, nthreads=cores)
     dt = max(time.perf_counter() - t, 1e-6)
-    n = int(min(nq, max(8, seconds * len(cal) / dt)))
-    if max_q:
-        n = min(n, max_q)
-    sel = np.sort(rng.choice(nq, n, replace=False))
+    return int(min(nq, max(8, seconds * len(cal) / dt)))
+
+
+def oracle_time(w, n, cores, seed):
+    import oracle
+    rng = np.random.default_rng(seed)
+    sel = np.sort(rng.choice(w.Q.shape[0], n, replace=False))
     t = time.perf_counter()
-    r = oracle.search(w.D, w.Q, w.d, qsel=sel, nthreads=cores)
-    dt = time.perf_counter() - t
-    return n, dt, int(r["hit"].sum()), cores
+    oracle.search(w.D, w.Q, w.d, qsel=sel, nthreads=cores)
+    return time.perf_counter() - t
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    w = make_workload(args, 0)
-    # each step: a bounded query sample (~step_seconds of CPU work)
-    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     import oracle
     oracle.build()
-    n, dt, hits, cores = oracle_rate(w, per_step)
-    rng = np.random.default_rng(1)
+    w = make_workload(args)
+    cores = host_cores()
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    n = oracle_sample_size(w, per_step, cores)
     times = []
     for k in range(args.warmup + args.steps):
-        sel = np.sort(rng.choice(w.Q.shape[0], n, replace=False))
-        t = time.perf_counter()
-        oracle.search(w.D, w.Q, w.d, qsel=sel, nthreads=cores)
-        el = time.perf_counter() - t
+        el = oracle_time(w, n, cores, seed=1 + k)
         if k >= args.warmup:
             times.append(el)
     tot = sum(times)
@@ -231,8 +233,8 @@ def run_reference(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "query segments/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args, w, ws),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args, w, 1),
         "cpu_baseline": {"value": value, "unit": "query segments/s", "cores": cores, "kind": "oracle",
                          "sample": f"{n} random queries of {w.Q.shape[0]} per step, all-pairs fp64 against "
                                    f"all {w.D.shape[0]} entries"},
@@ -242,29 +244,54 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, w, ws):
-    return {"workload": f"{w.name}-shaped", "n_entries": int(w.D.shape[0]), "n_queries_per_rank": int(w.Q.shape[0]),
-            "d": w.d, "m_bins": w.m_bins, "v_subbins": w.v_subbins, "grid": list(w.grid),
-            "variants": list(args.variants), "parallelism": f"query-sharded x{ws}, index replicated",
-            "variant_streams": 1 if (args.serial and not args.batched) else len(args.variants),
-            "search_api": "tds_search_many" if args.batched else "tds_search",
-            "l2": "flushed between steps (256 MiB write); timed steps bracketed by barrier + synchronize",
-            "note": w.note}
-
-
 # ---------------------------------------------------------------------------
 # the B200 arm
 # ---------------------------------------------------------------------------
+def roofline(dk, nD, nQ, kind, peaks, n_sms, traffic):
+    """SURVEY §8(d) roofline of one pair-kernel launch: T_roof = max(B_alg / HBM,
+    ops / FP32) against the measured kernel time; bound = the larger term."""
+    secs = dk["pair_kernel_ms"] / 1e3
+    hits = dk["results"]
+    ops = OPS_PER_PAIR * dk["pair_tests"] + OPS_PER_HIT * hits
+    nbytes = 36 * nD + 48 * nQ + 16 * hits + (4 * nD if kind == "spatiotemporal" else 0)
+    if kind == "spatial":       # no record reuse across queries: record + id per pair test
+        nbytes = 36 * dk["pair_tests"] + 48 * nQ + 16 * hits
+    hbm = float(peaks.get("hbm_gbs", 6548.8))                      # GB/s, measured copy
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    alu = n_sms * 128 * mhz * 1e6                                  # FP32 lane-ops/s (B200_PROFILING unit counts)
+    t_hbm, t_alu = nbytes / (hbm * 1e9), ops / alu
+    out = {"kernel": ("k_pair_spatial" if kind == "spatial" else "k_pair_range") + f" ({kind})",
+           "alu": {"achieved": ops / secs / 1e12, "peak": alu / 1e12, "unit": "Tops/s (FP32 lane ops)",
+                   "frac": t_alu / secs, "ops": ops,
+                   "work": f"{OPS_PER_PAIR} x {dk['pair_tests']} pair tests + {OPS_PER_HIT} x {hits} hits"},
+           "hbm": {"achieved": nbytes / secs / 1e9, "peak": hbm, "unit": "GB/s", "frac": t_hbm / secs,
+                   "bytes": nbytes},
+           "kernel_ms": dk["pair_kernel_ms"]}
+    if t_hbm >= t_alu:
+        out.update(bound="hbm", achieved=out["hbm"]["achieved"], peak=hbm, unit="GB/s", frac=t_hbm / secs,
+                   peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)")
+    else:
+        out.update(bound="alu", achieved=out["alu"]["achieved"], peak=alu / 1e12, unit="Tops/s",
+                   frac=t_alu / secs,
+                   peak_source=f"{n_sms} SMs x 128 FP32 lanes x sm_max_mhz {mhz:g} (MEASURED_PEAKS.json)")
+    out["traffic"] = traffic["dram_bytes"] if traffic else None
+    if traffic:
+        out["traffic_source"] = traffic.get("source")
+    return out
+
+
 def run_tds(args, ws, rank, local):
     import torch
     import paper_1410_2698_b200 as tds
     tds.load_library()
     dev = torch.device("cuda", local)
-    w = make_workload(args, rank)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    w = make_workload(args)
     Dh = torch.from_numpy(w.D).pin_memory()
     Qh = torch.from_numpy(w.Q).pin_memory()
     D = Dh.to(dev)
     Q = Qh.to(dev)
+    nQ, nD = int(w.Q.shape[0]), int(w.D.shape[0])
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     dist = None
@@ -275,239 +302,167 @@ def run_tds(args, ws, rank, local):
         if dist is not None:
             dist.barrier()
 
-    # the three variants are independent searches of one index; --concurrent runs
-    # them one host thread + CUDA stream each (the C-ABI releases the GIL and
-    # supports concurrent searches on different streams).  Default: serial (faster
-    # on Random-1M: 1.86 vs 2.05 ms per step, thread/join overheads dominate)
-    side = [torch.cuda.Stream(dev) for _ in args.variants]
-    from concurrent.futures import ThreadPoolExecutor
-    pool = ThreadPoolExecutor(max_workers=len(args.variants))
+    kinds = 0
+    for v in args.variants:
+        kinds |= tds.KINDS[v]
+    e_b = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e_b[0].record(stream)
+    idx = tds.Index(D, kinds=kinds, m=w.m_bins, v=w.v_subbins, grid=w.grid, stream=stream.cuda_stream)
+    e_b[1].record(stream)
+    torch.cuda.synchronize(dev)
+    build_ms = e_b[0].elapsed_time(e_b[1])
 
-    def one_variant(j, kind, idx, host):
-        st_ = side[j] if not args.serial else stream
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        with torch.cuda.stream(st_):
-            e[0].record(st_)
-            r = idx.search(Qh if host else Q, w.d, kind=kind, capacity=args.capacity, stream=st_.cuda_stream)
-            e[1].record(st_)
-            r.fetch(device=not host, stream=st_.cuda_stream)
-            e[2].record(st_)
-            stt = r.stats()
-            n = r.count
+    def search(kind, host=False):
+        return idx.search(Qh if host else Q, w.d, kind=kind, capacity=args.capacity, stream=stream.cuda_stream,
+                          part=rank, nparts=ws)
+
+    def step(collect=None):
+        rec = {}
+        for kind in args.variants:
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = search(kind)
+            e1.record(stream)
+            st = r.stats()
             r.close()
-        return e, stt, 16 * n
-
-    def step(collect=None, host=False):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        ev[0].record(stream)
-        idx = tds.Index(Dh if host else D, kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid,
-                        stream=stream.cuda_stream)
-        ev[1].record(stream)                    # build_index synchronises: the index is ready
-        if args.batched:
-            # one tds_search_many call: the variants run concurrently on side streams
-            # (overlapping their host synchronisations), then each fetches on its stream
-            evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in args.variants]
-            for j in range(len(args.variants)):
-                side[j].wait_stream(stream)
-                evs[j][0].record(side[j])
-            rs = idx.search_many([{"queries": Qh if host else Q, "d": w.d, "kind": k, "capacity": args.capacity,
-                                   "stream": side[j].cuda_stream} for j, k in enumerate(args.variants)])
-            outs = []
-            for j, r in enumerate(rs):
-                with torch.cuda.stream(side[j]):
-                    evs[j][1].record(side[j])
-                    r.fetch(device=not host, stream=side[j].cuda_stream)
-                    evs[j][2].record(side[j])
-                    stt = r.stats()
-                    n = r.count
-                    r.close()
-                outs.append((evs[j], stt, 16 * n))
-            for sj in side:
-                stream.wait_stream(sj)
-        elif args.serial:
-            outs = [one_variant(j, k, idx, host) for j, k in enumerate(args.variants)]
-        else:
-            futs = [pool.submit(one_variant, j, k, idx, host) for j, k in enumerate(args.variants)]
-            outs = [f.result() for f in futs]
-            for sj in side:
-                stream.wait_stream(sj)
-        end = torch.cuda.Event(enable_timing=True)
-        end.record(stream)
-        idx.close()
-        per = {k: o[1] for k, o in zip(args.variants, outs)}
-        d2h = sum(o[2] for o in outs)
+            rec[kind] = (e0, e1, st)
         if collect is not None:
-            collect.append((ev + [end], per, d2h, [o[0] for o in outs]))
-        return per
+            collect.append(rec)
 
-    # warm-up.  The first warm-up step runs the variants one after another and
-    # measures them: tds_search_many overlaps the searches' host synchronisations
-    # and launch chains, which pays only when the searches are short (each under
-    # 1 ms of device time, e.g. Random-1M); long pair kernels just compete for the
-    # SMs (Random-dense d = 0.01: 26 vs 21 ms per step), and it holds every
-    # variant's result at once (Random-dense d = 0.09: 40 GB each), so those stay serial.
-    want_batched = args.batched
-    args.batched = False
-    step()                                   # cold (first-touch, pool growth): not measured
-    per0 = step()
-    out_bytes = 16 * sum(int(v["n_results"]) for v in per0.values())
-    short = all(float(v["ms_total"]) < 1.0 for v in per0.values())
-    args.batched = (want_batched and short
-                    and out_bytes < 0.1 * torch.cuda.get_device_properties(dev).total_memory)
-    for _ in range(args.warmup - 2):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
 
-    # timed region: K steps, L2 flushed before each (outside the events)
+    # ---- timed region: K steps, barrier + synchronize on both sides of each
     launches0 = tds.kernel_launches()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
     recs = []
-    step_ms = []
     sampler.mark(0)
     for _ in range(args.steps):
-        flush.zero_()
         barrier()
         torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         step(recs)
-        e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        step_ms.append(e0.elapsed_time(e1))
-        if os.environ.get("TDS_BENCH_STEPS") == "1":
-            free_b, _ = torch.cuda.mem_get_info(dev)
-            print(f"[bench] step {len(step_ms) - 1}: {step_ms[-1]:.3f} ms; torch reserved "
-                  f"{torch.cuda.memory_reserved(dev) / 1e9:.1f} GB, device free {free_b / 1e9:.1f} GB",
-                  file=sys.stderr, flush=True)
     sampler.mark(1)
     clocks = sampler.stop()
     launches = tds.kernel_launches() - launches0
-    total_ms = sum(step_ms)
-    if dist is not None:
-        total_ms = max_over_ranks(dist, total_ms, dev)
 
-    nq = w.Q.shape[0]
-    nvar = len(args.variants)
-    nq_all = nq if dist is None else int(round(sum_over_ranks(dist, float(nq), dev)))
-    value = nvar * nq_all * args.steps / (total_ms / 1e3)
-    # per-phase breakdown (medians over the timed steps)
-    build_ms = statistics.median(r[0][0].elapsed_time(r[0][1]) for r in recs)
     per_kind = {}
-    for j, kind in enumerate(args.variants):
-        pt = [r[1][kind]["pair_tests"] for r in recs]
-        pm = [r[1][kind]["ms_pairs"] for r in recs]
-        first = recs[0][1][kind]
+    for kind in args.variants:
+        ms = [r[kind][0].elapsed_time(r[kind][1]) for r in recs]
+        tot = reduce_over_ranks(dist, sum(ms), dev, "max")
+        st = recs[0][kind][2]
+        pt = [r[kind][2]["pair_tests"] for r in recs]
+        pk = statistics.median(r[kind][2]["ms_pairs"] for r in recs)
+        pt_all = reduce_over_ranks(dist, float(pt[0]), dev, "sum")
+        res_all = reduce_over_ranks(dist, float(st["n_results"]), dev, "sum")
         per_kind[kind] = {
-            "search_ms": statistics.median(r[3][j][0].elapsed_time(r[3][j][1]) for r in recs),
-            "fetch_ms": statistics.median(r[3][j][1].elapsed_time(r[3][j][2]) for r in recs),
-            "pair_kernel_ms": statistics.median(pm),
-            "pair_tests": int(pt[0]),
-            "pairs_executed": int(first["pairs_executed"]),
-            "refined_pairs": int(first["refined_pairs"]),
-            "results": int(first["n_results"]),
-            "passes": int(first["passes"]),
-            "fallback_queries": int(first["fallback_queries"]),
-            "pair_tests_per_s": pt[0] / (statistics.median(pm) / 1e3) if statistics.median(pm) > 0 else None,
+            "t_search_ms": tot / args.steps, "t_search_ms_rank0_median": statistics.median(ms),
+            "t_search_ms_rank0_min": min(ms), "t_search_ms_rank0_max": max(ms),
+            "query_segments_per_s": nQ * args.steps / (tot / 1e3),
+            "pair_tests_per_s": pt_all * args.steps / (tot / 1e3),
+            "pair_tests": int(pt_all), "results": int(res_all),
+            "pair_kernel_ms": pk, "pair_tests_rank0": int(pt[0]), "results_rank0": int(st["n_results"]),
+            "pairs_executed": int(st["pairs_executed"]), "refined_pairs_fp64": int(st["refined_pairs"]),
+            "passes": int(st["passes"]), "fallback_queries": int(st["fallback_queries"]),
+            "ms_schedule": statistics.median(r[kind][2]["ms_schedule"] for r in recs),
+            "pair_kernel_share_of_search": pk / statistics.median(ms),
         }
-    searches_ms = statistics.median(r[0][1].elapsed_time(r[0][2]) for r in recs)
-    pair_tests_step = sum(v["pair_tests"] for v in per_kind.values())
-    # the paper's response time excludes the index build: search + fetch only
-    search_ms = searches_ms
-    pt_all = pair_tests_step if dist is None else sum_over_ranks(dist, float(pair_tests_step), dev)
+    head = args.variants[0]
+    total_ms = per_kind[head]["t_search_ms"] * args.steps
+    value = nQ * args.steps / (total_ms / 1e3)
     peaks = load_peaks()
-    # roofline of the dominant kernel: the pair kernel with the largest share.
-    # GPUSpatial streams one record + id per pair test (FSG slices are per (query,
-    # cell)) and is bound by HBM (36 B per pair test).  The range
-    # kernels (GPUTemporal / GPUSpatioTemporal) reuse each loaded record for up to
-    # 32 queries: their roof is the larger of the FP32 time (59 flops per scheduled
-    # pair test) and the HBM time of their algorithmic bytes (SURVEY 8(d):
-    # 36 B per entry of D + 48 B per query + 16 B per result record written), i.e.
-    # FP32 on sparse outputs and HBM on output-bound searches (Random-dense d=0.09).
-    dom = max(per_kind, key=lambda k: per_kind[k]["pair_kernel_ms"])
-    dk = per_kind[dom]
-    kname = "k_pair_spatial" if dom == "spatial" else "k_pair_range"
-    secs = dk["pair_kernel_ms"] / 1e3
-    hbm_peak = float(peaks.get("hbm_gbs", 6537.0))
-    alu_peak = fp32_peak_tflops(peaks, torch.cuda.get_device_properties(dev).multi_processor_count)
-    if dom == "spatial":
-        achieved = BYTES_PER_SPATIAL_PAIR * dk["pair_tests"] / secs / 1e9
-        peak = hbm_peak
-        roof = {"bound": "hbm", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); algorithmic 36 B (record + id) per pair test"}
-    else:
-        flops = FLOPS_PER_PAIR * dk["pair_tests"]
-        nbytes = 36 * w.D.shape[0] + 48 * w.Q.shape[0] + 16 * dk["results"]
-        if nbytes / (hbm_peak * 1e9) > flops / (alu_peak * 1e12):
-            achieved = nbytes / secs / 1e9
-            peak = hbm_peak
-            roof = {"bound": "hbm", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
-                    "unit": "GB/s",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); algorithmic bytes 36 B x |D| + 48 B x |Q| "
-                                   "+ 16 B x results (output-bound: the HBM time exceeds the FP32 time)"}
-        else:
-            achieved = flops / secs / 1e12
-            peak = alu_peak
-            roof = {"bound": "alu", "kernel": f"{kname} ({dom})", "achieved": achieved, "peak": peak,
-                    "unit": "TFLOP/s",
-                    "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
-                                   "algorithmic 59 flops per scheduled pair test"}
-    roof["frac"] = achieved / peak
-    roof["traffic"] = ncu_traffic(args, kname, dom)
-    roof["share_of_step"] = dk["pair_kernel_ms"] / statistics.median(step_ms)
+    # dominant kernel: the headline search's pair kernel (rank 0's launch: its own part)
+    dk = dict(per_kind[head])
+    dk["pair_tests"], dk["results"] = dk["pair_tests_rank0"], dk["results_rank0"]
+    kname = "k_pair_spatial" if head == "spatial" else "k_pair_range"
+    roof = roofline(dk, nD, nQ / ws, head, peaks, n_sms,
+                    ncu_traffic(args.config, w.d, kname, head) if ws == 1 else None)
+    for kind in args.variants[1:]:
+        dk2 = dict(per_kind[kind])
+        dk2["pair_tests"], dk2["results"] = dk2["pair_tests_rank0"], dk2["results_rank0"]
+        r2 = roofline(dk2, nD, nQ / ws, kind, peaks, n_sms, None)
+        per_kind[kind]["roofline"] = {"bound": r2["bound"], "frac": r2["frac"], "alu_frac": r2["alu"]["frac"],
+                                      "hbm_frac": r2["hbm"]["frac"]}
 
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    # ---- fetch (A11) and gather, timed after the region (reported separately)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r = search(head)
+    e0.record(stream)
+    cols = r.fetch(device=True, stream=stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_fetch = e0.elapsed_time(e1)
+    t_gather = None
+    if dist is not None:
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        tds_dist = __import__("paper_1410_2698_b200.dist", fromlist=["gather_results"])
+        g = tds_dist.gather_results(*cols, dst=0)
+        torch.cuda.synchronize(dev)
+        t_gather = reduce_over_ranks(dist, 1e3 * (time.perf_counter() - t0), dev, "max")
+        del g
+    r.close()
+    del cols
+
+    # ---- e2e through the public API with host buffers: Q copied in from pinned
+    # memory inside tds_search, records fetched to pinned host memory, every step
     e2e = None
     if not args.no_e2e:
-        for _ in range(max(1, args.warmup // 2)):
-            step(host=True)
-        torch.cuda.synchronize(dev)
-        er = []
-        e2e_ms = []
-        for _ in range(args.steps):
+        n_out = per_kind[head]["results_rank0"]
+        hbuf = torch.empty((4, max(n_out, 1)), dtype=torch.int32).pin_memory()
+        outs = (hbuf[0].numpy(), hbuf[1].numpy(), hbuf[2].numpy().view(np.float32), hbuf[3].numpy().view(np.float32))
+        e2e_ms, d2h = [], []
+        for k in range(args.steps + 1):
             flush.zero_()
             barrier()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            step(er, host=True)
+            r = search(head, host=True)
+            n = r.count
+            o = outs if n <= hbuf.shape[1] else None
+            r.fetch(device=False, stream=stream.cuda_stream, out=None if o is None else tuple(x[:n] for x in o))
             torch.cuda.synchronize(dev)
-            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            el = 1e3 * (time.perf_counter() - t0)
+            r.close()
             barrier()
-        tot = sum(e2e_ms)
-        if dist is not None:
-            tot = max_over_ranks(dist, tot, dev)
-        e2e = {"value": nvar * nq_all * args.steps / (tot / 1e3), "unit": "query segments/s",
-               "h2d_bytes_per_step": int(w.D.nbytes + nvar * w.Q.nbytes),
-               "d2h_bytes_per_step": int(statistics.median(x[2] for x in er)),
-               "timing": "host wall clock around each step, synchronize on both sides, max over ranks"}
+            if k:                                   # the first is a warm-up
+                e2e_ms.append(el)
+                d2h.append(16 * n)
+        tot = reduce_over_ranks(dist, sum(e2e_ms), dev, "max")
+        e2e = {"value": nQ * len(e2e_ms) / (tot / 1e3), "unit": "query segments/s",
+               "h2d_bytes_per_step": int(w.Q.nbytes), "d2h_bytes_per_step": int(statistics.median(d2h)),
+               "variant": head,
+               "timing": "host wall clock around tds_search (host queries) + tds_fetch_results (host "
+                         "destination), synchronize on both sides, max over ranks; index resident"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n, dt, hits, cores = oracle_rate(w, args.cpu_seconds)
+        import oracle
+        oracle.build()
+        cores = host_cores()
+        n = oracle_sample_size(w, args.cpu_seconds, cores)
+        dt = oracle_time(w, n, cores, seed=7)
         cpu = {"value": n / dt, "unit": "query segments/s", "cores": cores, "kind": "oracle",
-               "sample": f"{n} random queries of {nq}, all-pairs fp64 vs all {w.D.shape[0]} entries, "
-                         f"one answer per query ({dt:.1f} s)"}
+               "sample": f"{n} random queries of {nQ}, all-pairs fp64 vs all {nD} entries ({dt:.1f} s)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "query segments/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.config == "scale-out" else "weak", "vs_baseline": None,
-            "dtype": "f32+f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": config_dict(args, w, ws),
-            "pair_tests_per_s": pt_all * args.steps / (total_ms / 1e3),
+            "pair_tests_per_s": per_kind[head]["pair_tests_per_s"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,
-            "breakdown": {"build_index_ms": build_ms, "variants": per_kind,
-                          "step_ms_median": statistics.median(step_ms),
-                          "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
-            "search_only": {"value": ws * nvar * nq / (search_ms / 1e3), "unit": "query segments/s",
-                            "ranks": "rank 0's time, scaled by the rank count",
-                            "note": "per-step median of the three variants' tds_search + tds_fetch_results "
-                                    "(index build excluded, as in the paper's response time, P:1301-1304); rank 0"},
+            "breakdown": {"build_index_ms_untimed": build_ms, "t_fetch_ms": t_fetch, "t_gather_ms": t_gather,
+                          "variants": per_kind},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -518,30 +473,26 @@ def run_tds(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tds", choices=["tds", "reference"])
-    ap.add_argument("--config", default="random-1m")
+    ap.add_argument("--config", default="random-dense")
     ap.add_argument("--d", type=float, default=None)
     ap.add_argument("--m", type=int, default=None)
     ap.add_argument("--v", type=int, default=None)
     ap.add_argument("--grid", type=int, default=None)
-    ap.add_argument("--variants", default="all")
+    ap.add_argument("--variants", default=None, help="comma list; the first is the headline")
     ap.add_argument("--capacity", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--concurrent", action="store_true",
-                    help="run the variants concurrently from Python threads (one stream each)")
-    ap.add_argument("--serial-search", action="store_true",
-                    help="one tds_search call per variant, one after another (default: one "
-                         "tds_search_many call running the variants concurrently on side streams)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    args.variants = VARIANTS if args.variants == "all" else tuple(args.variants.split(","))
-    args.serial = not args.concurrent
-    args.batched = not args.concurrent and not args.serial_search
-    ws, rank, local = dist_setup(args)
+    if args.d is None:
+        args.d = DEFAULT_D.get(args.config, 1.0)
+    v = args.variants or DEFAULT_VARIANTS.get(args.config, "spatiotemporal,temporal")
+    args.variants = ("spatiotemporal", "temporal", "spatial") if v == "all" else tuple(v.split(","))
+    ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, ws, rank)
         if ws > 1:

@@ -143,6 +143,60 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
                float t_start, float t_end, uint64_t capacity, void *stream,
                tds_result *out, uint64_t *n_results);
 
+/*
+ * tds_search_part — part `part` of a work-balanced split of one tds_search into
+ * `nparts` parts (multi-GPU query sharding; the paper's
+ * search is data-parallel over query segments, one thread per query, P:430,
+ * P:698-701).  Every part computes the same schedule from the full query set
+ * and evaluates a contiguous slice of it:
+ *   GPUTemporal / GPUSpatioTemporal: the slice of the schedule, sorted by
+ *     (selector, range start), whose exact pair-test prefix sum crosses
+ *     part/nparts and (part+1)/nparts of the total (sum of hi - lo);
+ *   GPUSpatial: the queries (input order) whose flattened (query, cell) slot
+ *     prefix crosses the same fractions.
+ * The parts' result sets are disjoint and their union is the tds_search
+ * result (query ids stay rows of the full query set).  tds_stats.pair_tests
+ * and n_queries count this part only.  Arguments as tds_search, plus
+ *   part, nparts : 0 <= part < nparts (nparts = 1 is tds_search)
+ * Errors: those of tds_search; TDS_EINVAL for part >= nparts.
+ */
+int tds_search_part(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d,
+                    float t_start, float t_end, uint64_t capacity, uint32_t part, uint32_t nparts,
+                    void *stream, tds_result *out, uint64_t *n_results);
+
+/*
+ * tds_plan — the candidate-range schedule of a search without evaluating it
+ * (query prep + candidate-range lookup: GPUTemporal P:680-698 "E_k", and the
+ * GPUSpatioTemporal dimension choice P:1033-1083).  For every
+ * query row k (HOST output arrays of nq elements):
+ *   sel[k] : -1 temporal range (GPUTemporal, or a GPUSpatioTemporal fallback),
+ *            0 / 1 / 2 a subbin range of X / Y / Z, 3 no candidates
+ *   [lo[k], hi[k]) : the range in the sorted entries (sel = -1) or in X/Y/Z
+ *            (sorted-entry positions; see tds_index_export what = 0, 3-5)
+ * kind must be TDS_TEMPORAL or TDS_SPATIOTEMPORAL.  For tests and work
+ * planning.  Errors: TDS_EINVAL, TDS_EDATA, TDS_ENOMEM, TDS_ECUDA.
+ * Synchronises stream.
+ */
+int tds_plan(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start,
+             float t_end, void *stream, int32_t *sel, uint32_t *lo, uint32_t *hi);
+
+/*
+ * tds_time_partition — the entries of D owned by part `part` of `nparts` under
+ * time-partitioned sharding (the paper's distributed scenario, P:215-217;
+ * SURVEY §8f-1, reading C27): the positions [part*n/nparts, (part+1)*n/nparts)
+ * of the stable (t_start, row) order — contiguous time ranges of equal entry
+ * count.  The order is a device radix sort of the t_start column (the sort of
+ * the index build), so only 4 B per entry need to be resident.
+ *   t_start : n floats (device or host memory), t_start of every row of D
+ *   rows    : DEVICE output, room for n/nparts + 1 row numbers; receives the
+ *             rows of D of this part in (t_start, row) order
+ *   n_rows  : receives their count
+ * Errors: TDS_EINVAL (NULL, n == 0, part >= nparts), TDS_EDATA (non-finite
+ * t_start), TDS_ENOMEM, TDS_ECUDA.  Synchronises stream.
+ */
+int tds_time_partition(const float *t_start, uint64_t n, uint32_t part, uint32_t nparts, void *stream,
+                       uint32_t *rows, uint64_t *n_rows);
+
 /* one request of tds_search_many: the arguments of tds_search */
 typedef struct tds_search_req {
     int kind;

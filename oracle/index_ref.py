@@ -12,6 +12,10 @@ Readings of silent / garbled points are SURVEY §8c C12-C15 and DESIGN.md
        ``[min(c_start, c_end), max(c_start, c_end)]`` touches; the query MBB is
        inflated by the full d before the slab lookup.
 * C14  FSG cells likewise; the query MBB is inflated by d.
+* C20  where floating point decides an integer (a bin, slab or cell number),
+       it is decided as the kernel decides it: fp32 round-to-nearest for the
+       cell arithmetic, directed rounding for the d-inflated query box (the
+       task's rule for integer decisions taken in floating point).
 """
 from __future__ import annotations
 
@@ -62,6 +66,30 @@ def temporal_bins(D_sorted: np.ndarray, m: int):
             "bin_of": j_of, "b": b, "t_min": t_min, "t_max": t_max}
 
 
+def member_extent_bins(D_sorted: np.ndarray, bin_of: np.ndarray, m: int, t0q: float, t1q: float):
+    """Bins a query (t0q, t1q) looks up under reading C13: the lookup uses the
+    members' own extents, not the literal B^start / B^end (Fig. 3's B_0 ends at
+    7.5 after B_1's 6.2, so B^end is not monotone).  Lower end: the
+    first bin holding a member with t_end > t0q; upper end: the last bin holding
+    a member with t_start < t1q (strict: segments that only touch do not
+    interact, C5).  Returns (j_lo, j_hi) inclusive, or None when j_lo > j_hi.
+    The candidate range is the hull of these bins."""
+    t0 = D_sorted[:, 3].astype(np.float64)
+    t1 = D_sorted[:, 7].astype(np.float64)
+    j_lo = j_hi = None
+    for j in range(m):
+        members = np.nonzero(bin_of == j)[0]
+        if members.size == 0:
+            continue
+        if j_lo is None and t1[members].max() > t0q:
+            j_lo = j
+        if t0[members].min() < t1q:
+            j_hi = j
+    if j_lo is None or j_hi is None or j_lo > j_hi:
+        return None
+    return j_lo, j_hi
+
+
 def temporal_schedule(bins: dict, t0q: float, t1q: float):
     """E_k for one query: the bins whose extent [B^start, B^end]
     overlaps [t0q, t1q]; E_k = [min B^first, max B^last] over the non-empty ones.
@@ -91,6 +119,39 @@ def spatial_extent(D: np.ndarray):
     return lo, hi, mx
 
 
+def f32_sub_rd(a: float, b: float) -> np.float32:
+    """a - b rounded toward -inf to float32 (a, b float32 values)."""
+    x = float(np.float64(a) - np.float64(b))
+    r = np.float32(x)
+    return np.nextafter(r, np.float32(-np.inf)) if float(r) > x else r
+
+
+def f32_add_ru(a: float, b: float) -> np.float32:
+    """a + b rounded toward +inf to float32."""
+    x = float(np.float64(a) + np.float64(b))
+    r = np.float32(x)
+    return np.nextafter(r, np.float32(np.inf)) if float(r) < x else r
+
+
+def d_up32(d: float) -> np.float32:
+    """The threshold as the fp32 stages use it: d rounded up to float32 (C25)."""
+    r = np.float32(d)
+    return np.nextafter(r, np.float32(np.inf)) if float(r) < d else r
+
+
+def grid_geometry(D: np.ndarray, cells):
+    """Origin and cell width per dimension of a grid of ``cells[c]`` equal cells
+    over D's spatial extent (C14, C15): o = c_min, w = (c_max - c_min) / cells,
+    in fp32 as the kernel computes them (w = 1 for a zero extent)."""
+    lo, hi, _ = spatial_extent(D)
+    o = np.array([np.float32(x) for x in lo], np.float32)
+    w = np.empty(3, np.float32)
+    for c in range(3):
+        ext = np.float32(np.float32(hi[c]) - np.float32(lo[c]))
+        w[c] = np.float32(ext / np.float32(cells[c])) if ext > 0 else np.float32(1.0)
+    return o, w
+
+
 def admissible_v(D: np.ndarray) -> np.ndarray:
     """Largest v per dimension with v <= (c_max - c_min) / max |c_start - c_end|."""
     lo, hi, mx = spatial_extent(D)
@@ -100,8 +161,23 @@ def admissible_v(D: np.ndarray) -> np.ndarray:
 
 
 def slab_of(c: float, o: float, w: float, v: int) -> int:
-    """Slab j of coordinate c: [o + j w, o + (j+1) w), last slab closed (C15)."""
-    return int(min(max(math.floor((c - o) / w), 0), v - 1))
+    """Slab j of coordinate c: [o + j w, o + (j+1) w), last slab closed (C15);
+    j = floor((c - o) / w) decided in fp32 (C20)."""
+    q = np.float32(np.float32(np.float32(c) - np.float32(o)) / np.float32(w))
+    return int(min(max(math.floor(q), 0), v - 1))
+
+
+def query_slabs(q: np.ndarray, d: float, o, w, v: int):
+    """Slabs [slab_lo[c], slab_hi[c]] of a query's MBB inflated by the full d in
+    every dimension (C15; the expansion is silent in P:1036-1050), the box's
+    ends rounded outward (C20)."""
+    dd = d_up32(d)
+    lo, hi = [], []
+    for c in range(3):
+        a, b = np.float32(min(q[c], q[4 + c])), np.float32(max(q[c], q[4 + c]))
+        lo.append(slab_of(f32_sub_rd(a, dd), o[c], w[c], v))
+        hi.append(slab_of(f32_add_ru(b, dd), o[c], w[c], v))
+    return lo, hi
 
 
 def st_arrays(D_sorted: np.ndarray, bin_of: np.ndarray, m: int, v: int, origin, width):
@@ -132,6 +208,44 @@ def st_arrays(D_sorted: np.ndarray, bin_of: np.ndarray, m: int, v: int, origin, 
         arrays.append(np.array(arr, dtype=np.int64))
         ranges.append(rng)
     return arrays, ranges
+
+
+def plan(D: np.ndarray, Q: np.ndarray, d: float, m: int, v: int, kind: str = "spatiotemporal",
+         window=(-np.inf, np.inf)):
+    """The schedule entry of every query in the layout
+    of tds_plan: (sel, lo, hi) with sel = -1 for the temporal range [lo, hi) of
+    sorted entries (GPUTemporal, or the GPUSpatioTemporal fallback), 0/1/2 for
+    the range [lo, hi) of X/Y/Z, 3 for no candidates (lo = hi = 0).  Queries
+    are clipped to the window and need t0 < t1 after clipping (C5, C8)."""
+    Ds, _ = temporal_sort(D)
+    b = temporal_bins(Ds, m)
+    bin_of = b["bin_of"]
+    off = np.searchsorted(bin_of, np.arange(m + 1), side="left")        # bin j = sorted ids [off[j], off[j+1])
+    if kind == "spatiotemporal":
+        o, w = grid_geometry(D, (v, v, v))
+        _, ranges = st_arrays(Ds, bin_of, m, v, o, w)
+    out = []
+    for k in range(Q.shape[0]):
+        t0c = max(float(Q[k, 3]), float(np.float32(window[0])))      # the window is float32 (tds.h)
+        t1c = min(float(Q[k, 7]), float(np.float32(window[1])))
+        if not t0c < t1c:
+            out.append((3, 0, 0))
+            continue
+        jj = member_extent_bins(Ds, bin_of, m, t0c, t1c)
+        if jj is None:
+            out.append((3, 0, 0))
+            continue
+        entry = (-1, int(off[jj[0]]), int(off[jj[1] + 1]))
+        if entry[1] >= entry[2]:
+            out.append((3, 0, 0))
+            continue
+        if kind == "spatiotemporal":
+            sl, sh = query_slabs(Q[k], d, o, w, v)
+            sel, first, last = st_select(ranges, jj[0], jj[1], sl, sh)
+            if sel >= 0:
+                entry = (sel, first, last + 1) if last >= first else (3, 0, 0)
+        out.append(entry)
+    return np.array(out, np.int64).reshape(-1, 3)
 
 
 def st_select(ranges, bins_lo: int, bins_hi: int, slab_lo, slab_hi):
@@ -174,10 +288,8 @@ def linearize(cx: int, cy: int, cz: int, grid) -> int:
 
 
 def cell_range(lo: float, hi: float, o: float, w: float, g: int):
-    """Cells [floor((lo-o)/w), floor((hi-o)/w)] clamped to [0, g-1]."""
-    a = int(min(max(math.floor((lo - o) / w), 0), g - 1))
-    b = int(min(max(math.floor((hi - o) / w), 0), g - 1))
-    return a, b
+    """Cells [floor((lo-o)/w), floor((hi-o)/w)] clamped to [0, g-1] (decided in fp32, C20)."""
+    return slab_of(lo, o, w, g), slab_of(hi, o, w, g)
 
 
 def rasterize(mbb_min, mbb_max, origin, width, grid):

@@ -34,7 +34,8 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 # every symbol include/tds.h declares
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
-               "tds_version", "tds_kernel_launches", "tds_merge_trajectories", "tds_search_many"]
+               "tds_version", "tds_kernel_launches", "tds_merge_trajectories", "tds_search_many",
+               "tds_search_part", "tds_plan", "tds_time_partition"]
 
 
 class TdsError(RuntimeError):
@@ -79,6 +80,10 @@ def load_library(path: str = LIB_PATH):
     lib.tds_build_index.argtypes = [vp, u64, ctypes.POINTER(_Params), vp, ctypes.POINTER(vp)]
     lib.tds_search.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, vp, ctypes.POINTER(vp),
                                ctypes.POINTER(u64)]
+    lib.tds_search_part.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, ctypes.c_uint32,
+                                    ctypes.c_uint32, vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
+    lib.tds_time_partition.argtypes = [vp, u64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, ctypes.POINTER(u64)]
+    lib.tds_plan.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, vp, vp, vp, vp]
     lib.tds_fetch_results.argtypes = [vp, u64, u64, vp, vp, vp, vp, i32, i32, vp]
     lib.tds_merge_trajectories.argtypes = [vp, vp, u64, vp, u64, f32, vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
     lib.tds_result_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
@@ -97,7 +102,8 @@ def load_library(path: str = LIB_PATH):
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_uint32)]
     for name in ("tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats",
-                 "tds_index_export", "tds_index_info", "tds_merge_trajectories", "tds_search_many"):
+                 "tds_index_export", "tds_index_info", "tds_merge_trajectories", "tds_search_many",
+                 "tds_search_part", "tds_plan", "tds_time_partition"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -171,16 +177,37 @@ class Index:
         self.m, self.v, self.grid, self.kinds = int(m), int(v), tuple(grid), int(kinds)
 
     def search(self, queries, d: float, window=(-math.inf, math.inf), kind="temporal", capacity: int = 0,
-               stream=None) -> "Result":
+               stream=None, part: int = 0, nparts: int = 1) -> "Result":
+        """tds_search, or with nparts > 1 part ``part`` of a work-balanced split
+        (tds_search_part: disjoint parts whose union is the full result)."""
         lib = load_library()
         k = KINDS[kind] if isinstance(kind, str) else int(kind)
         ptr, nq, keep = _segments(queries)
         h = ctypes.c_void_p()
         n = ctypes.c_uint64()
-        _check(lib.tds_search(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), int(capacity),
-                              _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
+        if nparts > 1:
+            _check(lib.tds_search_part(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]),
+                                       int(capacity), int(part), int(nparts), _stream_ptr(stream), ctypes.byref(h),
+                                       ctypes.byref(n)))
+        else:
+            _check(lib.tds_search(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), int(capacity),
+                                  _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
         del keep
         return Result(h, n.value)
+
+    def plan(self, queries, d: float, window=(-math.inf, math.inf), kind="spatiotemporal", stream=None):
+        """tds_plan: per query row (sel, lo, hi) of the schedule (numpy arrays)."""
+        lib = load_library()
+        k = KINDS[kind] if isinstance(kind, str) else int(kind)
+        ptr, nq, keep = _segments(queries)
+        sel = np.empty(nq, np.int32)
+        lo = np.empty(nq, np.uint32)
+        hi = np.empty(nq, np.uint32)
+        _check(lib.tds_plan(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), _stream_ptr(stream),
+                            sel.ctypes.data_as(ctypes.c_void_p), lo.ctypes.data_as(ctypes.c_void_p),
+                            hi.ctypes.data_as(ctypes.c_void_p)))
+        del keep
+        return sel, lo, hi
 
     def search_many(self, requests) -> list:
         """Independent searches of this index in one call (tds_search_many):
@@ -288,6 +315,25 @@ class Result:
             self.close()
         except Exception:
             pass
+
+
+def time_partition(t_start, part: int, nparts: int, stream=None):
+    """tds_time_partition: rows of D owned by ``part`` of ``nparts`` (contiguous
+    t_start ranges of equal count, from the device sort of the t_start column);
+    returns a CUDA int32 tensor in (t_start, row) order.  ``t_start`` is a 1-D
+    float32 tensor (CUDA or CPU) or numpy array."""
+    import torch
+    lib = load_library()
+    if isinstance(t_start, torch.Tensor):
+        t = t_start.to(torch.float32).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(t_start, dtype=np.float32)))
+    n = t.numel()
+    rows = torch.empty(n // max(int(nparts), 1) + 1, dtype=torch.int32, device="cuda")
+    cnt = ctypes.c_uint64()
+    _check(lib.tds_time_partition(ctypes.c_void_p(t.data_ptr()), n, int(part), int(nparts), _stream_ptr(stream),
+                                  ctypes.c_void_p(rows.data_ptr()), ctypes.byref(cnt)))
+    return rows[:cnt.value]
 
 
 def kernel_launches() -> int:

@@ -382,13 +382,13 @@ int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *
     ABI_CATCH
 }
 
-int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
-               uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results) {
-    NvtxRange nvtx_range("tds_search");
-    ABI_TRY
-    tds::set_error(0, "");
-    if (!idx || !out) fail(TDS_EINVAL, "NULL argument");
-    *out = nullptr;
+}  // extern "C"
+
+namespace {
+
+// argument checks shared by tds_search / tds_search_part / tds_plan
+void check_search_args(tds_index idx, int kind, double d, float t_start, float t_end) {
+    if (!idx) fail(TDS_EINVAL, "NULL argument");
     if (kind != TDS_TEMPORAL && kind != TDS_SPATIAL && kind != TDS_SPATIOTEMPORAL && kind != TDS_AUTO)
         fail(TDS_EINVAL, "kind = %d is not one of TDS_TEMPORAL/SPATIAL/SPATIOTEMPORAL/AUTO", kind);
     if (kind != TDS_AUTO && !(idx->kinds & (uint32_t)kind))
@@ -396,6 +396,13 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
     if (!(d > 0.0) || !isfinite(d) || d > 3.0e38) fail(TDS_EINVAL, "d = %g must be finite and > 0", d);
     if (isnan(t_start) || isnan(t_end) || t_start > t_end) fail(TDS_EINVAL, "bad window [%g, %g]",
                                                                (double)t_start, (double)t_end);
+}
+
+void run_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
+                uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results, const tds::SearchOpts &opt) {
+    if (!out) fail(TDS_EINVAL, "NULL argument");
+    *out = nullptr;
+    check_search_args(idx, kind, d, t_start, t_end);
     cudaStream_t s = (cudaStream_t)stream;
     tds_result_s *r = new tds_result_s();
     cudaGetDevice(&r->device);
@@ -403,7 +410,7 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
         if (nq > 0) {
             Staged in;
             stage(queries, nq, s, in);
-            tds::search(idx, kind, in.p, nq, d, t_start, t_end, capacity, s, r);
+            tds::search(idx, kind, in.p, nq, d, t_start, t_end, capacity, s, r, opt);
         }
     } catch (...) {
         free_result(r);
@@ -412,6 +419,72 @@ int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, dou
     }
     *out = r;
     if (n_results) *n_results = r->n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tds_search(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
+               uint64_t capacity, void *stream, tds_result *out, uint64_t *n_results) {
+    NvtxRange nvtx_range("tds_search");
+    ABI_TRY
+    tds::set_error(0, "");
+    run_search(idx, kind, queries, nq, d, t_start, t_end, capacity, stream, out, n_results, tds::SearchOpts());
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_search_part(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start,
+                    float t_end, uint64_t capacity, uint32_t part, uint32_t nparts, void *stream, tds_result *out,
+                    uint64_t *n_results) {
+    NvtxRange nvtx_range("tds_search_part");
+    ABI_TRY
+    tds::set_error(0, "");
+    if (nparts < 1 || part >= nparts) fail(TDS_EINVAL, "part %u of %u", part, nparts);
+    tds::SearchOpts opt;
+    opt.part = part;
+    opt.nparts = nparts;
+    run_search(idx, kind, queries, nq, d, t_start, t_end, capacity, stream, out, n_results, opt);
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_time_partition(const float *t_start, uint64_t n, uint32_t part, uint32_t nparts, void *stream,
+                       uint32_t *rows, uint64_t *n_rows) {
+    NvtxRange nvtx_range("tds_time_partition");
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!t_start || !rows || !n_rows) fail(TDS_EINVAL, "NULL argument");
+    if (n == 0 || n >= (1ull << 32) - 1) fail(TDS_EINVAL, "n = %llu", (unsigned long long)n);
+    if (nparts < 1 || part >= nparts) fail(TDS_EINVAL, "part %u of %u", part, nparts);
+    cudaStream_t s = (cudaStream_t)stream;
+    StagedU32 in;
+    stage_u32(reinterpret_cast<const uint32_t *>(t_start), n, s, in);
+    *n_rows = tds::time_partition(reinterpret_cast<const float *>(in.p), n, part, nparts, rows, s);
+    return TDS_OK;
+    ABI_CATCH
+}
+
+int tds_plan(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
+             void *stream, int32_t *sel, uint32_t *lo, uint32_t *hi) {
+    NvtxRange nvtx_range("tds_plan");
+    ABI_TRY
+    tds::set_error(0, "");
+    check_search_args(idx, kind, d, t_start, t_end);
+    if (kind == TDS_SPATIAL || kind == TDS_AUTO) fail(TDS_EINVAL, "tds_plan: kind must be TDS_TEMPORAL or TDS_SPATIOTEMPORAL");
+    if (nq > 0 && (!sel || !lo || !hi)) fail(TDS_EINVAL, "NULL argument");
+    if (nq == 0) return TDS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    tds_result_s r;
+    cudaGetDevice(&r.device);
+    tds::SearchOpts opt;
+    opt.plan_sel = sel;
+    opt.plan_lo = lo;
+    opt.plan_hi = hi;
+    Staged in;
+    stage(queries, nq, s, in);
+    tds::search(idx, kind, in.p, nq, d, t_start, t_end, 0, s, &r, opt);
     return TDS_OK;
     ABI_CATCH
 }

@@ -77,7 +77,9 @@ struct DevStats {
     unsigned int ch;                 // candidates per work item
     unsigned int cat_cnt[5];         // schedule entries per category
     unsigned int probe_pass, probe_total;   // density probe (k_density_probe)
-    unsigned int pad[3];
+    unsigned int part_lo, part_hi;   // tds_search_part: schedule entries / query rows of this part
+    unsigned long long part_slot_lo, part_slot_hi;   // GPUSpatial part: flattened slot range
+    unsigned int pad[1];
 };
 
 struct Sched {                       // 16 B schedule entry
@@ -338,11 +340,14 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     const float dsu = (14.f * U) * Mu * rsA + (6.f * U) * V1 * Mu * rA + fabsf(su) * relA;
     const float drem = (28.f * U) * d * Mu + A * dsu * dsu + (2.f * U) * (d2 + rem);
     const float dw = w * (0.5f * drem * rcp_approx(rem) + 0.5f * relA + 4.f * U);
-    const float dst = 2.f * (dsu + dw);                         // x2 safety
+    // x2 safety on the first-order terms, + the rounding of s_u -+ w
+    const float dst = fmaf(U, fabsf(su) + w, 2.f * (dsu + dw));
     const float lo = su - w, hi = su + w;
     tin = a + fminf(fmaxf(lo, 0.f), L);
     tout = a + fminf(fmaxf(hi, 0.f), L);
-    const float tol = 1e-6f * fmaxf(L, fminf(fabsf(a), fabsf(b))) - (4.f * U) * fmaxf(fabsf(a), fabsf(b)) - 2.f * U * L;
+    // accepted offsets are within 8e-6 (b - a) of the exact ones; the output adds
+    // its fp32 rounding (<= 0.5 ulp(t)): |t - t_exact| <= 1e-5 (b - a) + ulp(t)
+    const float tol = (8e-6f) * L;
     const bool in_ok = (lo + dst < 0.f) || (dst <= tol);
     const bool out_ok = (hi - dst > L) || (dst <= tol);
     return (in_ok && out_ok) ? 2 : 1;
@@ -418,7 +423,7 @@ __device__ __forceinline__ void hit_kind2(float4 q0, float4 q1, float t0c, float
     upk2(rem, rm0, rm1);
     const f32x2 rr = pk2(rcp_approx(rm0), rcp_approx(rm1));
     const f32x2 dw = mul2(w, add2(fma2(mul2(bc2(0.5f), drem), rr, mul2(bc2(0.5f), relA)), bc2(4.f * U)));
-    const f32x2 dst = mul2(bc2(2.f), add2(dsu, dw));
+    const f32x2 dst = fma2(bc2(U), add2(asu, w), mul2(bc2(2.f), add2(dsu, dw)));   // as hit_kind
     float w0, w1, ds0, ds1;
     upk2(w, w0, w1);
     upk2(dst, ds0, ds1);
@@ -427,10 +432,7 @@ __device__ __forceinline__ void hit_kind2(float4 q0, float4 q1, float t0c, float
     tout0 = a0 + fminf(fmaxf(hi0, 0.f), L0);
     tin1 = a1 + fminf(fmaxf(lo1, 0.f), L1);
     tout1 = a1 + fminf(fmaxf(hi1, 0.f), L1);
-    const float tol0 = 1e-6f * fmaxf(L0, fminf(fabsf(a0), fabsf(b0))) - (4.f * U) * fmaxf(fabsf(a0), fabsf(b0)) -
-                       2.f * U * L0;
-    const float tol1 = 1e-6f * fmaxf(L1, fminf(fabsf(a1), fabsf(b1))) - (4.f * U) * fmaxf(fabsf(a1), fabsf(b1)) -
-                       2.f * U * L1;
+    const float tol0 = (8e-6f) * L0, tol1 = (8e-6f) * L1;
     const bool ok0 = ((lo0 + ds0 < 0.f) | (ds0 <= tol0)) & ((hi0 - ds0 > L0) | (ds0 <= tol0));
     const bool ok1 = ((lo1 + ds1 < 0.f) | (ds1 <= tol1)) & ((hi1 - ds1 > L1) | (ds1 <= tol1));
     k0 = pass0 ? ((cert0 & ok0) ? 2 : 1) : 0;
@@ -913,8 +915,10 @@ __global__ void k_permute_sched(const Sched *__restrict__ in, const uint32_t *__
 // tiles: runs of <= 32 consecutive schedule entries within one category
 __global__ void k_make_tiles(const Sched *__restrict__ S, uint32_t n_base, uint32_t n_total_entries,
                              DevStats *__restrict__ st_w, uint32_t range_lo, uint32_t range_hi,
-                             Tile *__restrict__ tiles, uint32_t max_tiles, uint32_t *__restrict__ nchunk_len) {
+                             Tile *__restrict__ tiles, uint32_t max_tiles, uint32_t *__restrict__ nchunk_len,
+                             int part_range) {
     const DevStats *st = st_w;
+    if (part_range) { range_lo = st->part_lo; range_hi = st->part_hi; }   // tds_search_part
     // one warp per tile slot; the tile layout is derived from the category counts
     uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
@@ -1473,6 +1477,7 @@ struct SpatialArgs {
     const uint32_t *row_q, *row_alo, *row_cxy;   // work items (query, cell): query, slice start, packed cell
     const unsigned long long *slot_start;   // [nrows + 1]
     const uint32_t *slot_row;        // [slots] row of each slot (small searches), else nullptr
+    unsigned long long slot_lo, slot_hi;   // the slots this launch evaluates (tds_search_part: a sub-range)
     uint32_t nrows;
     FsgGrid G;
 };
@@ -1494,19 +1499,20 @@ __device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint3
     return lo;
 }
 
-__global__ void k_slot_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, uint64_t nslots,
-                            uint32_t *__restrict__ slot_row) {
+// slot_row[k] = row of slot base + k
+__global__ void k_slot_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, unsigned long long base,
+                            uint64_t nslots, uint32_t *__restrict__ slot_row) {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < nslots) slot_row[k] = find_row(ss, 0, nrows, k);
+    if (k < nslots) slot_row[k] = find_row(ss, 0, nrows, base + k);
 }
 
-__global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, uint64_t ngrab,
-                            uint32_t *__restrict__ grab_row) {
+// grab_row[k] = row of slot base + k * SP_GRAB (clamped to the last slot < end)
+__global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, unsigned long long base,
+                            unsigned long long end, uint64_t ngrab, uint32_t *__restrict__ grab_row) {
     uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k > ngrab) return;
-    const unsigned long long total = ss[nrows];
-    unsigned long long s = k * SP_GRAB;
-    if (s >= total) s = total ? total - 1 : 0;
+    unsigned long long s = base + k * SP_GRAB;
+    if (s >= end) s = end > base ? end - 1 : base;
     grab_row[k] = find_row(ss, 0, nrows, s);
 }
 
@@ -1518,7 +1524,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
     const int lane = threadIdx.x & 31;
     WarpState &W = sm[threadIdx.x >> 5];
     DevStats *st = A.pc.o.st;
-    const unsigned long long total = A.slot_start[A.nrows];
+    const unsigned long long total = A.slot_hi;
     warp_state_init(W, lane);
     uint32_t qn = 0;
     unsigned long long exec = 0, direct_hits = 0;
@@ -1531,13 +1537,14 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
         unsigned gi = 0;
         if (lane == 0) gi = atomicAdd(&st->work_ctr, 1u);
         gi = __shfl_sync(FULL, gi, 0);
-        const unsigned long long B = (unsigned long long)gi * SP_GRAB;
+        const unsigned long long B = A.slot_lo + (unsigned long long)gi * SP_GRAB;
         if (B >= total) break;
         const unsigned long long Bend = min(B + SP_GRAB, total);
         const uint32_t rlo = A.grab_row[gi], rhi = A.grab_row[gi + 1] + 1;
         // row of this lane's first slot (small search inside the grab's row range);
         // later slots advance the row linearly (rows are consecutive in slot order)
-        uint32_t r = A.slot_row ? A.slot_row[min(B + lane, Bend - 1)] : find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
+        uint32_t r = A.slot_row ? A.slot_row[min(B + lane, Bend - 1) - A.slot_lo]
+                                : find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
         unsigned long long r_start = A.slot_start[r], r_next = A.slot_start[r + 1];
         uint32_t r_alo = A.row_alo[r], r_cxy = A.row_cxy[r], r_p = A.row_q[r];
         exec += Bend - B;
@@ -1551,7 +1558,7 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
                 vv[u] = s < Bend;
                 if (vv[u] && s >= r_next) {
                     // next item holding slot s (binary search: many (query, cell) items are empty)
-                    r = A.slot_row ? A.slot_row[s] : find_row(A.slot_start, r + 1, rhi, s);
+                    r = A.slot_row ? A.slot_row[s - A.slot_lo] : find_row(A.slot_start, r + 1, rhi, s);
                     r_start = A.slot_start[r];
                     r_next = A.slot_start[r + 1];
                     r_alo = A.row_alo[r];
@@ -1743,6 +1750,62 @@ __global__ void k_rec_field(const Rec *__restrict__ rs, uint64_t n, int which, c
     vals[i] = src;
 }
 
+// ---------------------------------------------------------------------------
+// work-balanced parts of one search (tds_search_part): part k of K
+// takes the contiguous slice of the sorted schedule whose exact pair-test prefix
+// sum crosses k/K and (k+1)/K of the total (prefix sum + binary search)
+// ---------------------------------------------------------------------------
+__global__ void k_sched_work(const Sched *__restrict__ S, uint32_t n, uint64_t *__restrict__ w) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) w[p] = S[p].sel == 3 ? 0ull : (uint64_t)(S[p].hi - S[p].lo);
+    if (p == n) w[p] = 0ull;
+}
+
+// first index p in [0, n] with pre(p) >= target, pre non-decreasing
+template <class F>
+__device__ __forceinline__ uint32_t part_lower_bound(F pre, uint32_t n, unsigned long long target) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pre(mid) >= target) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ unsigned long long part_target(unsigned long long total, uint32_t k, uint32_t K) {
+    return (unsigned long long)(((unsigned __int128)total * k) / K);
+}
+
+// range variants: pre = exclusive prefix of the sorted schedule's range lengths
+__global__ void k_part_bounds(const uint64_t *__restrict__ pre, uint32_t n, uint32_t part, uint32_t nparts,
+                              DevStats *st) {
+    if (threadIdx.x || blockIdx.x) return;
+    const unsigned long long total = pre[n];
+    auto f = [&](uint32_t p) { return pre[p]; };
+    const uint32_t lo = part == 0 ? 0u : part_lower_bound(f, n, part_target(total, part, nparts));
+    uint32_t hi = part + 1 >= nparts ? n : part_lower_bound(f, n, part_target(total, part + 1, nparts));
+    if (hi < lo) hi = lo;
+    st->part_lo = lo;
+    st->part_hi = hi;
+    st->pair_tests = pre[hi] - pre[lo];
+}
+
+// GPUSpatial: parts at query granularity; query p's slots start at ss[row_start[p]]
+__global__ void k_part_bounds_spatial(const unsigned long long *__restrict__ ss, const uint32_t *__restrict__ row_start,
+                                      uint32_t n, uint32_t part, uint32_t nparts, DevStats *st) {
+    if (threadIdx.x || blockIdx.x) return;
+    auto f = [&](uint32_t p) { return ss[row_start[p]]; };
+    const unsigned long long total = f(n);
+    const uint32_t lo = part == 0 ? 0u : part_lower_bound(f, n, part_target(total, part, nparts));
+    uint32_t hi = part + 1 >= nparts ? n : part_lower_bound(f, n, part_target(total, part + 1, nparts));
+    if (hi < lo) hi = lo;
+    st->part_lo = lo;
+    st->part_hi = hi;
+    st->part_slot_lo = f(lo);
+    st->part_slot_hi = f(hi);
+    st->pair_tests = f(hi) - f(lo);
+}
+
 inline unsigned nblk(uint64_t n, int nt = 256) { return (unsigned)((n + nt - 1) / nt); }
 
 // ---------------------------------------------------------------------------
@@ -1806,13 +1869,13 @@ int fsg_literal() {
 // build tiles + work items for schedule entries [lo, hi) of the sorted schedule
 // (the category counts in st describe the whole sorted schedule)
 uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, DBuf<Tile> &tiles,
-                    DBuf<uint32_t> &item_start, cudaStream_t s) {
+                    DBuf<uint32_t> &item_start, cudaStream_t s, int part_range = 0) {
     uint32_t n = hi - lo;
-    uint32_t max_tiles = n / 32 + 5;
+    uint32_t max_tiles = n / 32 + 5;     // also bounds the tiles of any sub-range (part_range)
     tiles = DBuf<Tile>(max_tiles, s);
     item_start = DBuf<uint32_t>(max_tiles + 1, s);
     k_make_tiles<<<nblk((uint64_t)max_tiles * 32), 256, 0, s>>>(sched, lo, n, st, lo, hi, tiles.p, max_tiles,
-                                                                item_start.p);
+                                                                item_start.p, part_range);
     TDS_CHECK_LAUNCH();
     uint32_t target = (uint32_t)persistent_blocks(RANGE_BPS) * (PT / 32) * 4;
     k_tile_chunks<<<nblk(max_tiles), 256, 0, s>>>(item_start.p, max_tiles, &st->union_total, st, target);
@@ -1833,7 +1896,8 @@ struct Ctx {
 }  // namespace
 
 void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64, float T0, float T1,
-            uint64_t capacity, cudaStream_t s, tds_result_s *res) {
+            uint64_t capacity, cudaStream_t s, tds_result_s *res, const SearchOpts &opt) {
+    const uint32_t part = opt.nparts > 1 ? opt.part : 0u, nparts = std::max<uint32_t>(opt.nparts, 1u);
     // fp32 paths use d rounded up (conservative: never drops a pair within the
     // caller's d); the fp64 evaluation uses the caller's d exactly
     float d = (float)d64;
@@ -1933,6 +1997,22 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
                 S.pair_tests_alt = p_t;
             }
         }
+        if (opt.plan_sel) {
+            // tds_plan: the schedule entry of every query row (query order, before the sort)
+            std::vector<Sched> hsched(n);
+            TDS_CUDA(cudaMemcpyAsync(hsched.data(), sched.p, sizeof(Sched) * n, cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaMemcpyAsync(pinned_stats(), dst.p, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+            TDS_CUDA(cudaStreamSynchronize(s));
+            if (pinned_stats()->bad)
+                fail(TDS_EDATA, "query segment %llu has a non-finite value or t_end <= t_start", ~pinned_stats()->bad);
+            for (uint32_t p = 0; p < n; ++p) {
+                opt.plan_sel[p] = hsched[p].sel;
+                opt.plan_lo[p] = hsched[p].lo;
+                opt.plan_hi[p] = hsched[p].hi;
+            }
+            S.kind = kind;
+            return;
+        }
         // sort S by (array selector, range start): one stable radix sort
         radix_sort_pairs(keys.p, order.p, n, 0, 16, s);
         {
@@ -1941,7 +2021,18 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             TDS_CHECK_LAUNCH();
             std::swap(sched.p, tmp.p);
         }
-        ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s);
+        if (nparts > 1) {
+            // this part's slice of the sorted schedule: equal shares of the exact pair tests
+            DBuf<uint64_t> w(n + 1, s);
+            k_sched_work<<<nblk(n + 1), 256, 0, s>>>(sched.p, n, w.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u64(w.p, w.p, n + 1, nullptr, s);
+            k_part_bounds<<<1, 32, 0, s>>>(w.p, n, part, nparts, dst.p);
+            TDS_CHECK_LAUNCH();
+            ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s, /*part_range=*/1);
+        } else {
+            ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s);
+        }
     } else {
         for (int c = 0; c < 3; ++c) { G.o[c] = idx->ext.lo[c]; G.w[c] = idx->w_fsg[c]; G.g[c] = idx->grid[c]; }
         qbox = DBuf<int4>(2ull * n, s);
@@ -1974,6 +2065,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         TDS_CHECK_LAUNCH();
         slot_start = DBuf<unsigned long long>(nrows + 1, s);
         exclusive_scan_u64(rl64.p, (uint64_t *)slot_start.p, nrows + 1, (uint64_t *)&dst.p->pair_tests, s);
+        if (nparts > 1) {   // this part: the queries whose slots cross equal shares of the total
+            k_part_bounds_spatial<<<1, 32, 0, s>>>(slot_start.p, row_start.p, n, part, nparts, dst.p);
+            TDS_CHECK_LAUNCH();
+        }
     }
     tr.mark("schedule");
     // pair tests bound the result count: size the pass buffer
@@ -1987,6 +2082,17 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     S.fallback_queries = hs.fallback;
     S.kind = kind;
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
+    unsigned long long slot_lo = 0, slot_hi = hs.pair_tests;   // GPUSpatial slots of this call
+    if (nparts > 1) {
+        if (spatial) {
+            S.n_queries = hs.part_hi - hs.part_lo;
+            slot_lo = hs.part_slot_lo;
+            slot_hi = hs.part_slot_hi;
+        } else {
+            const uint32_t live = (uint32_t)(nq - hs.cat_cnt[4]);
+            S.n_queries = std::min(hs.part_hi, live) > hs.part_lo ? std::min(hs.part_hi, live) - hs.part_lo : 0;
+        }
+    }
     // density probe, on large range searches only (one small kernel + a read-back):
     // dense-heavy searches (>= HYST_HI % of the probed pairs pass the filter) run the
     // four-candidate dense step (the D4 instantiation of k_pair_range)
@@ -2063,18 +2169,21 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         TDS_CHECK_LAUNCH();
         tr.note("dense4", d4 ? 1.0 : 0.0);
     } else if (nrows > 0 && hs.pair_tests > 0) {
-        const uint64_t ngrab = (hs.pair_tests + SP_GRAB - 1) / SP_GRAB;
+        const uint64_t nslots = slot_hi - slot_lo;
+        const uint64_t ngrab = (nslots + SP_GRAB - 1) / SP_GRAB;
         DBuf<uint32_t> grab_row(ngrab + 1, s);
-        k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, ngrab, grab_row.p);
+        k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, slot_lo, slot_hi, ngrab, grab_row.p);
         TDS_CHECK_LAUNCH();
         DBuf<uint32_t> slot_row;
-        if (hs.pair_tests <= SLOT_ROW_MAX) {
-            slot_row = DBuf<uint32_t>(hs.pair_tests, s);
-            k_slot_rows<<<nblk(hs.pair_tests), 256, 0, s>>>(slot_start.p, nrows, hs.pair_tests, slot_row.p);
+        if (nslots <= SLOT_ROW_MAX) {
+            slot_row = DBuf<uint32_t>(nslots, s);
+            k_slot_rows<<<nblk(nslots), 256, 0, s>>>(slot_start.p, nrows, slot_lo, nslots, slot_row.p);
             TDS_CHECK_LAUNCH();
         }
         SpatialArgs a{};
         a.slot_row = slot_row.p;
+        a.slot_lo = slot_lo;
+        a.slot_hi = slot_hi;
         a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
         a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
@@ -2303,16 +2412,18 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             TDS_CUDA(cudaStreamSynchronize(s));
             const uint64_t ngrab = (bslots + SP_GRAB - 1) / SP_GRAB;
             DBuf<uint32_t> grab_row(ngrab + 1, s);
-            k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, ngrab, grab_row.p);
+            k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, 0ull, bslots, ngrab, grab_row.p);
             TDS_CHECK_LAUNCH();
             DBuf<uint32_t> slot_row;
             if (bslots && bslots <= SLOT_ROW_MAX) {
                 slot_row = DBuf<uint32_t>(bslots, s);
-                k_slot_rows<<<nblk(bslots), 256, 0, s>>>(ss.p, bnrows, bslots, slot_row.p);
+                k_slot_rows<<<nblk(bslots), 256, 0, s>>>(ss.p, bnrows, 0ull, bslots, slot_row.p);
                 TDS_CHECK_LAUNCH();
             }
             SpatialArgs a{};
             a.slot_row = slot_row.p;
+            a.slot_lo = 0;
+            a.slot_hi = bslots;
             a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
             a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;

@@ -236,11 +236,19 @@ struct tds_result_s {
 };
 
 namespace tds {
+struct SearchOpts {
+    uint32_t part = 0, nparts = 1;            // tds_search_part: this part of a work-balanced split
+    int32_t *plan_sel = nullptr;              // tds_plan: host outputs per query row (range variants);
+    uint32_t *plan_lo = nullptr, *plan_hi = nullptr;   // set -> schedule only, no pair kernel
+};
 void search(tds_index_s *idx, int kind, const float4 *q, uint64_t nq, double d, float T0, float T1,
-            uint64_t capacity, cudaStream_t s, tds_result_s *res);
+            uint64_t capacity, cudaStream_t s, tds_result_s *res, const SearchOpts &opt = SearchOpts());
 void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint32_t *eid, float *tin,
            float *tout, bool dst_dev, bool sorted, cudaStream_t s);
 void free_result(tds_result_s *r);
+// rows of D owned by part `part` of `nparts` (partition.cu); rows: device, >= n / nparts + 1
+uint64_t time_partition(const float *t_start, uint64_t n, uint32_t part, uint32_t nparts, uint32_t *rows,
+                        cudaStream_t s);
 void merge_trajectories(tds_result_s *r, const uint32_t *q_traj, uint64_t nq, const uint32_t *e_traj, uint64_t ne,
                         float gap, cudaStream_t s, tds_result_s *out);
 }  // namespace tds

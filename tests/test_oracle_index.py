@@ -154,3 +154,106 @@ def test_fsg_build_roundtrip():
             k = np.searchsorted(Gm[:, 0], ir.linearize(*c, grid))
             assert e in A[Gm[k, 1]:Gm[k, 2] + 1]
     assert len(A) == total                                # #A = sum of cells per MBB
+
+
+# ---------------------------------------------------------------------------
+# extents, admissible v, geometry, C13 lookup and the schedule
+# ---------------------------------------------------------------------------
+def test_spatial_extent_and_admissible_v_fig4():
+    """Hand-derived from the Fig. 4 entry rows (golden file): x spans [0, 10]
+    (l9 starts at 0, l6 ends at 10) with the largest per-segment x extent 2
+    (l2, l4, l6, l9); y spans [2, 9] with largest extent 3 (l5, l9); z spans
+    [1, 13] with largest extent 6 (l4: 1 -> 7).  P:816-821: v <= floor(ext /
+    max extent) -> 5, 2 and exactly 12 / 6 = 2 (an integral bound)."""
+    D, _ = fig4()
+    lo, hi, mx = ir.spatial_extent(D)
+    assert lo.tolist() == [0.0, 2.0, 1.0]
+    assert hi.tolist() == [10.0, 9.0, 13.0]
+    assert mx.tolist() == [2.0, 3.0, 6.0]
+    assert ir.admissible_v(D).tolist() == [5.0, 2.0, 2.0]
+
+
+def test_spatial_extent_uses_both_endpoints_and_the_max():
+    # every extreme sits at a segment END, and the two segments have different
+    # per-dimension extents (a mean or a start-only reduction fails this)
+    D = np.array([[0, 0, 0, 0, 3, -1, 2, 1],
+                  [1, 1, 1, 0, -2, 4, 0, 1]], np.float32)
+    lo, hi, mx = ir.spatial_extent(D)
+    assert lo.tolist() == [-2.0, -1.0, 0.0]
+    assert hi.tolist() == [3.0, 4.0, 2.0]
+    assert mx.tolist() == [3.0, 3.0, 2.0]          # |3-0|, |4-1|, |2-0|
+    assert ir.admissible_v(D).tolist() == [1.0, 1.0, 1.0]
+    # 2.9999 -> 2 (floor), a zero extent -> unbounded
+    D2 = np.array([[0, 0, 5, 0, 1, 0, 5, 1], [2.9999, 0, 5, 1, 1.9999, 0, 5, 2]], np.float32)
+    v = ir.admissible_v(D2)
+    assert v[0] == 2.0 and np.isinf(v[1]) and np.isinf(v[2])
+
+
+def test_grid_geometry():
+    D = np.array([[0, 5, -1, 0, 12, 5, 2, 1]], np.float32)
+    o, w = ir.grid_geometry(D, (3, 4, 2))
+    assert o.tolist() == [0.0, 5.0, -1.0]
+    assert w.tolist() == [4.0, 1.0, 1.5]            # 12/3, zero extent -> 1, 3/2
+
+
+def test_member_extent_bins_fig3():
+    """C13 on Fig. 3 (m = 4): bin j's members end by 7.5, 6.2, 11, 12 and start
+    from 0, 3.9, 6.5, 9.3 (golden rows).  (3.0, 3.5): B_0 has members ending
+    after 3.0 and starting before 3.5; B_1's members all start at >= 3.9 ->
+    bins 0..0, although the literal B_1 = [3, 6.2] overlaps the query."""
+    Ds, _ = ir.temporal_sort(fig3_segments())
+    b = ir.temporal_bins(Ds, 4)
+    f = lambda a, z: ir.member_extent_bins(Ds, b["bin_of"], 4, a, z)
+    assert f(5.0, 5.5) == (0, 1)
+    assert f(3.0, 3.5) == (0, 0)
+    assert ir.temporal_schedule(b, 3.0, 3.5) == (0, 8)         # the literal bins: a superset
+    assert f(6.5, 6.9) == (0, 2)
+    assert f(7.55, 7.6) == (2, 2)                              # B_0 ends at 7.5 < 7.55
+    assert f(11.95, 12.5) == (3, 3)
+    assert f(12.5, 13.0) is None                               # nothing ends after 12.5
+    assert f(11.5, 11.6) == (3, 3)                             # B_2's members end by 11 < 11.5
+    assert f(-1.0, 0.0) is None                                # touches l0's start only (C5)
+
+
+def test_query_slabs_round_outward():
+    # 1 - 1e-8 rounds to 1.0 under round-to-nearest (slab 1); rounded down it is
+    # 0.99999994 (slab 0): the inflated box must include slab 0 (completeness)
+    lo, hi = ir.query_slabs(np.array([1, 1, 1, 0, 1, 1, 1, 1], np.float32), 1e-8, (0, 0, 0), (1, 1, 1), 4)
+    assert lo == [0, 0, 0] and hi == [1, 1, 1]
+    assert ir.d_up32(0.1) >= 0.1 and float(ir.d_up32(0.1)) == float(np.nextafter(np.float32(0.1), np.inf)) \
+        or float(np.float32(0.1)) >= 0.1
+
+
+def _plan_fixture():
+    # 4 entries, m = 2 bins over t in [0, 3] (b = 1.5), v = 2 slabs per dimension
+    # over x [0, 4], y [0, 2], z [0, 1] (widths 2, 1, 0.5)
+    D = np.array([[0, 0, 0, 0, 1, 0, 0, 1],
+                  [3, 1, 0, 0, 4, 1, 0, 1],
+                  [0, 0, 0, 2, 0, 1, 0, 3],
+                  [4, 2, 1, 2, 4, 2, 1, 3]], np.float32)
+    Q = np.array([[0.5, 0.2, 0, 0.2, 0.5, 0.2, 0, 0.8],      # x/y/z slab 0, bin 0: x and y tie at 1 -> x
+                  [1.9, 1.5, 0.5, 2.1, 2.1, 1.5, 0.5, 2.9],  # only y usable (slab 1), bin 1: Y[3:5]
+                  [1.9, 0.95, 0.5, 0.1, 2.1, 1.05, 0.5, 0.9],  # two slabs everywhere: temporal fallback
+                  [0.5, 0.2, 0, 5, 0.5, 0.2, 0, 6],          # after every entry: nothing
+                  [0.5, 0.2, 0, 1, 0.5, 0.2, 0, 2],          # touches bin 0's ends and bin 1's starts (C5)
+                  [0.5, 0.2, 0.8, 0.2, 0.5, 0.2, 0.8, 0.8]], np.float32)   # z slab 1 of bin 0 is empty -> picked
+    d = [0.25, 0.05, 0.05, 0.05, 0.05, 0.05]
+    return D, Q, d
+
+
+def test_st_arrays_and_plan_hand_example():
+    D, Q, d = _plan_fixture()
+    Ds, _ = ir.temporal_sort(D)
+    b = ir.temporal_bins(Ds, 2)
+    assert b["bin_of"].tolist() == [0, 0, 1, 1]
+    o, w = ir.grid_geometry(D, (2, 2, 2))
+    assert w.tolist() == [2.0, 1.0, 0.5]
+    arrays, _ = ir.st_arrays(Ds, b["bin_of"], 2, 2, o, w)
+    assert [a.tolist() for a in arrays] == [[0, 2, 1, 3], [0, 2, 1, 2, 3], [0, 1, 2, 3]]
+    st = [tuple(ir.plan(D, Q[k:k + 1], d[k], 2, 2, "spatiotemporal")[0]) for k in range(len(Q))]
+    assert st == [(0, 0, 1), (1, 3, 5), (-1, 0, 2), (3, 0, 0), (3, 0, 0), (3, 0, 0)]
+    tp = [tuple(ir.plan(D, Q[k:k + 1], d[k], 2, 2, "temporal")[0]) for k in range(len(Q))]
+    assert tp == [(-1, 0, 2), (-1, 2, 4), (-1, 0, 2), (3, 0, 0), (3, 0, 0), (-1, 0, 2)]
+    # a window that clips the query to nothing
+    assert tuple(ir.plan(D, Q[:1], 0.25, 2, 2, "temporal", window=(0.5, 1.0))[0]) == (-1, 0, 2)
+    assert tuple(ir.plan(D, Q[:1], 0.25, 2, 2, "temporal", window=(0.8, 1.0))[0]) == (3, 0, 0)
