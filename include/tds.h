@@ -99,6 +99,7 @@ typedef struct {
     int32_t kind;               /* the variant that ran (TDS_TEMPORAL / TDS_SPATIAL / TDS_SPATIOTEMPORAL) */
     int32_t reserved;
     uint64_t pair_tests_alt;    /* TDS_AUTO: scheduled pair tests of the variant not chosen (else 0) */
+    uint64_t capacity;          /* records the pass buffer held (after any halving on ENOMEM) */
 } tds_stats;
 
 /*
@@ -297,6 +298,17 @@ int tds_index_info(tds_index idx, uint64_t *n, int32_t *m, int32_t *v, int32_t *
 /* tds_kernel_launches — number of CUDA kernels this process has launched through
  * the library so far (a monotone counter; benchmarks difference it). */
 uint64_t tds_kernel_launches(void);
+
+/* tds_trim — release the device memory the library's pools hold unused (result
+ * buffers are kept for reuse by later searches until this call or until an
+ * allocation fails).  Current device; call when no search is running. */
+void tds_trim(void);
+
+/* tds_test_inject_enomem — TEST HOOK (fault injection, not for production use):
+ * k >= 0 makes the next k large (result buffer) allocations fail with
+ * TDS_ENOMEM; returns the number of failures injected so far in the process
+ * (k < 0: only query the counter). */
+uint64_t tds_test_inject_enomem(int k);
 
 /* tds_version — library build string. */
 const char *tds_version(void);

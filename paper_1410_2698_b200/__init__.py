@@ -35,7 +35,7 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
                "tds_version", "tds_kernel_launches", "tds_merge_trajectories", "tds_search_many",
-               "tds_search_part", "tds_plan", "tds_time_partition"]
+               "tds_search_part", "tds_plan", "tds_time_partition", "tds_trim", "tds_test_inject_enomem"]
 
 
 class TdsError(RuntimeError):
@@ -61,7 +61,8 @@ class _Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in ("n_results", "n_queries", "pair_tests", "pairs_executed",
                                                "refined_pairs", "passes", "spilled", "fallback_queries")] + \
                [(k, ctypes.c_float) for k in ("ms_schedule", "ms_pairs", "ms_compact", "ms_total")] + \
-               [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("pair_tests_alt", ctypes.c_uint64)]
+               [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("pair_tests_alt", ctypes.c_uint64),
+                ("capacity", ctypes.c_uint64)]
 
 
 _lib = None
@@ -96,6 +97,9 @@ def load_library(path: str = LIB_PATH):
     lib.tds_last_error.restype = ctypes.c_char_p
     lib.tds_version.restype = ctypes.c_char_p
     lib.tds_kernel_launches.restype = ctypes.c_uint64
+    lib.tds_trim.restype = None
+    lib.tds_test_inject_enomem.argtypes = [i32]
+    lib.tds_test_inject_enomem.restype = ctypes.c_uint64
     lib.tds_index_export.argtypes = [vp, i32, vp, u64, ctypes.POINTER(u64)]
     lib.tds_search_many.argtypes = [vp, i32, ctypes.POINTER(_SearchReq), ctypes.POINTER(vp), ctypes.POINTER(u64)]
     lib.tds_index_info.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_int32),
@@ -334,6 +338,17 @@ def time_partition(t_start, part: int, nparts: int, stream=None):
     _check(lib.tds_time_partition(ctypes.c_void_p(t.data_ptr()), n, int(part), int(nparts), _stream_ptr(stream),
                                   ctypes.c_void_p(rows.data_ptr()), ctypes.byref(cnt)))
     return rows[:cnt.value]
+
+
+def trim() -> None:
+    """tds_trim: release the device memory the library's pools hold unused."""
+    load_library().tds_trim()
+
+
+def test_inject_enomem(k: int = -1) -> int:
+    """TEST HOOK (tds_test_inject_enomem): fail the next k large allocations with
+    TDS_ENOMEM (k >= 0); returns the failures injected so far."""
+    return int(load_library().tds_test_inject_enomem(int(k)))
 
 
 def kernel_launches() -> int:

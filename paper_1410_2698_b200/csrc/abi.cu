@@ -53,23 +53,49 @@ void fail(int code, const char *fmt, ...) {
     throw Error{code, buf};
 }
 
-static void init_pool_once() {
-    static std::atomic<bool> done{false};
-    if (done.load(std::memory_order_acquire)) return;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;   // keep freed memory in the pool (no re-mapping per search)
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// Two private stream-ordered pools per device (the device's default pool and its
+// attributes are left alone: other libraries in the process may use it):
+//  * the small pool for temporaries (schedules, scans, staging), which keeps up to
+//    SMALL_KEEP bytes mapped between searches;
+//  * the big pool for result buffers, so that their tens-of-GB blocks are reused by
+//    later searches instead of being split by small temporaries; it keeps freed
+//    memory until tds_trim() (or an allocation failure) releases it.
+constexpr int MAX_DEV = 64;
+constexpr uint64_t SMALL_KEEP = 4ull << 30;
+
+static cudaMemPool_t make_pool(int dev, uint64_t keep) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
     }
-    done.store(true, std::memory_order_release);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    return pool;
 }
 
+static cudaMemPool_t device_pool(int which) {   // 0 small, 1 big
+    static cudaMemPool_t pools[2][MAX_DEV] = {};
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAX_DEV) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[which][dev]) pools[which][dev] = make_pool(dev, which ? UINT64_MAX : SMALL_KEEP);
+    return pools[which][dev];
+}
+
+static cudaMemPool_t small_pool() { return device_pool(0); }
+static cudaMemPool_t big_pool() { return device_pool(1); }
+
 void *dalloc(size_t bytes, cudaStream_t s) {
-    init_pool_once();
     void *p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    cudaMemPool_t pool = small_pool();
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, bytes, pool, s) : cudaMallocAsync(&p, bytes, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         fail(e == cudaErrorMemoryAllocation ? TDS_ENOMEM : TDS_ECUDA, "cudaMallocAsync(%zu bytes): %s", bytes,
@@ -82,31 +108,10 @@ void dfree(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
-// A separate stream-ordered pool for the large result buffers, so that their
-// blocks are reused by later searches instead of being split by the many small
-// temporaries of the default pool (which forces fresh mappings of tens of GB).
-static cudaMemPool_t big_pool() {
-    static cudaMemPool_t pool = nullptr;
-    static int dev_of_pool = -1;
-    static std::mutex mu;                     // concurrent searches (tds_search_many)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(mu);
-    if (pool && dev_of_pool == dev) return pool;
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.handleTypes = cudaMemHandleTypeNone;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
-        cudaGetLastError();
-        pool = nullptr;
-        return nullptr;
-    }
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    dev_of_pool = dev;
-    return pool;
+// release the memory both pools of the current device hold unused (tds_trim)
+void trim_pools() {
+    for (int w = 0; w < 2; ++w)
+        if (cudaMemPool_t pool = device_pool(w)) cudaMemPoolTrimTo(pool, 0);
 }
 
 void *dalloc_big(size_t bytes, cudaStream_t s);
@@ -121,8 +126,8 @@ static uint64_t device_budget_bytes_now();
 // other's buffers; allocations by other libraries after the snapshot are not
 // tracked (the 0.45 factor and the halving retry on ENOMEM cover them).
 static uint64_t pools_used_bytes(int dev) {
-    cudaMemPool_t pools[2] = {nullptr, big_pool()};
-    cudaDeviceGetDefaultMemPool(&pools[0], dev);
+    (void)dev;
+    cudaMemPool_t pools[2] = {small_pool(), big_pool()};
     uint64_t tot = 0;
     for (cudaMemPool_t pool : pools) {
         uint64_t used = 0;
@@ -173,8 +178,8 @@ static uint64_t device_budget_bytes_now() {
     uint64_t extra = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaMemPool_t pools[2] = {nullptr, big_pool()};
-    cudaDeviceGetDefaultMemPool(&pools[0], dev);
+    (void)dev;
+    cudaMemPool_t pools[2] = {small_pool(), big_pool()};
     for (cudaMemPool_t pool : pools) {
         if (!pool) continue;
         uint64_t reserved = 0, used = 0;
@@ -185,26 +190,20 @@ static uint64_t device_budget_bytes_now() {
     return (uint64_t)fr + extra;
 }
 
-// Fault injection (tests): TDS_INJECT_ENOMEM="k[:tag]" makes the next k large
-// allocations fail with TDS_ENOMEM; a new value (another tag) re-arms it.
+// Fault injection for tests (tds_test_inject_enomem): the next k large
+// allocations fail with TDS_ENOMEM; g_injected counts the failures injected.
+static std::atomic<int> g_inject_left{0};
+static std::atomic<uint64_t> g_injected{0};
+
 static bool inject_enomem() {
-    const char *e = getenv("TDS_INJECT_ENOMEM");
-    if (!e || !*e) return false;
-    static std::mutex mu;
-    static std::string armed;
-    static int left = 0;
-    std::lock_guard<std::mutex> lock(mu);
-    if (armed != e) {
-        armed = e;
-        left = atoi(e);
-    }
-    if (left <= 0) return false;
-    --left;
+    if (g_inject_left.load(std::memory_order_relaxed) <= 0) return false;
+    if (g_inject_left.fetch_sub(1) <= 0) return false;
+    g_injected.fetch_add(1);
     return true;
 }
 
 void *dalloc_big(size_t bytes, cudaStream_t s) {
-    if (inject_enomem()) fail(TDS_ENOMEM, "injected allocation failure (TDS_INJECT_ENOMEM), %zu bytes", bytes);
+    if (inject_enomem()) fail(TDS_ENOMEM, "injected allocation failure (tds_test_inject_enomem), %zu bytes", bytes);
     cudaMemPool_t pool = big_pool();
     if (!pool) return dalloc(bytes, s);
     void *p = nullptr;
@@ -346,6 +345,13 @@ const char *tds_last_error(void) { return tds::last_error(); }
 const char *tds_version(void) { return "tds-b200 0.1 (sm_100a)"; }
 
 uint64_t tds_kernel_launches(void) { return tds::g_launches.load(); }
+
+void tds_trim(void) { tds::trim_pools(); }
+
+uint64_t tds_test_inject_enomem(int k) {
+    if (k >= 0) tds::g_inject_left.store(k);
+    return tds::g_injected.load();
+}
 
 int tds_build_index(const tds_seg *entries, uint64_t n, const tds_index_params *params, void *stream,
                     tds_index *out) {

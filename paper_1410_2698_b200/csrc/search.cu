@@ -1615,22 +1615,45 @@ __global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_c
 // ---------------------------------------------------------------------------
 // overflow handling (A10): keep records of complete queries, re-plan the rest
 // ---------------------------------------------------------------------------
-__global__ void k_keep_flags(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
-                             const uint32_t *__restrict__ chunk_used, const uint64_t *__restrict__ chunk_off,
-                             const uint8_t *__restrict__ redo, Rec *__restrict__ flat, uint8_t *__restrict__ keep,
-                             uint64_t nflat) {
-    // flatten the chunked buffer (one warp per chunk) and flag records to keep
+// records of each chunk of the pass buffer to keep (their query did not lose a
+// record, so it is not re-run); one warp per chunk
+__global__ void k_chunk_kept(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                             const uint32_t *__restrict__ chunk_used, const uint8_t *__restrict__ redo,
+                             uint64_t *__restrict__ kept) {
+    uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (c > nchunks) return;
+    uint32_t cnt = 0;
+    if (c < nchunks) {
+        const uint32_t u = chunk_used[c];
+        for (uint32_t k = lane; k < u; k += 32) cnt += redo[buf[c * CS + k].qid] ? 0u : 1u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    if (lane == 0) kept[c] = cnt;                 // kept[nchunks] = 0 (total after the scan)
+}
+
+// kept records straight from the chunked pass buffer into the exact store, in
+// chunk order (warp per chunk; positions by ballot within the chunk)
+__global__ void k_scatter_kept_chunked(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                                       const uint32_t *__restrict__ chunk_used, const uint8_t *__restrict__ redo,
+                                       const uint64_t *__restrict__ kept_off, Rec *__restrict__ out) {
     uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (c >= nchunks) return;
-    uint32_t u = chunk_used[c];
-    uint64_t o = chunk_off[c];
-    for (uint32_t k = lane; k < u; k += 32) {
-        Rec r = buf[c * CS + k];
-        if (o + k < nflat) {
-            flat[o + k] = r;
-            keep[o + k] = redo[r.qid] ? 0 : 1;
+    const uint32_t u = chunk_used[c];
+    uint64_t base = kept_off[c];
+    for (uint32_t k0 = 0; k0 < u; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        Rec r{0u, 0u, 0.f, 0.f};
+        bool keep = false;
+        if (k < u) {
+            r = buf[c * CS + k];
+            keep = !redo[r.qid];
         }
+        const unsigned m = __ballot_sync(FULL, keep);
+        if (keep) out[base + __popc(m & ((1u << lane) - 1u))] = r;
+        base += __popc(m);
     }
 }
 
@@ -1645,16 +1668,6 @@ __global__ void k_flatten(const Rec *__restrict__ buf, uint32_t CS, uint64_t nch
     for (uint32_t k = lane; k < u; k += 32) flat[o + k] = buf[c * CS + k];
 }
 
-__global__ void k_u8_to_u32(const uint8_t *__restrict__ a, uint64_t n, uint32_t *__restrict__ b) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = a[i];
-}
-
-__global__ void k_scatter_kept(const Rec *__restrict__ flat, const uint8_t *__restrict__ keep,
-                               const uint32_t *__restrict__ pos, uint64_t n, Rec *__restrict__ out) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && keep[i]) out[pos[i]] = flat[i];
-}
 
 __global__ void k_chunk_offsets_u64(const uint32_t *__restrict__ used, uint64_t n, uint64_t *__restrict__ out) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2146,6 +2159,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     }
     tr.mark("alloc");
     tr.note("cap_GB", cap * sizeof(Rec) / 1e9);
+    S.capacity = cap;
     if (big_lock.owns_lock()) big_lock.unlock();   // the pool counts the buffer from here on
     DBuf<uint32_t> chunk_used(nchunks, s);
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
@@ -2249,21 +2263,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     }
 
     // ---- overflow: keep complete queries, re-plan the others exactly ------------
-    const uint64_t stored = std::min<unsigned long long>(hs.reserved, cap);
-    uint64_t nflat = hs.hits - hs.dropped;          // records physically in the buffer
-    (void)stored;
-    DBuf<Rec> flat(nflat, s, /*big=*/true);
-    DBuf<uint8_t> keep(nflat, s);
-    k_keep_flags<<<nblk(std::max<uint64_t>(nres, 1) * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, chunk_off.p, redo.p, flat.p,
-                                                  keep.p, nflat);
+    // memory: the pass buffer + 8 B per chunk + the exact store; kept records move
+    // from the chunked buffer straight into the store
+    DBuf<uint64_t> kept_off(nres + 1, s);
+    k_chunk_kept<<<nblk((nres + 1) * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, redo.p, kept_off.p);
     TDS_CHECK_LAUNCH();
-    DBuf<uint32_t> kpos(nflat + 1, s), k32(nflat + 1, s);
-    TDS_CUDA(cudaMemsetAsync(k32.p, 0, 4ull * (nflat + 1), s));
-    k_u8_to_u32<<<nblk(nflat), 256, 0, s>>>(keep.p, nflat, k32.p);
-    TDS_CHECK_LAUNCH();
-    exclusive_scan_u32(k32.p, kpos.p, nflat + 1, nullptr, s);
-    uint32_t nkept = 0;
-    TDS_CUDA(cudaMemcpyAsync(&nkept, kpos.p + nflat, 4, cudaMemcpyDeviceToHost, s));
+    exclusive_scan_u64(kept_off.p, kept_off.p, nres + 1, nullptr, s);
+    uint64_t nkept = 0;
+    TDS_CUDA(cudaMemcpyAsync(&nkept, kept_off.p + nres, 8, cudaMemcpyDeviceToHost, s));
 
     // redo list with exact counts, in schedule order (range) / input order (spatial)
     std::vector<uint32_t> hcnt;
@@ -2303,13 +2310,43 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
                           (unsigned long long)cap);
         redo_total += c;
     }
-    const uint64_t total = (uint64_t)nkept + redo_total;
-    DBuf<Rec> store(total, s, /*big=*/true);
-    k_scatter_kept<<<nblk(nflat), 256, 0, s>>>(flat.p, keep.p, kpos.p, nflat, store.p);
-    TDS_CHECK_LAUNCH();
-    flat.reset();
-    keep.reset();
-    buf.reset();
+    const uint64_t total = nkept + redo_total;
+    DBuf<Rec> store;
+    try {
+        store = DBuf<Rec>(total, s, /*big=*/true);
+    } catch (const Error &e) {
+        if (e.code != TDS_ENOMEM) throw;
+        set_error(0, "");
+    }
+    if (store.p) {
+        if (nres) {
+            k_scatter_kept_chunked<<<nblk(nres * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, redo.p,
+                                                                   kept_off.p, store.p);
+            TDS_CHECK_LAUNCH();
+        }
+        buf.reset();
+    } else {
+        // not enough device memory for the pass buffer and the exact store at once:
+        // spill the kept records to mapped pinned host memory, release the pass
+        // buffer, then allocate the store and copy them back (peak = the larger one)
+        Rec *host = nullptr, *host_dev = nullptr;
+        TDS_CUDA(cudaHostAlloc((void **)&host, std::max<uint64_t>(nkept, 1) * sizeof(Rec), cudaHostAllocMapped));
+        struct HostFree { Rec *p; ~HostFree() { cudaFreeHost(p); } } host_guard{host};
+        TDS_CUDA(cudaHostGetDevicePointer((void **)&host_dev, host, 0));
+        if (nres) {
+            k_scatter_kept_chunked<<<nblk(nres * 32), 256, 0, s>>>(buf.p, CS, nres, chunk_used.p, redo.p,
+                                                                   kept_off.p, host_dev);
+            TDS_CHECK_LAUNCH();
+        }
+        buf.reset();
+        TDS_CUDA(cudaStreamSynchronize(s));
+        device_budget_refresh();
+        store = DBuf<Rec>(total, s, /*big=*/true);
+        if (nkept) TDS_CUDA(cudaMemcpyAsync(store.p, host, nkept * sizeof(Rec), cudaMemcpyHostToDevice, s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        tr.note("spilled_to_host", (double)nkept);
+    }
+    kept_off.reset();
     S.spilled = nkept;
 
     // per-query exact offsets in redo order

@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import synth
-from parity import check
+from parity import check, stratified
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -56,16 +56,21 @@ def _cuda(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
+NS = 2048          # 2,048 time-stratified queries per full-size configuration
+
+
 @pytest.fixture(scope="module")
 def dense():
     return synth.random_dense()
 
 
-@pytest.mark.parametrize("d", [0.01, 0.09])
+@pytest.mark.parametrize("d", [0.01, 0.03, 0.05, 0.07, 0.09])
 def test_random_dense_full(tds, dense, d):
+    """Random-dense-shaped at full size (the bench's headline configuration)
+    over the density sweep of P:1633-1634 / P:1689-1697, GPUSpatioTemporal and
+    GPUTemporal; d = 0.09 is the output-bound point (~2.5e9 records)."""
     w = dense
-    rng = np.random.default_rng(int(d * 1000))
-    sel = np.sort(rng.choice(w.Q.shape[0], 96, replace=False))
+    sel = stratified(w.Q, NS, seed=int(d * 1000))
     ref = oracle.search(w.D, w.Q, d, qsel=sel)
     idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=w.m_bins, v=w.v_subbins)
     Qd = _cuda(w.Q)
@@ -85,8 +90,7 @@ def test_random_dense_paper_buffer(tds, dense):
     full size gives the same result set as one pass."""
     w = dense
     d = 0.03
-    rng = np.random.default_rng(3)
-    sel = np.sort(rng.choice(w.Q.shape[0], 64, replace=False))
+    sel = stratified(w.Q, 256, seed=3)
     ref = oracle.search(w.D, w.Q, d, qsel=sel)
     idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL, m=w.m_bins)
     Qd = _cuda(w.Q)
@@ -97,37 +101,43 @@ def test_random_dense_paper_buffer(tds, dense):
     assert st2["passes"] == 1 and (n, h) == (n2, h2)
 
 
-def test_merger_full(tds):
-    w = synth.merger()
-    d = 1.0
-    rng = np.random.default_rng(7)
-    sel = np.sort(rng.choice(w.Q.shape[0], 64, replace=False))
+@pytest.fixture(scope="module")
+def merger():
+    return synth.merger()
+
+
+@pytest.mark.parametrize("d", [1.0, 5.0])
+def test_merger_full(tds, merger, d):
+    """Merger-shaped at full size, all three variants; d = 5 kpc is the paper's
+    largest (~1.5e9 records): GPUSpatial's hit-heavy path."""
+    w = merger
+    sel = stratified(w.Q, NS, seed=7 + int(d))
     ref = oracle.search(w.D, w.Q, d, qsel=sel)
     idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
     Qd = _cuda(w.Q)
     out = {}
     for kind in ("temporal", "spatiotemporal", "spatial"):
         got, n, h, st = _search_sampled(idx, Qd, d, kind, sel)
-        check(got, ref, w.D, w.Q, d, label=f"merger {kind}")
+        check(got, ref, w.D, w.Q, d, label=f"merger d={d} {kind}")
         out[kind] = (n, h)
     assert out["temporal"] == out["spatiotemporal"] == out["spatial"]
 
 
-def test_scale_out_shard(tds):
-    """scale-out (BASELINE.json configs[4]): the 100M-segment database, one GPU's
-    shard of the 10M query segments (1/8), GPUTemporal and GPUSpatioTemporal,
-    sampled against the oracle and cross-checked by hash."""
-    w = synth.scale_out(shard=(3, 8), d=5.0)
-    assert w.D.shape[0] == 99_750_000
-    d = 5.0
-    rng = np.random.default_rng(9)
-    sel = np.sort(rng.choice(w.Q.shape[0], 24, replace=False))
+@pytest.mark.parametrize("d,ns", [(50.0, NS), (5.0, 256)])
+def test_scale_out_full(tds, d, ns):
+    """scale-out (BASELINE.json configs[4]): the 100M-segment database and the
+    full 10M query segments on one GPU (the bench's N = 1 launch; at N GPUs each
+    rank runs a part of this search), GPUTemporal and GPUSpatioTemporal, sampled
+    against the oracle and cross-checked by hash."""
+    w = synth.scale_out(d=d)
+    assert w.D.shape[0] == 99_750_000 and w.Q.shape[0] == 9_975_000
+    sel = stratified(w.Q, ns, seed=9)
     ref = oracle.search(w.D, w.Q, d, qsel=sel)
     idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=w.m_bins, v=w.v_subbins)
     Qd = _cuda(w.Q)
     out = {}
     for kind in ("temporal", "spatiotemporal"):
         got, n, h, st = _search_sampled(idx, Qd, d, kind, sel)
-        check(got, ref, w.D, w.Q, d, label=f"scale-out {kind}")
+        check(got, ref, w.D, w.Q, d, label=f"scale-out d={d} {kind}")
         out[kind] = (n, h)
     assert out["temporal"] == out["spatiotemporal"]

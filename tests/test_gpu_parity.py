@@ -156,11 +156,18 @@ def test_host_inputs_and_host_fetch(tds, tiny):
 
 
 def test_index_build_matches_paper_structures(tds, tiny):
-    """GPU bins / X-Y-Z / FSG arrays equal oracle/index_ref on the same data."""
+    """GPU extents / bins / X-Y-Z / FSG arrays equal oracle/index_ref on the same
+    data; the geometry (extents, slab and cell widths) is computed by index_ref
+    from D, not taken from the GPU."""
     from oracle import index_ref as ir
     w, _ = tiny
     m, v, grid = 7, 2, (4, 3, 5)
     idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=m, v=v, grid=grid)
+    ext = idx.export("extents")
+    lo, hi, mx = ir.spatial_extent(w.D)
+    assert np.array_equal(ext[2:5], lo.astype(np.float32)) and np.array_equal(ext[5:8], hi.astype(np.float32))
+    assert np.array_equal(ext[8:11], mx.astype(np.float32))      # |c1 - c0| rounded to float32
+    assert ext[0] == w.D[:, 3].min() and ext[1] == w.D[:, 7].max()
     Ds, perm = ir.temporal_sort(w.D)
     assert np.array_equal(idx.export("perm"), perm)
     b = ir.temporal_bins(Ds, m)
@@ -171,23 +178,66 @@ def test_index_build_matches_paper_structures(tds, tiny):
             assert max(b["B_start"][j] + b["b"], idx.export("bin_hi")[j]) == pytest.approx(b["B_end"][j])
         else:
             assert off[j] == off[j + 1]
-    ext = idx.export("extents")
-    lo, hi = ext[2:5], ext[5:8]
-    wst = ext[11:14]
-    arrays, ranges = ir.st_arrays(Ds, b["bin_of"], m, v, lo, wst)
+    o, wst = ir.grid_geometry(w.D, (v, v, v))
+    assert np.array_equal(ext[11:14], wst)
+    arrays, ranges = ir.st_arrays(Ds, b["bin_of"], m, v, o, wst)
     for c, name in enumerate(("st_x", "st_y", "st_z")):
         assert np.array_equal(idx.export(name), arrays[c])
-        o = idx.export(["st_off_x", "st_off_y", "st_off_z"][c])
+        offs = idx.export(["st_off_x", "st_off_y", "st_off_z"][c])
         for (i, j), rg in ranges[c].items():
-            a0, a1 = o[j * m + i], o[j * m + i + 1]
+            a0, a1 = offs[j * m + i], offs[j * m + i + 1]
             assert (rg is None and a0 == a1) or (rg is not None and (a0, a1 - 1) == rg)
-    wf = (hi - lo) / np.array(grid, np.float32)
-    G, A = ir.fsg_build(Ds, grid, lo, wf)
+    o_f, wf = ir.grid_geometry(w.D, grid)
+    G, A = ir.fsg_build(Ds, grid, o_f, wf)
     cell_off = idx.export("fsg_cell_off")
     A_gpu = idx.export("fsg_A")
     assert np.array_equal(A_gpu, A)
     for h, a0, a1 in G:
         assert cell_off[h] == a0 and cell_off[h + 1] == a1 + 1
+
+
+def test_admissible_v_matches_index_ref(tds, tiny):
+    """the build accepts v up to index_ref.admissible_v (same v in all
+    dimensions, so the smallest bound) and rejects the next."""
+    from oracle import index_ref as ir
+    w, _ = tiny
+    vmax = int(ir.admissible_v(w.D).min())
+    assert vmax >= 1
+    tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=5, v=vmax).close()
+    with pytest.raises(tds.TdsError) as ei:
+        tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=5, v=vmax + 1)
+    assert ei.value.status == "TDS_EINVAL"
+
+
+@pytest.mark.parametrize("case", ["tiny", "tiny-window", "dense-small", "hand"])
+@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
+def test_plan_matches_index_ref(tds, case, kind):
+    """tds_plan (the GPU schedule: C13 bin lookup, slab choice, fallback) equals
+    index_ref.plan query by query: same selector (dimension or temporal
+    fallback or empty) and the same range."""
+    from oracle import index_ref as ir
+    window = (-math.inf, math.inf)
+    if case.startswith("tiny"):
+        w = synth.tiny()
+        D, Q, d, m, v = w.D, w.Q, w.d, 10, 2
+        if case == "tiny-window":
+            window = (1.5, 4.25)
+    elif case == "dense-small":
+        w = synth.random_dense(n_particles=512, n_timesteps=13, n_query_traj=64)
+        D, Q, d, m, v = w.D, w.Q, 0.001, 12, 2
+    else:
+        import test_oracle_index as toi
+        D, Q, ds = toi._plan_fixture()
+        d, m, v = ds[0], 2, 2
+    idx = tds.Index(_cuda(D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=m, v=v)
+    sel, lo, hi = idx.plan(_cuda(Q), d, window=window, kind=kind)
+    want = ir.plan(D, Q, d, m, v, kind, window=window)
+    got = np.stack([sel.astype(np.int64), lo.astype(np.int64), hi.astype(np.int64)], 1)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert bad.size == 0, f"{bad.size} queries differ, e.g. {[(int(k), got[k].tolist(), want[k].tolist()) for k in bad[:5]]}"
+    if kind == "spatiotemporal" and case != "hand":
+        assert ((sel >= 0) & (sel < 3)).any()             # both subbin and fallback paths exercised
+        assert ((sel == -1) | (sel == 3)).any()
 
 
 @pytest.fixture(scope="module")
@@ -307,6 +357,7 @@ def test_time_partitioned_union_equals_single_index(tds, world):
     import torch
     from paper_1410_2698_b200.dist import TimeShardedIndex
     w = synth.random_1m(n_traj=400)
+    ref = oracle.search(w.D, w.Q, 20.0)
     full = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=1000, v=2)
     for kind in ("temporal", "spatiotemporal"):
         r = full.search(_cuda(w.Q), 20.0, kind=kind)
@@ -315,11 +366,11 @@ def test_time_partitioned_union_equals_single_index(tds, world):
         parts = []
         for rank in range(world):
             sh = TimeShardedIndex(w.D, rank, world, kinds=tds.TEMPORAL | tds.SPATIOTEMPORAL, m=1000, v=2)
-            q, e, _, _ = sh.search(_cuda(w.Q), 20.0, kind=kind)
-            parts.append(keys(q.cpu().numpy(), e.cpu().numpy()))
-        kb = np.sort(np.concatenate(parts))
-        assert np.unique(kb).size == kb.size
-        assert np.array_equal(ka, kb)
+            q, e, ti, to = sh.search(_cuda(w.Q), 20.0, kind=kind)
+            parts.append([x.cpu().numpy() for x in (q, e, ti, to)])
+        u = [np.concatenate([p_[k] for p_ in parts]) for k in range(4)]
+        check(tuple(u), ref, w.D, w.Q, 20.0, label=f"time slices x{world} {kind}")   # the oracle, no duplicates
+        assert np.array_equal(ka, np.sort(keys(u[0], u[1])))
 
 
 @pytest.mark.parametrize("kind", ["temporal", "spatiotemporal", "spatial"])
@@ -415,6 +466,7 @@ def test_st_materialised_ablation_same_result(tds, monkeypatch):
     mat = tds.Index(_cuda(w.D), kinds=tds.SPATIOTEMPORAL, m=1000, v=4)
     b = mat.search(_cuda(w.Q), 30.0, kind="spatiotemporal").fetch(sorted=True, device=False)
     assert len(a[0]) > 0
+    check(b, oracle.search(w.D, w.Q, 30.0), w.D, w.Q, 30.0, label="ST materialised")
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
 
@@ -459,6 +511,7 @@ def test_tight_range_equals_bin_hull(tds, name, kind, monkeypatch):
     got, st = _run(idx, w.Q, d, kind)
     monkeypatch.delenv("TDS_TIGHT_RANGE")
     assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(hull[0], hull[1])))
+    check(got, oracle.search(w.D, w.Q, d), w.D, w.Q, d, label=f"tight ranges {kind}")
     assert st["pair_tests"] <= st_h["pair_tests"]
     if name != "tiny" and kind == "temporal":
         assert st["pair_tests"] < st_h["pair_tests"]
@@ -490,43 +543,85 @@ def test_dense4_instantiation_matches_oracle(tds, name, kind, monkeypatch):
 
 
 @pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
-def test_enomem_fallback_injected(tds, kind, monkeypatch):
+def test_enomem_fallback_injected(tds, kind):
     """Fault injection: the automatic result capacity survives failed
-    allocations of its pass buffer (TDS_INJECT_ENOMEM) by
-    halving the capacity and re-taking the memory budget (one or two injected
-    failures, as far as the floor allows); the result is the same pair set as
-    without failures.  A single failure with capacity at the floor
-    surfaces as TDS_ENOMEM."""
+    allocations of its pass buffer (tds_test_inject_enomem) by halving the
+    capacity and re-taking the memory budget; the result is the same pair set as
+    without failures, the failures were injected, and the capacity halved once
+    per failure.  A failure with the capacity at the floor surfaces as
+    TDS_ENOMEM."""
     w = synth.random_1m(n_traj=300, query_frac_stride=10)
     d = 20.0
     idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
     base, st = _run(idx, w.Q, d, kind)
     assert st["pair_tests"] > (1 << 20)              # above the halving floor
     nfail = 2 if st["pair_tests"] > 4 * (1 << 20) else 1
-    monkeypatch.setenv("TDS_INJECT_ENOMEM", f"{nfail}:{kind}")
-    got, _ = _run(idx, w.Q, d, kind)
-    monkeypatch.delenv("TDS_INJECT_ENOMEM")
+    n0 = tds.test_inject_enomem(nfail)
+    got, st2 = _run(idx, w.Q, d, kind)
+    assert tds.test_inject_enomem(0) == n0 + nfail
+    assert st2["capacity"] == st["capacity"] >> nfail
     assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(base[0], base[1])))
     ref = oracle.search(w.D, w.Q[:400], d)
     sel = got[0] < 400
     check(tuple(x[sel] for x in got), ref, w.D, w.Q[:400], d, label=f"{kind} enomem")
     small = w.Q[:50]
-    monkeypatch.setenv("TDS_INJECT_ENOMEM", f"1:{kind}-floor")
-    with pytest.raises(tds.TdsError):
+    n1 = tds.test_inject_enomem(1)
+    with pytest.raises(tds.TdsError) as ei:
         _run(idx, small, d, kind)
-    monkeypatch.delenv("TDS_INJECT_ENOMEM")
+    assert ei.value.status == "TDS_ENOMEM"
+    assert tds.test_inject_enomem(0) == n1 + 1
 
 
-def test_enomem_injected_spatial_surfaces(tds, monkeypatch):
+def test_enomem_injected_spatial_surfaces(tds):
     """GPUSpatial with a small automatic capacity (below the halving floor): an
     injected pass-buffer allocation failure surfaces as TDS_ENOMEM, and the next
     search succeeds."""
     w = synth.tiny()
     idx = tds.Index(_cuda(w.D), kinds=tds.SPATIAL, m=w.m_bins, grid=w.grid)
-    monkeypatch.setenv("TDS_INJECT_ENOMEM", "1:spatial-floor")
+    n0 = tds.test_inject_enomem(1)
     with pytest.raises(tds.TdsError) as ei:
         _run(idx, w.Q, w.d, "spatial")
     assert ei.value.status == "TDS_ENOMEM"
+    assert tds.test_inject_enomem(0) == n0 + 1
     got, _ = _run(idx, w.Q, w.d, "spatial")
-    monkeypatch.delenv("TDS_INJECT_ENOMEM")
     check(got, oracle.search(w.D, w.Q, w.d), w.D, w.Q, w.d, label="spatial after injected ENOMEM")
+
+
+def test_real_memory_pressure_overflow(tds):
+    """Real memory pressure (no injection): a ballast allocation leaves the search
+    room for about 1.4x its result records; the automatic capacity halves on
+    ENOMEM until the pass buffer fits, the pass overflows, the kept records
+    spill to host memory while the exact store is allocated, and the re-plan
+    returns the same records (reading C22)."""
+    import torch
+    w = synth.random_dense(n_particles=8192, n_timesteps=49, n_query_traj=1024)
+    d = 0.03
+    idx = tds.Index(_cuda(w.D), kinds=tds.TEMPORAL, m=200)
+    Q = _cuda(w.Q)
+    r = idx.search(Q, d, kind="temporal")
+    base = r.fetch(sorted=True, device=False)
+    need = 16 * r.count
+    r.close()
+    assert need > (256 << 20)
+    tds.trim()
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    # room for ~1.4x the result set: below what the automatic capacity asks for
+    # (the pair-test bound) and below the pass buffer + exact store of an overflow
+    ballast = torch.empty(max(0, free - (14 * need) // 10 - (64 << 20)), dtype=torch.uint8, device="cuda")
+    try:
+        tds.trim()
+        r = idx.search(Q, d, kind="temporal")
+        st = r.stats()
+        got = r.fetch(sorted=True, device=False)
+        r.close()
+    finally:
+        del ballast
+        torch.cuda.empty_cache()
+    assert st["passes"] > 1 and st["capacity"] * 16 < need
+    for x, y in zip(got, base):
+        assert np.array_equal(x, y)
+    sel = np.unique(got[0])[:: max(1, np.unique(got[0]).size // 200)]
+    ref = oracle.search(w.D, w.Q, d, qsel=sel)
+    m = np.isin(got[0], sel)
+    check(tuple(x[m] for x in got), ref, w.D, w.Q, d, label="memory pressure")
