@@ -305,10 +305,10 @@ uint64_t tds_kernel_launches(void);
 void tds_trim(void);
 
 /* tds_test_inject_enomem — TEST HOOK (fault injection, not for production use):
- * k >= 0 makes the next k large (result buffer) allocations fail with
- * TDS_ENOMEM; returns the number of failures injected so far in the process
- * (k < 0: only query the counter). */
-uint64_t tds_test_inject_enomem(int k);
+ * k >= 0: after letting the next `skip` large (result buffer) allocations
+ * through, make the following k fail with TDS_ENOMEM.  Returns the number of
+ * failures injected so far in the process (k < 0: only query the counter). */
+uint64_t tds_test_inject_enomem(int k, int skip);
 
 /* tds_version — library build string. */
 const char *tds_version(void);

@@ -98,7 +98,7 @@ def load_library(path: str = LIB_PATH):
     lib.tds_version.restype = ctypes.c_char_p
     lib.tds_kernel_launches.restype = ctypes.c_uint64
     lib.tds_trim.restype = None
-    lib.tds_test_inject_enomem.argtypes = [i32]
+    lib.tds_test_inject_enomem.argtypes = [i32, i32]
     lib.tds_test_inject_enomem.restype = ctypes.c_uint64
     lib.tds_index_export.argtypes = [vp, i32, vp, u64, ctypes.POINTER(u64)]
     lib.tds_search_many.argtypes = [vp, i32, ctypes.POINTER(_SearchReq), ctypes.POINTER(vp), ctypes.POINTER(u64)]
@@ -345,10 +345,10 @@ def trim() -> None:
     load_library().tds_trim()
 
 
-def test_inject_enomem(k: int = -1) -> int:
-    """TEST HOOK (tds_test_inject_enomem): fail the next k large allocations with
-    TDS_ENOMEM (k >= 0); returns the failures injected so far."""
-    return int(load_library().tds_test_inject_enomem(int(k)))
+def test_inject_enomem(k: int = -1, skip: int = 0) -> int:
+    """TEST HOOK (tds_test_inject_enomem): after ``skip`` large allocations, fail
+    the next k with TDS_ENOMEM (k >= 0); returns the failures injected so far."""
+    return int(load_library().tds_test_inject_enomem(int(k), int(skip)))
 
 
 def kernel_launches() -> int:

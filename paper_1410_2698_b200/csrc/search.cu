@@ -35,24 +35,15 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
 constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
-#ifndef TDS_DENSE4
-#define TDS_DENSE4 2          // dense windows, four candidates per query step: 0 never, 1 always, 2 by probe
-#endif
-#ifndef TDS_HYST
-#define TDS_HYST 1            // dense/sparse window choice with hysteresis (HYST_HI / HYST_LO)
-#endif
 #ifndef TDS_HYST_HI
 #define TDS_HYST_HI 50
 #endif
 #ifndef TDS_HYST_LO
 #define TDS_HYST_LO 25
 #endif
-#ifndef TDS_DIRECT_MIN
-#define TDS_DIRECT_MIN 16
-#endif
 constexpr int HYST_HI = TDS_HYST_HI, HYST_LO = TDS_HYST_LO;
-constexpr unsigned long long PROBE_MIN_PAIRS = 1ull << 28;   // density probe only above this many pair tests   // % of a window's pairs passing the filter
-constexpr int DIRECT_MIN = TDS_DIRECT_MIN;  // filter passes per 64-candidate window for the in-place path
+constexpr unsigned long long CAP_PROBE_MIN = 1ull << 24;     // result-size probe above this many pair tests
+constexpr uint64_t CAP_FLOOR = 1ull << 22;                   // records: floor of the probed capacity
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
 constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
@@ -353,92 +344,6 @@ __device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t
     return (in_ok && out_ok) ? 2 : 1;
 }
 
-// hit_kind<true> for two candidates at once (dense windows): the same arithmetic
-// and the same first-order bound per candidate, with the elementwise work in
-// packed fp32x2 and no early exits (both candidates are resolved together).
-// Returns the kinds through k0 / k1 (0 = miss, 1 = fp64, 2 = certain hit).
-__device__ __forceinline__ void hit_kind2(float4 q0, float4 q1, float t0c, float t1c, const ECand &e0, const ECand &e1,
-                                          float d, int &k0, float &tin0, float &tout0, int &k1, float &tin1,
-                                          float &tout1) {
-    constexpr float U = 1.0f / 16777216.0f;
-    const float a0 = fmaxf(t0c, e0.t0), b0 = fminf(t1c, e0.t1);
-    const float a1 = fmaxf(t0c, e1.t0), b1 = fminf(t1c, e1.t1);
-    const f32x2 a = pk2(a0, a1), et0 = pk2(e0.t0, e1.t0);
-    const f32x2 aq = sub2(a, bc2(q0.w)), nae = sub2(et0, a);          // a - t0q, -(a - t0e) (exact negation)
-    const f32x2 dpx = sub2(bc2(q0.x), pk2(e0.px, e1.px)), dpy = sub2(bc2(q0.y), pk2(e0.py, e1.py)),
-                dpz = sub2(bc2(q0.z), pk2(e0.pz, e1.pz));
-    const f32x2 evx = pk2(e0.vx, e1.vx), evy = pk2(e0.vy, e1.vy), evz = pk2(e0.vz, e1.vz);
-    const f32x2 Dx = fma2(nae, evx, fma2(aq, bc2(q1.x), dpx));
-    const f32x2 Dy = fma2(nae, evy, fma2(aq, bc2(q1.y), dpy));
-    const f32x2 Dz = fma2(nae, evz, fma2(aq, bc2(q1.z), dpz));
-    const f32x2 Vx = sub2(bc2(q1.x), evx), Vy = sub2(bc2(q1.y), evy), Vz = sub2(bc2(q1.z), evz);
-    const f32x2 L = sub2(pk2(b0, b1), a);
-    const f32x2 A = fma2(Vx, Vx, fma2(Vy, Vy, mul2(Vz, Vz)));
-    const f32x2 B = fma2(Dx, Vx, fma2(Dy, Vy, mul2(Dz, Vz)));
-    float A0, A1, L0, L1, P0, P1;
-    upk2(A, A0, A1);
-    upk2(L, L0, L1);
-    const float rA0 = rcp_approx(A0), rA1 = rcp_approx(A1);
-    const f32x2 rA = pk2(rA0, rA1);
-    upk2(mul2(B, rA), P0, P1);
-    const float su0 = -P0, su1 = -P1;
-    const f32x2 su = pk2(su0, su1);
-    const f32x2 s = pk2(fminf(fmaxf(su0, 0.f), L0), fminf(fmaxf(su1, 0.f), L1));
-    const f32x2 yx = fma2(s, Vx, Dx), yy = fma2(s, Vy, Dy), yz = fma2(s, Vz, Dz);
-    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
-    float x0, x1, y0, y1, z0, z1;
-    upk2(dpx, x0, x1);
-    upk2(dpy, y0, y1);
-    upk2(dpz, z0, z1);
-    const f32x2 M = add2(pk2(fabsf(x0) + fabsf(y0) + fabsf(z0), fabsf(x1) + fabsf(y1) + fabsf(z1)),
-                         add2(bc2(q1.w), pk2(e0.ext, e1.ext)));
-    const f32x2 thr = fma2(bc2(KU), M, bc2(d));
-    const f32x2 dl = fma2(bc2(-KU), M, bc2(d));
-    float h0, h1, th0, th1, dl0, dl1;
-    upk2(h, h0, h1);
-    upk2(mul2(thr, thr), th0, th1);
-    upk2(dl, dl0, dl1);
-    const bool pass0 = (a0 < b0) & (h0 <= th0), pass1 = (a1 < b1) & (h1 <= th1);
-    const bool cert0 = (dl0 > 0.f) & (h0 < dl0 * dl0), cert1 = (dl1 > 0.f) & (h1 < dl1 * dl1);
-    // interval and its bound (as hit_kind)
-    const f32x2 ux = fma2(su, Vx, Dx), uy = fma2(su, Vy, Dy), uz = fma2(su, Vz, Dz);
-    const f32x2 hu = fma2(ux, ux, fma2(uy, uy, mul2(uz, uz)));
-    const float d2 = d * d;
-    float r0, r1;
-    upk2(sub2(bc2(d2), hu), r0, r1);
-    const f32x2 rem = pk2(fmaxf(r0, 0.f), fmaxf(r1, 0.f));
-    float wq0, wq1;
-    upk2(mul2(rem, rA), wq0, wq1);
-    const f32x2 w = pk2(sqrt_approx(wq0), sqrt_approx(wq1));
-    const f32x2 V1 = pk2(fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e0.vx) + fabsf(e0.vy) + fabsf(e0.vz),
-                         fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e1.vx) + fabsf(e1.vy) + fabsf(e1.vz));
-    const f32x2 rsA = pk2(rsqrt_approx(A0), rsqrt_approx(A1));
-    const f32x2 asu = pk2(fabsf(su0), fabsf(su1));
-    const f32x2 Su = pk2(fmaxf(fabsf(su0), L0), fmaxf(fabsf(su1), L1));
-    const f32x2 Mu = fma2(Su, V1, M);
-    const f32x2 relA = fma2(mul2(bc2(12.f * U), V1), rsA, bc2(5.f * U));
-    const f32x2 dsu = fma2(asu, relA, fma2(mul2(mul2(bc2(6.f * U), V1), Mu), rA, mul2(mul2(bc2(14.f * U), Mu), rsA)));
-    const f32x2 drem = fma2(bc2(2.f * U), add2(bc2(d2), rem), fma2(mul2(A, dsu), dsu, mul2(bc2(28.f * U * d), Mu)));
-    float rm0, rm1;
-    upk2(rem, rm0, rm1);
-    const f32x2 rr = pk2(rcp_approx(rm0), rcp_approx(rm1));
-    const f32x2 dw = mul2(w, add2(fma2(mul2(bc2(0.5f), drem), rr, mul2(bc2(0.5f), relA)), bc2(4.f * U)));
-    const f32x2 dst = fma2(bc2(U), add2(asu, w), mul2(bc2(2.f), add2(dsu, dw)));   // as hit_kind
-    float w0, w1, ds0, ds1;
-    upk2(w, w0, w1);
-    upk2(dst, ds0, ds1);
-    const float lo0 = su0 - w0, hi0 = su0 + w0, lo1 = su1 - w1, hi1 = su1 + w1;
-    tin0 = a0 + fminf(fmaxf(lo0, 0.f), L0);
-    tout0 = a0 + fminf(fmaxf(hi0, 0.f), L0);
-    tin1 = a1 + fminf(fmaxf(lo1, 0.f), L1);
-    tout1 = a1 + fminf(fmaxf(hi1, 0.f), L1);
-    const float tol0 = (8e-6f) * L0, tol1 = (8e-6f) * L1;
-    const bool ok0 = ((lo0 + ds0 < 0.f) | (ds0 <= tol0)) & ((hi0 - ds0 > L0) | (ds0 <= tol0));
-    const bool ok1 = ((lo1 + ds1 < 0.f) | (ds1 <= tol1)) & ((hi1 - ds1 > L1) | (ds1 <= tol1));
-    k0 = pass0 ? ((cert0 & ok0) ? 2 : 1) : 0;
-    k1 = pass1 ? ((cert1 & ok1) ? 2 : 1) : 0;
-}
-
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
 // the sublevel interval of the convex quadratic ||Pq(t)-Pe(t)||^2 <= d^2 on [a,b].
 __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 eb, double d, double T0, double T1,
@@ -479,6 +384,62 @@ __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 e
     t_in = (float)(a + lo);
     t_out = (float)(a + hi);
     return true;
+}
+
+// Refine one queued pair in the relative form (P(t) = P0 + (t - t0) v) with
+// first-order error bounds evaluated from the pair's own magnitudes (DESIGN.md
+// §5 "refine"): 0 = miss, 1 = undecided (fp64), 2 = certain hit with an fp32
+// interval within 8e-6 (b - a) of the exact one.  dlo / dhi: d rounded down / up.
+__device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float t1c, float4 e0, float t1e, float vex,
+                                          float vey, float vez, float dlo, float dhi, float &tin, float &tout) {
+    constexpr float U = 1.0f / 16777216.0f;
+    const float a = fmaxf(t0c, e0.w), b = fminf(t1c, t1e);
+    if (!(a < b)) return 0;                                    // C5
+    const float L = b - a, aq = a - q0.w, ae = a - e0.w;
+    const float dpx = q0.x - e0.x, dpy = q0.y - e0.y, dpz = q0.z - e0.z;
+    const float Dx = fmaf(-ae, vex, fmaf(aq, q1.x, dpx));
+    const float Dy = fmaf(-ae, vey, fmaf(aq, q1.y, dpy));
+    const float Dz = fmaf(-ae, vez, fmaf(aq, q1.z, dpz));
+    const float Vx = q1.x - vex, Vy = q1.y - vey, Vz = q1.z - vez;
+    // position error over the span: eD at s = 0 (roundings of dp, a - t0, the
+    // velocities (<= 4u each) and the two FMAs), eV per unit s (velocities and V)
+    const float V1e = fabsf(vex) + fabsf(vey) + fabsf(vez);
+    const float D1 = fabsf(Dx) + fabsf(Dy) + fabsf(Dz), W1 = fabsf(Vx) + fabsf(Vy) + fabsf(Vz);
+    const float eD = U * fmaf(7.f, fabsf(aq) * q1.w + fabsf(ae) * V1e, fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + 2.f * D1);
+    const float eV = U * fmaf(5.f, q1.w + V1e, W1);
+    const float eP = 1.5f * fmaf(L, eV, eD);                   // x1.5 on the first-order bound
+    const float mg = fmaf(4.f * U, dhi, eP);                   // + rounding of the squared norms
+    const float din = dlo - mg, dout = dhi + mg;
+    // both span ends certainly within d: the whole span (convexity)
+    const float ybx = fmaf(L, Vx, Dx), yby = fmaf(L, Vy, Dy), ybz = fmaf(L, Vz, Dz);
+    const float ha = fmaf(Dx, Dx, fmaf(Dy, Dy, Dz * Dz)), hb = fmaf(ybx, ybx, fmaf(yby, yby, ybz * ybz));
+    const float din2 = din * din;
+    if (din > 0.f && ha < din2 && hb < din2) { tin = a; tout = b; return 2; }
+    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
+    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
+    const float rA = rcp_approx(A);
+    const float su = -B * rA;
+    const float s = fminf(fmaxf(su, 0.f), L);
+    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
+    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
+    if (!(h <= dout * dout)) return 0;                         // certain miss
+    if (!(din > 0.f && h < din2)) return 1;                    // near the threshold
+    const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
+    const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
+    const float rem = fmaxf(fmaf(dhi, dhi, -hu), 0.f);
+    const float w = sqrt_approx(rem * rA);
+    const float lo = su - w, hi = su + w;
+    // error of the unclamped ends: root sensitivity d eP / (A w) to the position
+    // error, + roundings of h_u and d^2, of B (3u |D|_1 |V|_1 / A), of s_u and w
+    const float dlt = fmaf(U, fabsf(su) + w,
+                           1.5f * fmaf(fmaf(dhi, eP, (4.5f * U) * dhi * dhi), rcp_approx(A * w),
+                                       fmaf((3.f * U) * D1 * W1, rA, U * fmaf(7.f, fabsf(su), 5.f * w))));
+    tin = a + fminf(fmaxf(lo, 0.f), L);
+    tout = a + fminf(fmaxf(hi, 0.f), L);
+    const float tol = 8e-6f * L;
+    const bool in_ok = (lo + dlt < 0.f) || (dlt <= tol);
+    const bool out_ok = (hi - dlt > L) || (dlt <= tol);
+    return (in_ok && out_ok) ? 2 : 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -649,6 +610,7 @@ struct PairCtx {                     // what the fp64 path needs
     float d, T0, T1;                 // d: the threshold rounded up to float (fp32 paths)
     OutArgs o;
     double d64;                      // the caller's threshold (fp64 path)
+    float dlo;                       // d rounded down to float (certain-hit tests of refine_rel)
 };
 
 // Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
@@ -706,8 +668,10 @@ __device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uin
             const float4 qa = __ldg(C->Q + 2 * (uint64_t)q), qb = __ldg(C->Q + 2 * (uint64_t)q + 1);
             const float4 ea = __ldg(C->rec + 2 * (uint64_t)j), eb = __ldg(C->rec + 2 * (uint64_t)j + 1);
             const QConst qc = make_qconst(qa, qb, C->T0, C->T1);
-            k = hit_kind(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext), qc.t0c,
-                         qc.t1c, make_ecand(ea, eb), C->d, tin, tout);   // k == 0: no shared span
+            const ECand e = make_ecand(ea, eb);
+            k = refine_rel(make_float4(qc.px, qc.py, qc.pz, qc.t0),
+                           make_float4(qc.vx, qc.vy, qc.vz, fabsf(qc.vx) + fabsf(qc.vy) + fabsf(qc.vz)), qc.t0c, qc.t1c,
+                           make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, C->dlo, C->d, tin, tout);
         }
     }
     const bool hit = (k == 2), need64 = (k == 1);
@@ -1007,48 +971,10 @@ inline float filter_threshold(float d) {
     return df;
 }
 
-// Pairs of query qid that passed the fp32 filter (lane's candidates j0, j1):
-// certain hits with an accurate fp32 interval are appended; the rest is queued
-// for fp64.  Out of line: the hit path must not cost the pair loop registers.
-// Returns the number of hits appended here.
-template <bool EXACT>
-__device__ __forceinline__ uint32_t handle_passed(const PairCtx *C, WarpState *W, uint32_t *qn_io, bool m0, bool m1,
-                                               float4 q0, float4 q1, float t0c, float t1c, uint32_t qid, uint32_t j0,
-                                               uint32_t j1, const ECand &e0, const ECand &e1) {
-    const int lane = threadIdx.x & 31;
-    const float d = C->d;
-    float ti0 = 0.f, to0 = 0.f, ti1 = 0.f, to1 = 0.f;
-    int k0 = 0, k1 = 0;
-    if (m0) k0 = hit_kind(q0, q1, t0c, t1c, e0, d, ti0, to0);
-    if (m1) k1 = hit_kind(q0, q1, t0c, t1c, e1, d, ti1, to1);
-    uint32_t hits = 0;
-    const unsigned hm0 = __ballot_sync(FULL, k0 == 2), hm1 = __ballot_sync(FULL, k1 == 2);
-    if (hm0 | hm1) {
-        append2<EXACT>(C->o, *W, k0 == 2, k1 == 2, hm0, hm1, Rec{qid, k0 == 2 ? __ldg(C->perm + j0) : 0u, ti0, to0},
-                       Rec{qid, k1 == 2 ? __ldg(C->perm + j1) : 0u, ti1, to1}, lane);
-        hits = __popc(hm0) + __popc(hm1);
-    }
-    uint32_t qn = *qn_io;
-    queue_add(*W, qn, k0 == 1, qid | F64_FLAG, j0, lane);      // known undecided: straight to fp64
-    queue_add(*W, qn, k1 == 1, qid | F64_FLAG, j1, lane);
-    queue_drain<EXACT>(C, *W, qn, lane);
-    __syncwarp();
-    if (lane == 0) *qn_io = qn;
-    __syncwarp();
-    return hits;
-}
-
-struct __align__(16) RangeWarpSmem {
-    float4 q[32][6];                 // group query constants: (p0,t0) (v,ext) (t0c,t1c,lo,hi)
-                                     // and the absolute form (c,m) (v,t0c') (t1c',lo,hi,-)
-    WarpState ws;
-    uint32_t qn;                     // refine queue fill
-};
-
-// Density probe (per search, before the pair kernel): the fraction of filter
-// passes on up to 64 sampled schedule entries x 128 candidates from the middle of
-// their ranges, with the relative-form filter; decides whether the dense-heavy
-// D4 instantiation of k_pair_range runs.  One warp per sampled entry.
+// Result-size probe of a range search (per search, before the pair kernel): the
+// fraction of filter passes on sampled schedule entries (one warp each, spread
+// over the sorted schedule) x 128 candidates from the middle of their ranges,
+// with the relative-form filter; sizes the automatic pass buffer.
 __global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const float4 *__restrict__ Q,
                                 const float4 *__restrict__ rec, const uint32_t *__restrict__ arr0,
                                 const uint32_t *__restrict__ arr1, const uint32_t *__restrict__ arr2, float d, float T0,
@@ -1064,10 +990,11 @@ __global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const f
     const QConst qc = make_qconst(__ldg(Q + 2 * (uint64_t)e.qid), __ldg(Q + 2 * (uint64_t)e.qid + 1), T0, T1);
     const float4 q0 = make_float4(qc.px, qc.py, qc.pz, qc.t0), q1 = make_float4(qc.vx, qc.vy, qc.vz, qc.ext);
     const uint32_t len = e.hi - e.lo, m = min(len, 128u);
-    const uint32_t c0 = e.lo + (len - m) / 2;
     uint32_t pass = 0;
     for (uint32_t k = lane; k < m; k += 32) {
-        const uint32_t c = c0 + k, j = arr ? __ldg(arr + c) : c;
+        // spread over the whole range (a contiguous block of an id-ordered range
+        // can be unrepresentative, e.g. the boundary between two clusters)
+        const uint32_t c = e.lo + (uint32_t)(((uint64_t)k * len) / m), j = arr ? __ldg(arr + c) : c;
         const ECand ec = make_ecand(__ldg(rec + 2 * (uint64_t)j), __ldg(rec + 2 * (uint64_t)j + 1));
         pass += filter_pair(q0, q1, qc.t0c, qc.t1c, ec, d) ? 1u : 0u;
     }
@@ -1079,18 +1006,126 @@ __global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const f
     }
 }
 
+struct __align__(16) RangeWarpSmem {
+    float4 q[32][6];                 // group query slot g: (p0, t0) (v, |v|_1) (t0c, t1c, |p1 - p0|_1, -)
+                                     // and the absolute form (c, m) (v, t0c') (t1c', lo, hi, qid)
+    WarpState ws;                    // append chunk, refine queue (slot g, sorted position j), fp64 queue
+    uint32_t cnt[32];                // records of slot g found by the refine path in this work item
+    uint32_t qn;                     // refine queue fill
+};
+
+// Evaluate refine-queue entries [base, base + n), n <= 32 (lane k takes entry
+// k): (slot g, sorted entry position j) -> refine_rel with the query's terms from
+// shared memory; certain hits are appended, undecided pairs go to the fp64 queue.
+template <bool EXACT>
+__device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, uint32_t n, uint32_t base) {
+    const int lane = threadIdx.x & 31;
+    const bool v = (uint32_t)lane < n;
+    const uint32_t g = v ? W->ws.rq[base + lane] : 0u, j = v ? W->ws.rj[base + lane] : 0u;
+    __syncwarp();                    // queue slots read: later queue additions may reuse them
+    float tin = 0.f, tout = 0.f;
+    int k = 0;
+    uint32_t qid = 0;
+    if (v) {
+        const float4 q0 = W->q[g][0], q1 = W->q[g][1], q2 = W->q[g][2];
+        qid = __float_as_uint(W->q[g][5].w);
+        const ECand e = make_ecand(__ldg(A->pc.rec + 2 * (uint64_t)j), __ldg(A->pc.rec + 2 * (uint64_t)j + 1));
+        k = refine_rel(q0, q1, q2.x, q2.y, make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, A->pc.dlo,
+                       A->pc.d, tin, tout);
+    }
+    const bool hit = (k == 2), need64 = (k == 1);
+    const Rec r{qid, hit ? __ldg(A->pc.perm + j) : 0u, tin, tout};
+    append<EXACT>(A->pc.o, W->ws, hit, r, lane);
+    if (hit) atomicAdd(&W->cnt[g], 1u);
+    const unsigned hm = __ballot_sync(FULL, hit), m64 = __ballot_sync(FULL, need64);
+    const uint32_t fn = W->ws.fn;
+    if (need64) {
+        const uint32_t pos = fn + __popc(m64 & ((1u << lane) - 1u));
+        W->ws.fq[pos] = qid;
+        W->ws.fj[pos] = j;
+    }
+    __syncwarp();
+    if (lane == 0) { W->ws.hits += __popc(hm); W->ws.fn = fn + __popc(m64); }
+    __syncwarp();
+    if (fn + __popc(m64) >= 32) flush64<EXACT>(&A->pc, &W->ws, 32);
+}
+
+// warp-wide: evaluate the newest 32 queued pairs while >= 32 are queued
+template <bool EXACT>
+__device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W, uint32_t &qn) {
+    while (qn >= 32) {
+        __syncwarp();
+        qn -= 32;
+        range_refine<EXACT>(A, &W, 32, qn);
+    }
+}
+
+// Dense windows: for the lane's two candidates against query slot g, in the
+// relative form: in0/in1 = both span ends certainly within d (then the whole
+// shared span [a, b] is within d: the squared distance is convex in t; the
+// pair's interval is exactly [a, b]), ps0/ps1 = the closest approach passes the
+// filter.  Certainty margin KU M, M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e -
+// p0e|_1 (the relative-form bound of DESIGN.md §5 holds at every point of the
+// span, so at both ends).  Packed FP32x2 per candidate pair.
+__device__ __forceinline__ void dense_test2(float4 q0, float4 q1, float4 q2, const ECand &e0, const ECand &e1, float d,
+                                            bool &in0, bool &in1, bool &ps0, bool &ps1, float &a0, float &b0,
+                                            float &a1, float &b1) {
+    a0 = fmaxf(q2.x, e0.t0); b0 = fminf(q2.y, e0.t1);
+    a1 = fmaxf(q2.x, e1.t0); b1 = fminf(q2.y, e1.t1);
+    const f32x2 a = pk2(a0, a1);
+    const f32x2 L = sub2(pk2(b0, b1), a);
+    const f32x2 aq = sub2(a, bc2(q0.w)), nae = sub2(pk2(e0.t0, e1.t0), a);
+    const f32x2 dpx = sub2(bc2(q0.x), pk2(e0.px, e1.px)), dpy = sub2(bc2(q0.y), pk2(e0.py, e1.py)),
+                dpz = sub2(bc2(q0.z), pk2(e0.pz, e1.pz));
+    const f32x2 evx = pk2(e0.vx, e1.vx), evy = pk2(e0.vy, e1.vy), evz = pk2(e0.vz, e1.vz);
+    const f32x2 Dx = fma2(nae, evx, fma2(aq, bc2(q1.x), dpx));
+    const f32x2 Dy = fma2(nae, evy, fma2(aq, bc2(q1.y), dpy));
+    const f32x2 Dz = fma2(nae, evz, fma2(aq, bc2(q1.z), dpz));
+    const f32x2 Vx = sub2(bc2(q1.x), evx), Vy = sub2(bc2(q1.y), evy), Vz = sub2(bc2(q1.z), evz);
+    const f32x2 ybx = fma2(L, Vx, Dx), yby = fma2(L, Vy, Dy), ybz = fma2(L, Vz, Dz);
+    const f32x2 ha = fma2(Dx, Dx, fma2(Dy, Dy, mul2(Dz, Dz)));
+    const f32x2 hb = fma2(ybx, ybx, fma2(yby, yby, mul2(ybz, ybz)));
+    float x0, x1, y0, y1, z0, z1;
+    upk2(dpx, x0, x1);
+    upk2(dpy, y0, y1);
+    upk2(dpz, z0, z1);
+    const f32x2 M = add2(pk2(fabsf(x0) + fabsf(y0) + fabsf(z0), fabsf(x1) + fabsf(y1) + fabsf(z1)),
+                         add2(bc2(q2.z), pk2(e0.ext, e1.ext)));
+    const f32x2 thr = fma2(bc2(KU), M, bc2(d)), dl = fma2(bc2(-KU), M, bc2(d));
+    const f32x2 A = fma2(Vx, Vx, fma2(Vy, Vy, mul2(Vz, Vz)));
+    const f32x2 B = fma2(Dx, Vx, fma2(Dy, Vy, mul2(Dz, Vz)));
+    float A0, A1, L0, L1, u0, u1;
+    upk2(A, A0, A1);
+    upk2(L, L0, L1);
+    upk2(mul2(B, pk2(rcp_approx(A0), rcp_approx(A1))), u0, u1);
+    const f32x2 sv = pk2(fminf(fmaxf(-u0, 0.f), L0), fminf(fmaxf(-u1, 0.f), L1));
+    const f32x2 yx = fma2(sv, Vx, Dx), yy = fma2(sv, Vy, Dy), yz = fma2(sv, Vz, Dz);
+    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
+    float ha0, ha1, hb0, hb1, h0, h1, t0, t1, l0, l1, dl0, dl1;
+    upk2(ha, ha0, ha1);
+    upk2(hb, hb0, hb1);
+    upk2(h, h0, h1);
+    upk2(mul2(thr, thr), t0, t1);
+    upk2(mul2(dl, dl), l0, l1);
+    upk2(dl, dl0, dl1);
+    in0 = (a0 < b0) & (dl0 > 0.f) & (ha0 < l0) & (hb0 < l0);
+    in1 = (a1 < b1) & (dl1 > 0.f) & (ha1 < l1) & (hb1 < l1);
+    ps0 = (a0 < b0) & (h0 <= t0);
+    ps1 = (a1 < b1) & (h1 <= t1);
+}
+
 // Mapping: a work item is a group of <= 32
 // consecutive schedule entries (one category) and a chunk of the union of their
-// candidate ranges.  Lane g owns query g of the group (its constants are staged
-// in shared memory); the warp then walks the chunk 32 candidates at a time with
-// lane = candidate.  A ballot over the owners gives the queries whose range
-// meets the current 32 candidates, so each loaded candidate is tested against
-// every query that needs it and gaps between ranges are skipped.  Pairs that
-// pass the fp32 filter are queued and evaluated 32 at a time in fp64.
-// D4: the dense-window step takes four candidates per query (two hit_kind2
-// chains); its registers slow the sparse loop, so it is a separate instantiation
-// chosen per search by the density probe (k_density_probe).
-template <bool EXACT, bool D4 = false>
+// candidate ranges.  Lane g owns query slot g of the group (its constants are
+// staged in shared memory); the warp walks the chunk 128 candidates at a time
+// with lane = candidate (4 per lane).  A ballot over the owners gives the
+// queries whose range meets the window, so each loaded candidate is tested
+// against every query that needs it and gaps between ranges are skipped.
+// Sparse windows: the absolute-form filter (packed, two chains); passes are
+// queued (slot, candidate) and evaluated 32 at a time by range_refine.  Dense
+// windows (hysteresis on the window's pass fraction): the fused relative-form
+// step dense_test2 appends whole-span hits at once and queues the rest.
+template <bool EXACT>
 __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_constant__ RangeArgs A) {
     __shared__ RangeWarpSmem sm[PT / 32];
     const int lane = threadIdx.x & 31;
@@ -1101,10 +1136,11 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     const float d = A.pc.d;
     const float df = A.df;
     warp_state_init(W.ws, lane);
-    if (lane == 0) W.qn = 0;
+    W.cnt[lane] = 0;
+    uint32_t qn = 0;                         // refine queue fill (warp-uniform)
     __syncwarp();
     unsigned long long exec = 0, direct_hits = 0;
-    bool dense = false;                      // warp-uniform: last filtered window was output-bound
+    bool dense = false;                      // warp-uniform: the last window was hit-heavy
     while (true) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
@@ -1119,7 +1155,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         const uint32_t chunk = item - A.item_start[lo];
         const uint32_t c_lo = T.ulo + chunk * CH;
         const uint32_t c_hi = min(c_lo + CH, T.uhi);
-        // ---- owner side: lane g stages query g of the group
+        // ---- owner side: lane g stages query slot g of the group
         const uint32_t p = T.tb + lane;
         const bool active = p < T.te;
         Sched S{0, 0, 0, 3};
@@ -1133,11 +1169,12 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             const FSeg qf = make_fseg(qa, qb, A.tc);
             __syncwarp();
             W.q[lane][0] = make_float4(qc.px, qc.py, qc.pz, qc.t0);
-            W.q[lane][1] = make_float4(qc.vx, qc.vy, qc.vz, qc.ext);
-            W.q[lane][2] = make_float4(qc.t0c, qc.t1c, __uint_as_float(my_lo), __uint_as_float(my_hi));
+            W.q[lane][1] = make_float4(qc.vx, qc.vy, qc.vz, fabsf(qc.vx) + fabsf(qc.vy) + fabsf(qc.vz));
+            W.q[lane][2] = make_float4(qc.t0c, qc.t1c, qc.ext, 0.f);
             W.q[lane][3] = make_float4(qf.cx, qf.cy, qf.cz, qf.m);
             W.q[lane][4] = make_float4(qf.vx, qf.vy, qf.vz, qc.t0c - A.tc);
-            W.q[lane][5] = make_float4(qc.t1c - A.tc, __uint_as_float(my_lo), __uint_as_float(my_hi), 0.f);
+            W.q[lane][5] = make_float4(qc.t1c - A.tc, __uint_as_float(my_lo), __uint_as_float(my_hi),
+                                       __uint_as_float(S.qid));
             __syncwarp();
         }
         uint32_t wlo = my_lo, whi = my_hi;
@@ -1147,9 +1184,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             whi = max(whi, __shfl_xor_sync(FULL, whi, o));
         }
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
-        uint32_t owner_hits = 0;             // hits of this lane's query found on the dense path
-        // windows of WIN = 128 candidates: lane handles cand + 32k, k = 0..3, as two
-        // packed pairs (two independent FFMA2 chains per query load)
+        uint32_t owner_hits = 0;             // whole-span hits of this lane's query slot (dense path)
         // records: sorted entries (temporal), the materialised X/Y/Z-ordered copy
         // (TDS_ST_MATERIALISE=1: streamed, independent of the id load), or rec[X[i]]
         const float4 *srec = (T.sel >= 0) ? A.srec[T.sel] : nullptr;
@@ -1163,103 +1198,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 a = __ldg(src);
                 b = __ldg(src + 1);
             }
-        };
-        auto ecand_of = [&](uint32_t j) {
-            return make_ecand(__ldg(A.pc.rec + 2 * (uint64_t)j), __ldg(A.pc.rec + 2 * (uint64_t)j + 1));
-        };
-        // dense-window path for the candidates (ca, cb): fused filter + certain-hit
-        // interval per pair, no recomputation; returns the number of passes
-        auto dense_pair = [&](unsigned mask, uint32_t ca, uint32_t cb, uint32_t cend, uint32_t ja, uint32_t jb) {
-            const ECand ea = ecand_of(ja), eb = ecand_of(jb);
-            const bool va = ca < cend, vb = cb < cend;
-            // entry rows of the lane's two candidates: loaded once per window (not per hit)
-            const uint32_t ida = va ? __ldg(A.pc.perm + ja) : 0u, idb = vb ? __ldg(A.pc.perm + jb) : 0u;
-            uint32_t passes = 0;
-            while (mask) {
-                const int g = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                float tia, toa, tib, tob;
-                int ka, kb;
-                hit_kind2(q0, q1, q2.x, q2.y, ea, eb, d, ka, tia, toa, kb, tib, tob);
-                if (!(va && ca >= glo && ca < ghi)) ka = 0;
-                if (!(vb && cb >= glo && cb < ghi)) kb = 0;
-                const unsigned pa = __ballot_sync(FULL, ka != 0), pb = __ballot_sync(FULL, kb != 0);
-                if (!(pa | pb)) continue;
-                passes += __popc(pa) + __popc(pb);
-                const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                const unsigned hma = __ballot_sync(FULL, ka == 2), hmb = __ballot_sync(FULL, kb == 2);
-                if (hma | hmb) {
-                    const bool h[2] = {ka == 2, kb == 2};
-                    const unsigned hm[2] = {hma, hmb};
-                    const Rec r[2] = {Rec{qid, ida, tia, toa}, Rec{qid, idb, tib, tob}};
-                    appendK<EXACT, 2>(A.pc.o, W.ws, h, hm, r, lane);
-                    const uint32_t hits_g = __popc(hma) + __popc(hmb);
-                    direct_hits += hits_g;
-                    if (lane == g) owner_hits += hits_g;
-                }
-                if ((pa & ~hma) | (pb & ~hmb)) {     // undecided in fp32: known fp64 pairs
-                    uint32_t qn = W.qn;
-                    queue_add(W.ws, qn, ka == 1, qid | F64_FLAG, ja, lane);
-                    queue_add(W.ws, qn, kb == 1, qid | F64_FLAG, jb, lane);
-                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
-                    __syncwarp();
-                    if (lane == 0) W.qn = qn;
-                    __syncwarp();
-                }
-            }
-            return passes;
-        };
-        // dense windows (D4 instantiation): per query, the lane's four candidates as two
-        // independent packed hit_kind2 chains (one chain per query step is latency-bound)
-        auto dense_quad = [&](unsigned mask, uint32_t c0, uint32_t cend, uint32_t j0, uint32_t j1, uint32_t j2,
-                              uint32_t j3) {
-            const ECand e0 = ecand_of(j0), e1 = ecand_of(j1), e2 = ecand_of(j2), e3 = ecand_of(j3);
-            const uint32_t id0 = c0 < cend ? __ldg(A.pc.perm + j0) : 0u, id1 = c0 + 32 < cend ? __ldg(A.pc.perm + j1) : 0u,
-                           id2 = c0 + 64 < cend ? __ldg(A.pc.perm + j2) : 0u, id3 = c0 + 96 < cend ? __ldg(A.pc.perm + j3) : 0u;
-            uint32_t passes = 0;
-            while (mask) {
-                const int g = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                const uint32_t glo = __float_as_uint(q2.z), ghi = __float_as_uint(q2.w);
-                float ti[4], to[4];
-                int kk[4];
-                hit_kind2(q0, q1, q2.x, q2.y, e0, e1, d, kk[0], ti[0], to[0], kk[1], ti[1], to[1]);
-                hit_kind2(q0, q1, q2.x, q2.y, e2, e3, d, kk[2], ti[2], to[2], kk[3], ti[3], to[3]);
-                // slot c valid for query g iff glo <= c < ghi (ghi <= whi) and c < cend
-                const uint32_t gw = ghi - glo, o0 = c0 - glo;
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (!(o0 + 32u * i < gw) || !(c0 + 32u * i < cend)) kk[i] = 0;
-                unsigned pm[4], hm[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) pm[i] = __ballot_sync(FULL, kk[i] != 0);
-                if (!((pm[0] | pm[1]) | (pm[2] | pm[3]))) continue;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) { passes += __popc(pm[i]); hm[i] = __ballot_sync(FULL, kk[i] == 2); }
-                const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                if ((hm[0] | hm[1]) | (hm[2] | hm[3])) {
-                    const bool h[4] = {kk[0] == 2, kk[1] == 2, kk[2] == 2, kk[3] == 2};
-                    const Rec r[4] = {Rec{qid, id0, ti[0], to[0]}, Rec{qid, id1, ti[1], to[1]},
-                                      Rec{qid, id2, ti[2], to[2]}, Rec{qid, id3, ti[3], to[3]}};
-                    appendK<EXACT, 4>(A.pc.o, W.ws, h, hm, r, lane);
-                    const uint32_t hits_g = __popc(hm[0]) + __popc(hm[1]) + __popc(hm[2]) + __popc(hm[3]);
-                    direct_hits += hits_g;
-                    if (lane == g) owner_hits += hits_g;
-                }
-                if (((pm[0] & ~hm[0]) | (pm[1] & ~hm[1])) | ((pm[2] & ~hm[2]) | (pm[3] & ~hm[3]))) {
-                    uint32_t qn = W.qn;          // undecided in fp32: known fp64 pairs
-                    queue_add4(W.ws, qn, kk[0] == 1, kk[1] == 1, kk[2] == 1, kk[3] == 1, qid | F64_FLAG, j0, j1, j2,
-                               j3, lane);
-                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
-                    __syncwarp();
-                    if (lane == 0) W.qn = qn;
-                    __syncwarp();
-                }
-            }
-            return passes;
         };
         uint32_t base = wlo;
         while (base < whi) {
@@ -1277,102 +1215,107 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
             exec += (unsigned long long)(cend - base) * __popc(mask);
-            if (dense) {
-                // output-bound regime (last window was dense)
-                {
-                    float4 a, b;
-                    load_cand(c0, c0 < cend, j0, a, b);
-                    load_cand(c1, c1 < cend, j1, a, b);
-                    load_cand(c2, c2 < cend, j2, a, b);
-                    load_cand(c3, c3 < cend, j3, a, b);
-                }
-                uint32_t passes = 0;
-                if (D4) {
-                    passes = dense_quad(mask, c0, cend, j0, j1, j2, j3);
-                } else {
-#pragma unroll 1
-                    for (int h = 0; h < 2; ++h) {      // one copy of the dense code (i-cache)
-                        if (h && base + 64 >= cend) break;
-                        passes += dense_pair(mask, h ? c2 : c0, h ? c3 : c1, cend, h ? j2 : j0, h ? j3 : j1);
-                    }
-                }
-#if TDS_HYST
-                // stay dense while >= HYST_LO % of the window's (query, slot) pairs pass
-                dense = 100u * passes >= (uint32_t)HYST_LO * __popc(wmask) * (cend - base);
-#else
-                dense = passes >= (uint32_t)DIRECT_MIN * __popc(wmask) * 2u;
-#endif
-                base = cend;
-                continue;
-            }
             uint32_t wpass = 0;                // filter passes of this window (all queries)
-            FSeg2 f01, f23;
-            {
-                float4 a0, b0, a1, b1;
-                load_cand(c0, c0 < cend, j0, a0, b0);
-                load_cand(c1, c1 < cend, j1, a1, b1);
-                f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-                load_cand(c2, c2 < cend, j2, a0, b0);
-                load_cand(c3, c3 < cend, j3, a1, b1);
-                f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-            }
-            while (mask) {
-                const int g = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float4 n0 = W.q[g][3], n1 = W.q[g][4], n2 = W.q[g][5];
-                const uint32_t glo = __float_as_uint(n2.y), ghi = __float_as_uint(n2.z);
-                bool m0, m1, m2, m3;
-                filter_abs2(n0, n1, n1.w, n2.x, f01, df, m0, m1);
-                filter_abs2(n0, n1, n1.w, n2.x, f23, df, m2, m3);
-                // warp-uniform: unless the query's range covers all WIN candidate slots
-                // (then all are valid: ghi <= whi), test each slot against the range
-                // (c < ghi <= whi implies c < cend: no separate validity test)
-                if (glo > base || ghi - base < WIN) {
-                    const uint32_t r0 = c0 - glo, gw = ghi - glo;
-                    m0 &= r0 < gw; m1 &= r0 + 32 < gw; m2 &= r0 + 64 < gw; m3 &= r0 + 96 < gw;
-                }
-                if (!__any_sync(FULL, (m0 | m1) | (m2 | m3))) continue;
-                const uint32_t qid = __shfl_sync(FULL, S.qid, g);
-                const uint32_t npass = __popc(__ballot_sync(FULL, m0)) + __popc(__ballot_sync(FULL, m1)) +
-                                       __popc(__ballot_sync(FULL, m2)) + __popc(__ballot_sync(FULL, m3));
-                wpass += npass;
-                if (!TDS_HYST && npass >= 2u * DIRECT_MIN) {
-                    // dense: most lanes passed -> in place (fp32 interval or fp64 queue); the
-                    // following windows use the fused path.  Candidates are re-read (L1) in
-                    // the relative form the interval needs.
-                    dense = true;
-                    const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2];
-                    uint32_t hits_g = 0;
+            if (dense) {
+                // the window in two halves of 64 candidates (two per lane), each against
+                // every query slot: one copy of the step, two candidate terms live
 #pragma unroll 1
-                    for (int h = 0; h < 2; ++h) {  // one copy of the in-place code (i-cache)
-                        const uint32_t ja = h ? j2 : j0, jb = h ? j3 : j1;
-                        hits_g += handle_passed<EXACT>(&A.pc, &W.ws, &W.qn, h ? m2 : m0, h ? m3 : m1, q0, q1, q2.x,
-                                                       q2.y, qid, ja, jb, ecand_of(ja), ecand_of(jb));
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t ca = c0 + 64u * h, cb = ca + 32u;
+                    if (ca - lane >= cend) break;
+                    uint32_t ja, jb;
+                    float4 a, b;
+                    load_cand(ca, ca < cend, ja, a, b);
+                    const ECand ea = make_ecand(a, b);
+                    load_cand(cb, cb < cend, jb, a, b);
+                    const ECand eb = make_ecand(a, b);
+                    // entry rows, loaded once per window (not per hit)
+                    const uint32_t ida = ca < cend ? __ldg(A.pc.perm + ja) : 0u, idb = cb < cend ? __ldg(A.pc.perm + jb) : 0u;
+                    unsigned m = wmask;
+                    while (m) {
+                        const int g = __ffs(m) - 1;
+                        m &= m - 1;
+                        const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2], q5 = W.q[g][5];
+                        const uint32_t glo = __float_as_uint(q5.y), ghi = __float_as_uint(q5.z);
+                        const uint32_t qid = __float_as_uint(q5.w);
+                        bool in0, in1, ps0, ps1;
+                        float a0, b0, a1, b1;
+                        dense_test2(q0, q1, q2, ea, eb, d, in0, in1, ps0, ps1, a0, b0, a1, b1);
+                        // slot c valid for slot g iff glo <= c < ghi (ghi <= whi) and c < cend
+                        const bool r0 = (ca - glo < ghi - glo) && (ca < cend);
+                        const bool r1 = (cb - glo < ghi - glo) && (cb < cend);
+                        in0 &= r0; in1 &= r1;
+                        ps0 = ps0 & r0 & !in0;
+                        ps1 = ps1 & r1 & !in1;
+                        const unsigned bi0 = __ballot_sync(FULL, in0), bi1 = __ballot_sync(FULL, in1);
+                        const unsigned bp0 = __ballot_sync(FULL, ps0), bp1 = __ballot_sync(FULL, ps1);
+                        wpass += __popc(bi0) + __popc(bi1) + __popc(bp0) + __popc(bp1);
+                        if (bi0 | bi1) {
+                            append2<EXACT>(A.pc.o, W.ws, in0, in1, bi0, bi1, Rec{qid, ida, a0, b0},
+                                           Rec{qid, idb, a1, b1}, lane);
+                            const uint32_t hg = __popc(bi0) + __popc(bi1);
+                            direct_hits += hg;
+                            if (lane == g) owner_hits += hg;
+                        }
+                        if (bp0 | bp1) {
+                            queue_add(W.ws, qn, ps0, (uint32_t)g, ja, lane);
+                            queue_add(W.ws, qn, ps1, (uint32_t)g, jb, lane);
+                            range_drain<EXACT>(&A, W, qn);
+                        }
                     }
-                    direct_hits += hits_g;
-                    if (lane == g) owner_hits += hits_g;
-                } else {
-                    // sparse: queue; the flush evaluates 32 at a time with every lane busy
-                    uint32_t qn = W.qn;
-                    queue_add4(W.ws, qn, m0, m1, m2, m3, qid, j0, j1, j2, j3, lane);
-                    queue_drain<EXACT>(&A.pc, W.ws, qn, lane);
-                    __syncwarp();
-                    if (lane == 0) W.qn = qn;
-                    __syncwarp();
+                }
+            } else {
+                FSeg2 f01, f23;
+                {
+                    float4 a0, b0, a1, b1;
+                    load_cand(c0, c0 < cend, j0, a0, b0);
+                    load_cand(c1, c1 < cend, j1, a1, b1);
+                    f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
+                    load_cand(c2, c2 < cend, j2, a0, b0);
+                    load_cand(c3, c3 < cend, j3, a1, b1);
+                    f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
+                }
+                while (mask) {
+                    const int g = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const float4 n0 = W.q[g][3], n1 = W.q[g][4], n2 = W.q[g][5];
+                    const uint32_t glo = __float_as_uint(n2.y), ghi = __float_as_uint(n2.z);
+                    bool m0, m1, m2, m3;
+                    filter_abs2(n0, n1, n1.w, n2.x, f01, df, m0, m1);
+                    filter_abs2(n0, n1, n1.w, n2.x, f23, df, m2, m3);
+                    // warp-uniform: unless the query's range covers all WIN candidate slots
+                    // (then all are valid: ghi <= whi), test each slot against the range
+                    // (c < ghi <= whi implies c < cend: no separate validity test)
+                    if (glo > base || ghi - base < WIN) {
+                        const uint32_t r0 = c0 - glo, gw = ghi - glo;
+                        m0 &= r0 < gw; m1 &= r0 + 32 < gw; m2 &= r0 + 64 < gw; m3 &= r0 + 96 < gw;
+                    }
+                    if (!__any_sync(FULL, (m0 | m1) | (m2 | m3))) continue;
+                    const uint32_t q0n = qn;
+                    queue_add4(W.ws, qn, m0, m1, m2, m3, (uint32_t)g, j0, j1, j2, j3, lane);
+                    wpass += qn - q0n;
+                    range_drain<EXACT>(&A, W, qn);
                 }
             }
-#if TDS_HYST
-            // switch to the fused dense path once >= HYST_HI % of the window's pairs pass
-            // (two thresholds: a window mix near one threshold toggled between the
-            // paths, and the in-place transition was slower than either)
-            dense = 100u * wpass >= (uint32_t)HYST_HI * __popc(wmask) * (cend - base);
-#endif
+            // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
+            // back to the sparse path below HYST_LO % (hysteresis: a window mix near one
+            // threshold would toggle between the paths)
+            dense = 100u * wpass >= (uint32_t)(dense ? HYST_LO : HYST_HI) * __popc(wmask) * (cend - base);
             base = cend;
         }
-        if (owner_hits) atomicAdd(&A.pc.o.qcount[S.qid], owner_hits);
+        // ---- item end: the queue refers to this group's slots
+        if (qn) {
+            __syncwarp();
+            range_refine<EXACT>(&A, &W, qn, 0);
+            qn = 0;
+        }
+        __syncwarp();
+        const uint32_t cq = owner_hits + W.cnt[lane];
+        W.cnt[lane] = 0;
+        if (active && cq) atomicAdd(&A.pc.o.qcount[S.qid], cq);
+        __syncwarp();
     }
     __syncwarp();
-    if (W.qn) flush_refine<EXACT>(&A.pc, &W.ws, W.qn);
     if (W.ws.fn) flush64<EXACT>(&A.pc, &W.ws, W.ws.fn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
@@ -1396,6 +1339,38 @@ __device__ __forceinline__ void query_box(float4 a, float4 b, float d, const Fsg
         lo[c] = cell_of(__fsub_rd(fminf(p0[c], p1[c]), d), G.o[c], G.w[c], G.g[c]);
         hi[c] = cell_of(__fadd_ru(fmaxf(p0[c], p1[c]), d), G.o[c], G.w[c], G.g[c]);
     }
+}
+
+// GPUSpatial query order (a locality order only; the result set does not
+// depend on it): by t_start, then by the Morton code of the start point's cell,
+// so that warps working at the same time read the same (cell, time) slices and
+// the slices are reused from L2.  Keys for two stable radix sorts (cell first,
+// then t_start).
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {      // 10 bits -> every third bit
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__global__ void k_fsg_order_keys(const float4 *__restrict__ Q, uint32_t n, FsgGrid G, uint32_t *__restrict__ kcell,
+                                 uint32_t *__restrict__ kt, uint32_t *__restrict__ vals) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const float4 a = Q[2 * (uint64_t)p];
+    const uint32_t cx = (uint32_t)cell_of(a.x, G.o[0], G.w[0], G.g[0]), cy = (uint32_t)cell_of(a.y, G.o[1], G.w[1], G.g[1]),
+                   cz = (uint32_t)cell_of(a.z, G.o[2], G.w[2], G.g[2]);
+    kcell[p] = (spread3(cx) << 2) | (spread3(cy) << 1) | spread3(cz);
+    kt[p] = float_key(isfinite(a.w) ? a.w : 0.f);
+    vals[p] = p;
+}
+
+__global__ void k_gather_u32(const uint32_t *__restrict__ src, const uint32_t *__restrict__ idx, uint32_t n,
+                             uint32_t *__restrict__ out) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) out[p] = src[idx[p]];
 }
 
 __global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__restrict__ list, uint32_t n, float d,
@@ -1514,6 +1489,45 @@ __global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t 
     unsigned long long s = base + k * SP_GRAB;
     if (s >= end) s = end > base ? end - 1 : base;
     grab_row[k] = find_row(ss, 0, nrows, s);
+}
+
+// Result-size probe of a GPUSpatial search: the fraction of passing pair tests
+// (relative-form filter + the reference-cell rule) on slots sampled evenly over
+// [s_lo, s_hi), one per thread.
+__global__ void k_density_probe_spatial(const unsigned long long *__restrict__ ss, uint32_t nrows,
+                                        unsigned long long s_lo, unsigned long long s_hi,
+                                        const uint32_t *__restrict__ row_q, const uint32_t *__restrict__ row_alo,
+                                        const uint32_t *__restrict__ row_cxy, const int4 *__restrict__ qbox,
+                                        const uint32_t *__restrict__ ecell, const float4 *__restrict__ Q,
+                                        const float4 *__restrict__ frec, float d, float T0, float T1, DevStats *st) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    const unsigned long long n = s_hi - s_lo;
+    uint32_t pass = 0, tot = 0;
+    if (n) {
+        const unsigned long long sl = s_lo + (unsigned long long)(((unsigned __int128)n * (2 * t + 1)) / (2ull * nt));
+        const uint32_t r = find_row(ss, 0, nrows, sl);
+        const uint32_t i = row_alo[r] + (uint32_t)(sl - ss[r]);
+        const int4 qlo = qbox[2 * row_q[r]];
+        const uint32_t m0 = ecell[i];
+        const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
+        const int rz = max((int)(m0 & 0x3ffu), qlo.z);
+        tot = 1;
+        if (pack_cell(rx, ry, rz) == row_cxy[r]) {
+            const QConst qc = make_qconst(__ldg(Q + 2 * (uint64_t)qlo.w), __ldg(Q + 2 * (uint64_t)qlo.w + 1), T0, T1);
+            pass = filter_pair(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext),
+                               qc.t0c, qc.t1c, make_ecand(__ldg(frec + 2 * (uint64_t)i), __ldg(frec + 2 * (uint64_t)i + 1)),
+                               d) ? 1u : 0u;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        pass += __shfl_xor_sync(FULL, pass, o);
+        tot += __shfl_xor_sync(FULL, tot, o);
+    }
+    if ((threadIdx.x & 31) == 0 && tot) {
+        atomicAdd(&st->probe_pass, pass);
+        atomicAdd(&st->probe_total, tot);
+    }
 }
 
 // lane = candidate slot of the flattened (query, cell row) work list; warps grab
@@ -1915,6 +1929,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // caller's d); the fp64 evaluation uses the caller's d exactly
     float d = (float)d64;
     if ((double)d < d64) d = nextafterf(d, INFINITY);
+    float dlo = (float)d64;                               // rounded down (certain-hit tests)
+    if ((double)dlo > d64) dlo = nextafterf(dlo, 0.f);
     tds_stats &S = res->stats;
     memset(&S, 0, sizeof S);
     res->stream = s;
@@ -1961,6 +1977,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     DBuf<int4> qbox;
     DBuf<uint32_t> row_start, row_q, row_alo, row_len, row_cxy;
     DBuf<unsigned long long> slot_start;
+    DBuf<uint32_t> fsg_order;          // GPUSpatial query order (rows of Q)
     uint32_t nrows = 0;
     if (!spatial) {
         sched = DBuf<Sched>(n, s);
@@ -2054,7 +2071,16 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         DBuf<unsigned long long> ntot(1, s);
         TDS_CUDA(cudaMemsetAsync(nr.p + n, 0, 4, s));
         TDS_CUDA(cudaMemsetAsync(ntot.p, 0, 8, s));
-        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, nullptr, n, d, T0, T1, G, nr.p, qbox.p, ntot.p, &dst.p->bad);
+        // query order: (t_start, Morton cell of the start point), for L2 reuse of the slices
+        DBuf<uint32_t> kc(n, s), kt(n, s), kt2(n, s);
+        fsg_order = DBuf<uint32_t>(n, s);
+        k_fsg_order_keys<<<nblk(n), 256, 0, s>>>(Q, n, G, kc.p, kt.p, fsg_order.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(kc.p, fsg_order.p, n, 0, 30, s);
+        k_gather_u32<<<nblk(n), 256, 0, s>>>(kt.p, fsg_order.p, n, kt2.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(kt2.p, fsg_order.p, n, 0, 32, s);
+        k_fsg_count<<<nblk(n), 256, 0, s>>>(Q, fsg_order.p, n, d, T0, T1, G, nr.p, qbox.p, ntot.p, &dst.p->bad);
         TDS_CHECK_LAUNCH();
         exclusive_scan_u32(nr.p, row_start.p, n + 1, nullptr, s);
         unsigned long long items64 = 0;
@@ -2106,23 +2132,32 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             S.n_queries = std::min(hs.part_hi, live) > hs.part_lo ? std::min(hs.part_hi, live) - hs.part_lo : 0;
         }
     }
-    // density probe, on large range searches only (one small kernel + a read-back):
-    // dense-heavy searches (>= HYST_HI % of the probed pairs pass the filter) run the
-    // four-candidate dense step (the D4 instantiation of k_pair_range)
-    // TDS_DENSE4 (environment) = 0 / 1 overrides the build default (tests, ablation)
-    const int d4_mode = [] {
-        const char *e = getenv("TDS_DENSE4");
-        return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : TDS_DENSE4;
-    }();
-    bool d4 = !spatial && d4_mode == 1;
-    if (!spatial && d4_mode == 2 && hs.pair_tests >= PROBE_MIN_PAIRS) {
-        k_density_probe<<<8, 256, 0, s>>>(sched.p, n, Q, idx->rec, idx->st_arr[0], idx->st_arr[1], idx->st_arr[2], d,
-                                          T0, T1, dst.p);
+    // result-size probe (automatic capacity, large searches): the pass fraction of a
+    // sample of the pair tests bounds the result count; the pass buffer takes three
+    // times the estimate (a pass that overflows re-plans exactly, C22) instead of one
+    // slot per pair test, which on hit-sparse searches meant a buffer 10-40x the
+    // result and a compaction copy after the pass
+    uint64_t est_hits = 0;
+    bool probed = false;
+    const unsigned long long probe_pairs = spatial ? slot_hi - slot_lo : hs.pair_tests;
+    if (capacity == 0 && probe_pairs >= CAP_PROBE_MIN) {
+        TDS_CUDA(cudaMemsetAsync(&dst.p->probe_pass, 0, 8, s));
+        if (!spatial) {
+            k_density_probe<<<32, 256, 0, s>>>(sched.p, n, Q, idx->rec, idx->st_arr[0], idx->st_arr[1],
+                                               idx->st_arr[2], d, T0, T1, dst.p);
+        } else {
+            k_density_probe_spatial<<<32, 256, 0, s>>>(slot_start.p, nrows, slot_lo, slot_hi, row_q.p, row_alo.p,
+                                                       row_cxy.p, qbox.p, idx->fsg_ecell, Q, idx->fsg_rec, d, T0, T1,
+                                                       dst.p);
+        }
         TDS_CHECK_LAUNCH();
         TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
         TDS_CUDA(cudaStreamSynchronize(s));
-        d4 = hs.probe_total && 100ull * hs.probe_pass >= (uint64_t)HYST_HI * hs.probe_total;
-        tr.note("probe_pass_frac", hs.probe_total ? (double)hs.probe_pass / hs.probe_total : -1.0);
+        if (hs.probe_total >= 1024) {
+            probed = true;
+            est_hits = (uint64_t)((double)probe_pairs * hs.probe_pass / hs.probe_total);
+        }
+        tr.note("probe_est_hits", (double)est_hits);
     }
 
     uint64_t cap = capacity;
@@ -2132,7 +2167,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         // pools hand out since (abi.cu; no cudaMemGetInfo per search).  Buffers above
         // 1 GB are sized and allocated under a process-wide lock, so concurrent
         // searches (tds_search_many) do not over-commit the device.
-        const uint64_t want = hs.pair_tests + 64;
+        uint64_t want = probe_pairs + 64;
+        if (probed) want = std::min<uint64_t>(want, 3 * est_hits + CAP_FLOOR);
         if (want * sizeof(Rec) > (1ull << 30)) big_lock = std::unique_lock<std::mutex>(big_alloc_mutex());
         const uint64_t budget_bytes = device_budget_bytes();
         cap = std::min<uint64_t>(want, (uint64_t)(budget_bytes * 0.45) / sizeof(Rec));
@@ -2175,13 +2211,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         RangeArgs a{};
         a.df = filter_threshold(d);
         a.tc = time_origin(idx);
-        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
+        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64, dlo};
         for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
-        if (d4) k_pair_range<false, true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
-        else k_pair_range<false, false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+        k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
-        tr.note("dense4", d4 ? 1.0 : 0.0);
     } else if (nrows > 0 && hs.pair_tests > 0) {
         const uint64_t nslots = slot_hi - slot_lo;
         const uint64_t ngrab = (nslots + SP_GRAB - 1) / SP_GRAB;
@@ -2198,7 +2232,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.slot_row = slot_row.p;
         a.slot_lo = slot_lo;
         a.slot_hi = slot_hi;
-        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
+        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64, dlo};
         a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
         a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
         a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
@@ -2408,7 +2442,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             RangeArgs a{};
             a.df = filter_threshold(d);
             a.tc = time_origin(idx);
-            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64};
+            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64, dlo};
             a.pc.o.st = bst.p;
             for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
             a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
@@ -2461,7 +2495,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.slot_row = slot_row.p;
             a.slot_lo = 0;
             a.slot_hi = bslots;
-            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64};
+            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64, dlo};
             a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
             a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
             a.nrows = bnrows; a.G = G;
