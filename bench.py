@@ -247,20 +247,20 @@ def run_reference(args, ws, rank):
 # ---------------------------------------------------------------------------
 # the B200 arm
 # ---------------------------------------------------------------------------
-def roofline(dk, nD, nQ, kind, peaks, n_sms, traffic):
+def roofline(dk, nD, nQ, kind, peaks, n_sms, traffic, nA=0):
     """SURVEY §8(d) roofline of one pair-kernel launch: T_roof = max(B_alg / HBM,
     ops / FP32) against the measured kernel time; bound = the larger term."""
     secs = dk["pair_kernel_ms"] / 1e3
     hits = dk["results"]
     ops = OPS_PER_PAIR * dk["pair_tests"] + OPS_PER_HIT * hits
     nbytes = 36 * nD + 48 * nQ + 16 * hits + (4 * nD if kind == "spatiotemporal" else 0)
-    if kind == "spatial":       # no record reuse across queries: record + id per pair test
-        nbytes = 36 * dk["pair_tests"] + 48 * nQ + 16 * hits
+    if kind == "spatial":       # the cell-ordered copy: 32-B record + 4-B entry row + 4-B min cell per A entry
+        nbytes = 40 * nA + 48 * nQ + 16 * hits
     hbm = float(peaks.get("hbm_gbs", 6548.8))                      # GB/s, measured copy
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu = n_sms * 128 * mhz * 1e6                                  # FP32 lane-ops/s (B200_PROFILING unit counts)
     t_hbm, t_alu = nbytes / (hbm * 1e9), ops / alu
-    out = {"kernel": ("k_pair_spatial" if kind == "spatial" else "k_pair_range") + f" ({kind})",
+    out = {"kernel": f"k_pair_range ({kind})",
            "alu": {"achieved": ops / secs / 1e12, "peak": alu / 1e12, "unit": "Tops/s (FP32 lane ops)",
                    "frac": t_alu / secs, "ops": ops,
                    "work": f"{OPS_PER_PAIR} x {dk['pair_tests']} pair tests + {OPS_PER_HIT} x {hits} hits"},
@@ -380,13 +380,14 @@ def run_tds(args, ws, rank, local):
     # dominant kernel: the headline search's pair kernel (rank 0's launch: its own part)
     dk = dict(per_kind[head])
     dk["pair_tests"], dk["results"] = dk["pair_tests_rank0"], dk["results_rank0"]
-    kname = "k_pair_spatial" if head == "spatial" else "k_pair_range"
+    kname = "k_pair_range"
+    nA = idx.export_nbytes("fsg_A") // 4 if idx.kinds & tds.SPATIAL else 0
     roof = roofline(dk, nD, nQ / ws, head, peaks, n_sms,
-                    ncu_traffic(args.config, w.d, kname, head) if ws == 1 else None)
+                    ncu_traffic(args.config, w.d, kname, head) if ws == 1 else None, nA)
     for kind in args.variants[1:]:
         dk2 = dict(per_kind[kind])
         dk2["pair_tests"], dk2["results"] = dk2["pair_tests_rank0"], dk2["results_rank0"]
-        r2 = roofline(dk2, nD, nQ / ws, kind, peaks, n_sms, None)
+        r2 = roofline(dk2, nD, nQ / ws, kind, peaks, n_sms, None, nA)
         per_kind[kind]["roofline"] = {"bound": r2["bound"], "frac": r2["frac"], "alu_frac": r2["alu"]["frac"],
                                       "hbm_frac": r2["hbm"]["frac"]}
 

@@ -244,6 +244,12 @@ class Index:
                                     ctypes.byref(nb)))
         return out
 
+    def export_nbytes(self, what: str) -> int:
+        """Size in bytes of one exported index array (tds_index_export with no destination)."""
+        nb = ctypes.c_uint64()
+        _check(load_library().tds_index_export(self._h, EXPORT[what], None, 0, ctypes.byref(nb)))
+        return int(nb.value)
+
     def close(self):
         if getattr(self, "_h", None):
             load_library().tds_index_free(self._h)

@@ -29,12 +29,7 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #ifndef TDS_RANGE_BPS
 #define TDS_RANGE_BPS 2
 #endif
-#ifndef TDS_SPATIAL_BPS
-#define TDS_SPATIAL_BPS 3
-#endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
-constexpr int SPATIAL_BPS = TDS_SPATIAL_BPS;
-constexpr int SP_PER_LANE = 8;           // slots per lane per grab (spatial kernel)
 #ifndef TDS_HYST_HI
 #define TDS_HYST_HI 50
 #endif
@@ -46,7 +41,6 @@ constexpr unsigned long long CAP_PROBE_MIN = 1ull << 24;     // result-size prob
 constexpr uint64_t CAP_FLOOR = 1ull << 22;                   // records: floor of the probed capacity
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
-constexpr unsigned long long SP_GRAB = 32ull * SP_PER_LANE;
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
 // (derived bound 20 u M, u = 2^-24; 64 u used)
 constexpr float KU = 64.0f / 16777216.0f;
@@ -69,6 +63,8 @@ struct DevStats {
     unsigned int cat_cnt[5];         // schedule entries per category
     unsigned int probe_pass, probe_total;   // density probe (k_density_probe)
     unsigned int part_lo, part_hi;   // tds_search_part: schedule entries / query rows of this part
+    double probe_est;                // result-size probe: sum over sampled entries of len x pass fraction
+    unsigned int probe_entries;      // sampled live entries
     unsigned long long part_slot_lo, part_slot_hi;   // GPUSpatial part: flattened slot range
     unsigned int pad[1];
 };
@@ -89,12 +85,6 @@ struct Tile {
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-__device__ __forceinline__ float rsqrt_approx(float x) {
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
@@ -279,69 +269,44 @@ __device__ __forceinline__ void filter_abs2(float4 n0, float4 n1, float t0c, flo
     pass1 = (a1 <= b1) & (h1 <= r1);
 }
 
-// For a pair that passed a filter: 0 = no shared span (a >= b), 2 = certain hit (fp32 closest approach
-// < d - eta) whose fp32 interval [tin, tout] is within its first-order error
-// bound of the exact one, the bound being <= 1e-6 * max(b - a, min(|a|, |b|))
-// for every end not certainly clamped to a or b (clamped ends are exact);
-// 1 = evaluate in fp64 (pair64).
-template <bool CHECK_MISS = false>
-__device__ __forceinline__ int hit_kind(float4 q0, float4 q1, float t0c, float t1c, const ECand &e, float d,
-                                        float &tin, float &tout) {
-    const float a = fmaxf(t0c, e.t0), b = fminf(t1c, e.t1);
-    const float aq = a - q0.w, ae = a - e.t0;
-    const float dpx = q0.x - e.px, dpy = q0.y - e.py, dpz = q0.z - e.pz;
-    const float Dx = fmaf(-ae, e.vx, fmaf(aq, q1.x, dpx));
-    const float Dy = fmaf(-ae, e.vy, fmaf(aq, q1.y, dpy));
-    const float Dz = fmaf(-ae, e.vz, fmaf(aq, q1.z, dpz));
-    const float Vx = q1.x - e.vx, Vy = q1.y - e.vy, Vz = q1.z - e.vz;
-    const float L = b - a;
-    const float A = fmaf(Vx, Vx, fmaf(Vy, Vy, Vz * Vz));
-    const float B = fmaf(Dx, Vx, fmaf(Dy, Vy, Dz * Vz));
-    const float rA = rcp_approx(A);
-    const float su = -B * rA;
-    const float s = fminf(fmaxf(su, 0.f), L);
-    const float yx = fmaf(s, Vx, Dx), yy = fmaf(s, Vy, Dy), yz = fmaf(s, Vz, Dz);
-    const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
-    const float M = fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + (q1.w + e.ext);
-    if (!(a < b)) return 0;                                     // C5 (filter_abs passes a == b)
-    if (CHECK_MISS) {                                           // fused filter (dense windows)
-        const float thr = fmaf(KU, M, d);
-        if (!(h <= thr * thr)) return 0;
-    }
-    const float dl = d - KU * M;
-    if (!(dl > 0.f) || !(h < dl * dl)) return 1;
-    const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
-    const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    const float d2 = d * d;
-    const float rem = fmaxf(d2 - hu, 0.f);
-    const float w = sqrt_approx(rem * rA);                     // MUFU.SQRT: |rel err| <= 2^-22, in dw
-    const float V1 = fabsf(q1.x) + fabsf(q1.y) + fabsf(q1.z) + fabsf(e.vx) + fabsf(e.vy) + fabsf(e.vz);
-    constexpr float U = 1.0f / 16777216.0f;
-    // the bound itself needs no IEEE division / sqrt: approximate MUFU results,
-    // covered by the x2 safety factor
-    const float rsA = rsqrt_approx(A);                         // 1 / sqrt(A)
-    // s_u may lie far outside [0, L]: magnitudes along the line up to |s_u| enter M_u,
-    // and the relative errors of A and of the reciprocal scale |s_u| and w
-    // first-order bounds: |dDa| <= 11 u M_u, |dDV| <= 6 u V1,
-    // s_u = -(Da.DV)/A -> |ds_u| <= 14 u M_u/sqrt(A) + 6 u V1 M_u/A + |s_u| (dA/A + 2u);
-    // rem = d^2 - h_u -> |drem| <= 2 d 14 u M_u + A ds_u^2 + 2 u (d^2 + rem)
-    const float Su = fmaxf(fabsf(su), L);
-    const float Mu = M + Su * V1;
-    const float relA = (12.f * U) * V1 * rsA + 5.f * U;
-    const float dsu = (14.f * U) * Mu * rsA + (6.f * U) * V1 * Mu * rA + fabsf(su) * relA;
-    const float drem = (28.f * U) * d * Mu + A * dsu * dsu + (2.f * U) * (d2 + rem);
-    const float dw = w * (0.5f * drem * rcp_approx(rem) + 0.5f * relA + 4.f * U);
-    // x2 safety on the first-order terms, + the rounding of s_u -+ w
-    const float dst = fmaf(U, fabsf(su) + w, 2.f * (dsu + dw));
-    const float lo = su - w, hi = su + w;
-    tin = a + fminf(fmaxf(lo, 0.f), L);
-    tout = a + fminf(fmaxf(hi, 0.f), L);
-    // accepted offsets are within 8e-6 (b - a) of the exact ones; the output adds
-    // its fp32 rounding (<= 0.5 ulp(t)): |t - t_exact| <= 1e-5 (b - a) + ulp(t)
-    const float tol = (8e-6f) * L;
-    const bool in_ok = (lo + dst < 0.f) || (dst <= tol);
-    const bool out_ok = (hi - dst > L) || (dst <= tol);
-    return (in_ok && out_ok) ? 2 : 1;
+// filter_abs2 plus the whole-span test of dense windows: in0 / in1 = both ends of
+// the shared span certainly within d (squared distance at a' and b' below
+// (dlo - 64u (m_q + m_e))^2, the same certified margin: the bound holds at every
+// point of the span, the rounded span ends included), so the pair's interval is
+// exactly [a, b] (convexity in t).  qin = dlo - 64u m_q of the query.
+__device__ __forceinline__ void filter_abs2x(float4 n0, float4 n1, float t0c, float t1c, float qin, const FSeg2 &e,
+                                             float df, bool &pass0, bool &pass1, bool &in0, bool &in1) {
+    const float a0 = fmaxf(t0c, e.t0a), b0 = fminf(t1c, e.t1a);
+    const float a1 = fmaxf(t0c, e.t0b), b1 = fminf(t1c, e.t1b);
+    const f32x2 Cx = sub2(bc2(n0.x), e.cx), Cy = sub2(bc2(n0.y), e.cy), Cz = sub2(bc2(n0.z), e.cz);
+    const f32x2 Vx = sub2(bc2(n1.x), e.vx), Vy = sub2(bc2(n1.y), e.vy), Vz = sub2(bc2(n1.z), e.vz);
+    const f32x2 A = fma2(Vx, Vx, fma2(Vy, Vy, mul2(Vz, Vz)));
+    const f32x2 B = fma2(Cx, Vx, fma2(Cy, Vy, mul2(Cz, Vz)));
+    float A0, A1;
+    upk2(A, A0, A1);
+    float u0, u1;
+    upk2(mul2(B, pk2(rcp_approx(A0), rcp_approx(A1))), u0, u1);
+    const f32x2 pa = pk2(a0, a1), pb = pk2(b0, b1);
+    const f32x2 t = pk2(fminf(fmaxf(-u0, a0), b0), fminf(fmaxf(-u1, a1), b1));
+    const f32x2 yx = fma2(t, Vx, Cx), yy = fma2(t, Vy, Cy), yz = fma2(t, Vz, Cz);
+    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
+    const f32x2 ax = fma2(pa, Vx, Cx), ay = fma2(pa, Vy, Cy), az = fma2(pa, Vz, Cz);
+    const f32x2 bx = fma2(pb, Vx, Cx), by = fma2(pb, Vy, Cy), bz = fma2(pb, Vz, Cz);
+    const f32x2 ha = fma2(ax, ax, fma2(ay, ay, mul2(az, az)));
+    const f32x2 hb = fma2(bx, bx, fma2(by, by, mul2(bz, bz)));
+    const f32x2 thr = fma2(bc2(KU), add2(bc2(n0.w), e.m), bc2(df));
+    const f32x2 tin = fma2(bc2(-KU), e.m, bc2(qin));
+    float h0, h1, r0, r1, ha0, ha1, hb0, hb1, ti0, ti1, q0, q1;
+    upk2(h, h0, h1);
+    upk2(mul2(thr, thr), r0, r1);
+    upk2(ha, ha0, ha1);
+    upk2(hb, hb0, hb1);
+    upk2(tin, ti0, ti1);
+    upk2(mul2(tin, tin), q0, q1);
+    pass0 = (a0 <= b0) & (h0 <= r0);
+    pass1 = (a1 <= b1) & (h1 <= r1);
+    in0 = (a0 < b0) & (ti0 > 0.f) & (ha0 < q0) & (hb0 < q0);
+    in1 = (a1 < b1) & (ti1 > 0.f) & (ha1 < q1) & (hb1 < q1);
 }
 
 // fp64 evaluation of the closed form (SURVEY §8c / DESIGN.md "Pair test"):
@@ -407,7 +372,8 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
     const float D1 = fabsf(Dx) + fabsf(Dy) + fabsf(Dz), W1 = fabsf(Vx) + fabsf(Vy) + fabsf(Vz);
     const float eD = U * fmaf(7.f, fabsf(aq) * q1.w + fabsf(ae) * V1e, fabsf(dpx) + fabsf(dpy) + fabsf(dpz) + 2.f * D1);
     const float eV = U * fmaf(5.f, q1.w + V1e, W1);
-    const float eP = 1.5f * fmaf(L, eV, eD);                   // x1.5 on the first-order bound
+    const float eP0 = fmaf(L, eV, eD);                         // first-order position error on [0, L]
+    const float eP = 1.5f * eP0;                               // x1.5 for the distance decisions
     const float mg = fmaf(4.f * U, dhi, eP);                   // + rounding of the squared norms
     const float din = dlo - mg, dout = dhi + mg;
     // both span ends certainly within d: the whole span (convexity)
@@ -432,7 +398,7 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
     // error of the unclamped ends: root sensitivity d eP / (A w) to the position
     // error, + roundings of h_u and d^2, of B (3u |D|_1 |V|_1 / A), of s_u and w
     const float dlt = fmaf(U, fabsf(su) + w,
-                           1.5f * fmaf(fmaf(dhi, eP, (4.5f * U) * dhi * dhi), rcp_approx(A * w),
+                           1.5f * fmaf(fmaf(dhi, eP0, (4.5f * U) * dhi * dhi), rcp_approx(A * w),
                                        fmaf((3.f * U) * D1 * W1, rA, U * fmaf(7.f, fabsf(su), 5.f * w))));
     tin = a + fminf(fmaxf(lo, 0.f), L);
     tout = a + fminf(fmaxf(hi, 0.f), L);
@@ -448,7 +414,8 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
 struct OutArgs {
     Rec *buf;                        // pass buffer (chunked) or store (exact)
     unsigned long long cap;          // pass buffer slots
-    uint32_t CS;                     // chunk size (slots)
+    uint32_t CS;                     // chunk size (slots), a power of two
+    uint32_t cs_shift;               // log2(CS)
     uint32_t *chunk_used;            // [ceil(cap/CS)]
     uint8_t *redo;                   // [nq] 1 = query lost a record
     uint32_t *qcount;                // [nq] records produced per query
@@ -466,10 +433,9 @@ struct WarpState {
     uint32_t ap_used, ap_size, ap_full;
     uint32_t refined, hits;
     uint32_t fn;                     // fp64 queue fill (< 32 between flushes)
-    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: query row (| F64_FLAG), sorted entry position
+    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: group slot, candidate (sorted / cell-ordered position)
     uint32_t fq[64], fj[64];         // fp64 queue: pairs the fp32 stages could not decide
 };
-constexpr uint32_t F64_FLAG = 0x80000000u;   // refine-queue entry already known to need fp64
 
 __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
     if (lane == 0) {
@@ -503,7 +469,7 @@ __device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit,
     unsigned long long base = W.ap_base;
     uint32_t used = W.ap_used, size = W.ap_size, full = W.ap_full;
     if (!full && used + k > size) {
-        if (size && lane == 0) o.chunk_used[base / o.CS] = used;
+        if (size && lane == 0) o.chunk_used[base >> o.cs_shift] = used;
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(&o.st->reserved, (unsigned long long)o.CS);
         nb = __shfl_sync(FULL, nb, 0);
@@ -549,7 +515,7 @@ __device__ __forceinline__ void appendK(const OutArgs &o, WarpState &W, const bo
     unsigned long long base = W.ap_base;
     uint32_t used = W.ap_used, size = W.ap_size, full = W.ap_full;
     if (!full && used + k > size) {
-        if (size && lane == 0) o.chunk_used[base / o.CS] = used;
+        if (size && lane == 0) o.chunk_used[base >> o.cs_shift] = used;
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(&o.st->reserved, (unsigned long long)o.CS);
         nb = __shfl_sync(FULL, nb, 0);
@@ -597,7 +563,7 @@ template <bool EXACT>
 __device__ __forceinline__ void warp_state_finish(const OutArgs &o, WarpState &W, int lane) {
     __syncwarp();
     if (lane == 0) {
-        if (!EXACT && !W.ap_full && W.ap_size) o.chunk_used[W.ap_base / o.CS] = W.ap_used;
+        if (!EXACT && !W.ap_full && W.ap_size) o.chunk_used[W.ap_base >> o.cs_shift] = W.ap_used;
         if (W.refined) atomicAdd(&o.st->refined, (unsigned long long)W.refined);
         if (W.hits) atomicAdd(&o.st->hits, (unsigned long long)W.hits);
     }
@@ -648,64 +614,6 @@ __device__ __forceinline__ void flush64(const PairCtx *C, WarpState *W, uint32_t
     __syncwarp();
 }
 
-// Evaluate queued pairs [base, base + n), n <= 32 (lane k takes pair k): certain
-// hits with an accurate fp32 interval are appended; the undecided go to the fp64
-// queue, which is evaluated 32 at a time (a warp-wide fp64 pass per 32 pairs that
-// need it, not per flush).  Entries flagged F64_FLAG skip the fp32 stage.
-template <bool EXACT>
-__device__ __forceinline__ void flush_refine(const PairCtx *C, WarpState *W, uint32_t n, uint32_t base = 0) {
-    const int lane = threadIdx.x & 31;
-    const bool v = (uint32_t)lane < n;
-    const uint32_t qraw = v ? W->rq[base + lane] : 0u, j = v ? W->rj[base + lane] : 0u;
-    const uint32_t q = qraw & ~F64_FLAG;
-    __syncwarp();                    // queue slots read: later queue_add may reuse them
-    float tin = 0.f, tout = 0.f;
-    int k = 0;
-    if (v) {
-        if (qraw & F64_FLAG) {
-            k = 1;
-        } else {
-            const float4 qa = __ldg(C->Q + 2 * (uint64_t)q), qb = __ldg(C->Q + 2 * (uint64_t)q + 1);
-            const float4 ea = __ldg(C->rec + 2 * (uint64_t)j), eb = __ldg(C->rec + 2 * (uint64_t)j + 1);
-            const QConst qc = make_qconst(qa, qb, C->T0, C->T1);
-            const ECand e = make_ecand(ea, eb);
-            k = refine_rel(make_float4(qc.px, qc.py, qc.pz, qc.t0),
-                           make_float4(qc.vx, qc.vy, qc.vz, fabsf(qc.vx) + fabsf(qc.vy) + fabsf(qc.vz)), qc.t0c, qc.t1c,
-                           make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, C->dlo, C->d, tin, tout);
-        }
-    }
-    const bool hit = (k == 2), need64 = (k == 1);
-    const uint32_t eid = hit ? __ldg(C->perm + j) : 0u;
-    Rec r{q, eid, tin, tout};
-    append<EXACT>(C->o, *W, hit, r, lane);
-    const unsigned hm = __ballot_sync(FULL, hit);
-    if (hit) {   // per-query counts, aggregated over the lanes of the same query
-        const unsigned peers = __match_any_sync(hm, q);
-        if ((peers & ((1u << lane) - 1u)) == 0) atomicAdd(&C->o.qcount[q], (uint32_t)__popc(peers));
-    }
-    // undecided pairs -> fp64 queue
-    const unsigned m64 = __ballot_sync(FULL, need64);
-    const uint32_t fn = W->fn;
-    if (need64) {
-        const uint32_t pos = fn + __popc(m64 & ((1u << lane) - 1u));
-        W->fq[pos] = q;
-        W->fj[pos] = j;
-    }
-    __syncwarp();
-    if (lane == 0) { W->hits += __popc(hm); W->fn = fn + __popc(m64); }
-    __syncwarp();
-    if (fn + __popc(m64) >= 32) flush64<EXACT>(C, W, 32);
-}
-
-// warp-wide: queue the pairs whose fp32 filter passed (no flush here)
-__device__ __forceinline__ void queue_add(WarpState &W, uint32_t &qn, bool maybe, uint32_t qid, uint32_t j, int lane) {
-    const unsigned mb = __ballot_sync(FULL, maybe);
-    if (!mb) return;
-    const uint32_t pos = qn + __popc(mb & ((1u << lane) - 1u));
-    if (maybe) { W.rq[pos] = qid; W.rj[pos] = j; }
-    qn += __popc(mb);
-}
-
 // warp-wide: queue four candidate slots at once (branch-free; the queue holds
 // < 32 entries before, so at most 32 + 4 x 32 after, within RQ_CAP)
 __device__ __forceinline__ void queue_add4(WarpState &W, uint32_t &qn, bool m0, bool m1, bool m2, bool m3,
@@ -723,25 +631,6 @@ __device__ __forceinline__ void queue_add4(WarpState &W, uint32_t &qn, bool m0, 
     p += __popc(b2);
     if (m3) { const uint32_t k = p + __popc(b3 & lt); W.rq[k] = qid; W.rj[k] = j3; }
     qn = p + __popc(b3);
-}
-
-// warp-wide: evaluate queued pairs in fp64, 32 at a time, while >= 32 are queued
-template <bool EXACT>
-__device__ __forceinline__ void queue_drain(const PairCtx *C, WarpState &W, uint32_t &qn, int lane) {
-    if (qn < 32) return;
-    __syncwarp();
-    uint32_t head = 0;
-    do {                                 // flush 32 at a time in place
-        flush_refine<EXACT>(C, &W, 32, head);
-        head += 32;
-    } while (qn - head >= 32);
-    const uint32_t rest = qn - head;     // move the remainder to the front
-    uint32_t t1 = 0, t2 = 0;
-    if ((uint32_t)lane < rest) { t1 = W.rq[head + lane]; t2 = W.rj[head + lane]; }
-    __syncwarp();
-    if ((uint32_t)lane < rest) { W.rq[lane] = t1; W.rj[lane] = t2; }
-    __syncwarp();
-    qn = rest;
 }
 
 struct SchedArgs {
@@ -957,7 +846,20 @@ struct RangeArgs {
     uint32_t ntiles;
     float df;                        // filter_abs threshold: d * (1 + 2^-20), rounded up
     float tc;                        // filter_abs time origin (middle of the index's time extent)
+    // GPUSpatial through this kernel (entries = (query, FSG cell) slices of the
+    // cell-ordered record copy): per entry its cell and the query box's low corner
+    // (packed), per candidate the min cell of its MBB; null for the range variants
+    const uint32_t *sp_cell, *sp_qlo, *ecell;
 };
+
+// GPUSpatial duplicate avoidance (replaces the host filter of P:558-559): a pair
+// (q, e) is tested only in the first cell (index-space min corner) of
+// cells(e) ∩ cells(q), i.e. the cell max(min cell of e, low corner of q's box)
+__device__ __forceinline__ bool ref_cell(uint32_t m0, uint32_t qlo, uint32_t cell) {
+    const uint32_t rx = max(m0 >> 21, qlo >> 21), ry = max((m0 >> 10) & 0x7ffu, (qlo >> 10) & 0x7ffu),
+                   rz = max(m0 & 0x3ffu, qlo & 0x3ffu);
+    return ((rx << 21) | (ry << 10) | rz) == cell;
+}
 
 // threshold of filter_abs: d (already rounded up) times 1 + 2^-20, rounded up,
 // so the rounding of thr and thr^2 never turns a pass into a reject
@@ -978,13 +880,15 @@ inline float filter_threshold(float d) {
 __global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const float4 *__restrict__ Q,
                                 const float4 *__restrict__ rec, const uint32_t *__restrict__ arr0,
                                 const uint32_t *__restrict__ arr1, const uint32_t *__restrict__ arr2, float d, float T0,
-                                float T1, DevStats *st) {
+                                float T1, const uint32_t *__restrict__ ecell, const uint32_t *__restrict__ sp_cell,
+                                const uint32_t *__restrict__ sp_qlo, DevStats *st) {
     const int lane = threadIdx.x & 31;
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     if (n == 0) return;
     const uint32_t p = (uint32_t)(((uint64_t)w * n) / nw + n / (2 * nw));
     if (p >= n) return;
     const Sched e = S[p];
+    if (lane == 0) atomicAdd(&st->probe_entries, 1u);   // every sampled entry (empty ones estimate 0)
     if (e.sel == 3 || e.hi <= e.lo) return;
     const uint32_t *arr = e.sel == 0 ? arr0 : e.sel == 1 ? arr1 : e.sel == 2 ? arr2 : nullptr;
     const QConst qc = make_qconst(__ldg(Q + 2 * (uint64_t)e.qid), __ldg(Q + 2 * (uint64_t)e.qid + 1), T0, T1);
@@ -996,13 +900,15 @@ __global__ void k_density_probe(const Sched *__restrict__ S, uint32_t n, const f
         // can be unrepresentative, e.g. the boundary between two clusters)
         const uint32_t c = e.lo + (uint32_t)(((uint64_t)k * len) / m), j = arr ? __ldg(arr + c) : c;
         const ECand ec = make_ecand(__ldg(rec + 2 * (uint64_t)j), __ldg(rec + 2 * (uint64_t)j + 1));
-        pass += filter_pair(q0, q1, qc.t0c, qc.t1c, ec, d) ? 1u : 0u;
+        const bool ref = !ecell || ref_cell(__ldg(ecell + j), sp_qlo[p], sp_cell[p]);   // GPUSpatial: no duplicates
+        pass += (ref && filter_pair(q0, q1, qc.t0c, qc.t1c, ec, d)) ? 1u : 0u;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pass += __shfl_xor_sync(FULL, pass, o);
     if (lane == 0) {
         atomicAdd(&st->probe_pass, pass);
         atomicAdd(&st->probe_total, m);
+        atomicAdd(&st->probe_est, (double)len * pass / m);   // this entry's estimated records
     }
 }
 
@@ -1011,6 +917,8 @@ struct __align__(16) RangeWarpSmem {
                                      // and the absolute form (c, m) (v, t0c') (t1c', lo, hi, qid)
     WarpState ws;                    // append chunk, refine queue (slot g, sorted position j), fp64 queue
     uint32_t cnt[32];                // records of slot g found by the refine path in this work item
+    float4 craw[4][32];              // dense windows: (t0, t1, entry row, min cell) of lane's candidate k
+    uint32_t spc[32], spq[32];       // GPUSpatial: cell and query-box low corner of slot g
     uint32_t qn;                     // refine queue fill
 };
 
@@ -1029,9 +937,11 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
     if (v) {
         const float4 q0 = W->q[g][0], q1 = W->q[g][1], q2 = W->q[g][2];
         qid = __float_as_uint(W->q[g][5].w);
-        const ECand e = make_ecand(__ldg(A->pc.rec + 2 * (uint64_t)j), __ldg(A->pc.rec + 2 * (uint64_t)j + 1));
-        k = refine_rel(q0, q1, q2.x, q2.y, make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, A->pc.dlo,
-                       A->pc.d, tin, tout);
+        if (!A->ecell || ref_cell(__ldg(A->ecell + j), W->spq[g], W->spc[g])) {
+            const ECand e = make_ecand(__ldg(A->pc.rec + 2 * (uint64_t)j), __ldg(A->pc.rec + 2 * (uint64_t)j + 1));
+            k = refine_rel(q0, q1, q2.x, q2.y, make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, A->pc.dlo,
+                           A->pc.d, tin, tout);
+        }
     }
     const bool hit = (k == 2), need64 = (k == 1);
     const Rec r{qid, hit ? __ldg(A->pc.perm + j) : 0u, tin, tout};
@@ -1060,60 +970,6 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
     }
 }
 
-// Dense windows: for the lane's two candidates against query slot g, in the
-// relative form: in0/in1 = both span ends certainly within d (then the whole
-// shared span [a, b] is within d: the squared distance is convex in t; the
-// pair's interval is exactly [a, b]), ps0/ps1 = the closest approach passes the
-// filter.  Certainty margin KU M, M = |p0q - p0e|_1 + |p1q - p0q|_1 + |p1e -
-// p0e|_1 (the relative-form bound of DESIGN.md §5 holds at every point of the
-// span, so at both ends).  Packed FP32x2 per candidate pair.
-__device__ __forceinline__ void dense_test2(float4 q0, float4 q1, float4 q2, const ECand &e0, const ECand &e1, float d,
-                                            bool &in0, bool &in1, bool &ps0, bool &ps1, float &a0, float &b0,
-                                            float &a1, float &b1) {
-    a0 = fmaxf(q2.x, e0.t0); b0 = fminf(q2.y, e0.t1);
-    a1 = fmaxf(q2.x, e1.t0); b1 = fminf(q2.y, e1.t1);
-    const f32x2 a = pk2(a0, a1);
-    const f32x2 L = sub2(pk2(b0, b1), a);
-    const f32x2 aq = sub2(a, bc2(q0.w)), nae = sub2(pk2(e0.t0, e1.t0), a);
-    const f32x2 dpx = sub2(bc2(q0.x), pk2(e0.px, e1.px)), dpy = sub2(bc2(q0.y), pk2(e0.py, e1.py)),
-                dpz = sub2(bc2(q0.z), pk2(e0.pz, e1.pz));
-    const f32x2 evx = pk2(e0.vx, e1.vx), evy = pk2(e0.vy, e1.vy), evz = pk2(e0.vz, e1.vz);
-    const f32x2 Dx = fma2(nae, evx, fma2(aq, bc2(q1.x), dpx));
-    const f32x2 Dy = fma2(nae, evy, fma2(aq, bc2(q1.y), dpy));
-    const f32x2 Dz = fma2(nae, evz, fma2(aq, bc2(q1.z), dpz));
-    const f32x2 Vx = sub2(bc2(q1.x), evx), Vy = sub2(bc2(q1.y), evy), Vz = sub2(bc2(q1.z), evz);
-    const f32x2 ybx = fma2(L, Vx, Dx), yby = fma2(L, Vy, Dy), ybz = fma2(L, Vz, Dz);
-    const f32x2 ha = fma2(Dx, Dx, fma2(Dy, Dy, mul2(Dz, Dz)));
-    const f32x2 hb = fma2(ybx, ybx, fma2(yby, yby, mul2(ybz, ybz)));
-    float x0, x1, y0, y1, z0, z1;
-    upk2(dpx, x0, x1);
-    upk2(dpy, y0, y1);
-    upk2(dpz, z0, z1);
-    const f32x2 M = add2(pk2(fabsf(x0) + fabsf(y0) + fabsf(z0), fabsf(x1) + fabsf(y1) + fabsf(z1)),
-                         add2(bc2(q2.z), pk2(e0.ext, e1.ext)));
-    const f32x2 thr = fma2(bc2(KU), M, bc2(d)), dl = fma2(bc2(-KU), M, bc2(d));
-    const f32x2 A = fma2(Vx, Vx, fma2(Vy, Vy, mul2(Vz, Vz)));
-    const f32x2 B = fma2(Dx, Vx, fma2(Dy, Vy, mul2(Dz, Vz)));
-    float A0, A1, L0, L1, u0, u1;
-    upk2(A, A0, A1);
-    upk2(L, L0, L1);
-    upk2(mul2(B, pk2(rcp_approx(A0), rcp_approx(A1))), u0, u1);
-    const f32x2 sv = pk2(fminf(fmaxf(-u0, 0.f), L0), fminf(fmaxf(-u1, 0.f), L1));
-    const f32x2 yx = fma2(sv, Vx, Dx), yy = fma2(sv, Vy, Dy), yz = fma2(sv, Vz, Dz);
-    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
-    float ha0, ha1, hb0, hb1, h0, h1, t0, t1, l0, l1, dl0, dl1;
-    upk2(ha, ha0, ha1);
-    upk2(hb, hb0, hb1);
-    upk2(h, h0, h1);
-    upk2(mul2(thr, thr), t0, t1);
-    upk2(mul2(dl, dl), l0, l1);
-    upk2(dl, dl0, dl1);
-    in0 = (a0 < b0) & (dl0 > 0.f) & (ha0 < l0) & (hb0 < l0);
-    in1 = (a1 < b1) & (dl1 > 0.f) & (ha1 < l1) & (hb1 < l1);
-    ps0 = (a0 < b0) & (h0 <= t0);
-    ps1 = (a1 < b1) & (h1 <= t1);
-}
-
 // Mapping: a work item is a group of <= 32
 // consecutive schedule entries (one category) and a chunk of the union of their
 // candidate ranges.  Lane g owns query slot g of the group (its constants are
@@ -1127,13 +983,12 @@ __device__ __forceinline__ void dense_test2(float4 q0, float4 q1, float4 q2, con
 // step dense_test2 appends whole-span hits at once and queues the rest.
 template <bool EXACT>
 __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_constant__ RangeArgs A) {
-    __shared__ RangeWarpSmem sm[PT / 32];
+    extern __shared__ __align__(16) unsigned char range_smem[];     // PT / 32 x RangeWarpSmem (> 48 KB)
     const int lane = threadIdx.x & 31;
-    RangeWarpSmem &W = sm[threadIdx.x >> 5];
+    RangeWarpSmem &W = reinterpret_cast<RangeWarpSmem *>(range_smem)[threadIdx.x >> 5];
     DevStats *st = A.pc.o.st;
     const uint32_t total = A.item_start[A.ntiles];
     const uint32_t CH = st->ch;
-    const float d = A.pc.d;
     const float df = A.df;
     warp_state_init(W.ws, lane);
     W.cnt[lane] = 0;
@@ -1175,6 +1030,10 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             W.q[lane][4] = make_float4(qf.vx, qf.vy, qf.vz, qc.t0c - A.tc);
             W.q[lane][5] = make_float4(qc.t1c - A.tc, __uint_as_float(my_lo), __uint_as_float(my_hi),
                                        __uint_as_float(S.qid));
+            if (A.ecell) {
+                W.spc[lane] = active ? A.sp_cell[p] : 0xffffffffu;
+                W.spq[lane] = active ? A.sp_qlo[p] : 0u;
+            }
             __syncwarp();
         }
         uint32_t wlo = my_lo, whi = my_hi;
@@ -1217,51 +1076,82 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             exec += (unsigned long long)(cend - base) * __popc(mask);
             uint32_t wpass = 0;                // filter passes of this window (all queries)
             if (dense) {
-                // the window in two halves of 64 candidates (two per lane), each against
-                // every query slot: one copy of the step, two candidate terms live
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t ca = c0 + 64u * h, cb = ca + 32u;
-                    if (ca - lane >= cend) break;
-                    uint32_t ja, jb;
-                    float4 a, b;
-                    load_cand(ca, ca < cend, ja, a, b);
-                    const ECand ea = make_ecand(a, b);
-                    load_cand(cb, cb < cend, jb, a, b);
-                    const ECand eb = make_ecand(a, b);
-                    // entry rows, loaded once per window (not per hit)
-                    const uint32_t ida = ca < cend ? __ldg(A.pc.perm + ja) : 0u, idb = cb < cend ? __ldg(A.pc.perm + jb) : 0u;
-                    unsigned m = wmask;
-                    while (m) {
-                        const int g = __ffs(m) - 1;
-                        m &= m - 1;
-                        const float4 q0 = W.q[g][0], q1 = W.q[g][1], q2 = W.q[g][2], q5 = W.q[g][5];
-                        const uint32_t glo = __float_as_uint(q5.y), ghi = __float_as_uint(q5.z);
-                        const uint32_t qid = __float_as_uint(q5.w);
-                        bool in0, in1, ps0, ps1;
-                        float a0, b0, a1, b1;
-                        dense_test2(q0, q1, q2, ea, eb, d, in0, in1, ps0, ps1, a0, b0, a1, b1);
-                        // slot c valid for slot g iff glo <= c < ghi (ghi <= whi) and c < cend
-                        const bool r0 = (ca - glo < ghi - glo) && (ca < cend);
-                        const bool r1 = (cb - glo < ghi - glo) && (cb < cend);
-                        in0 &= r0; in1 &= r1;
-                        ps0 = ps0 & r0 & !in0;
-                        ps1 = ps1 & r1 & !in1;
-                        const unsigned bi0 = __ballot_sync(FULL, in0), bi1 = __ballot_sync(FULL, in1);
-                        const unsigned bp0 = __ballot_sync(FULL, ps0), bp1 = __ballot_sync(FULL, ps1);
-                        wpass += __popc(bi0) + __popc(bi1) + __popc(bp0) + __popc(bp1);
-                        if (bi0 | bi1) {
-                            append2<EXACT>(A.pc.o, W.ws, in0, in1, bi0, bi1, Rec{qid, ida, a0, b0},
-                                           Rec{qid, idb, a1, b1}, lane);
-                            const uint32_t hg = __popc(bi0) + __popc(bi1);
-                            direct_hits += hg;
-                            if (lane == g) owner_hits += hg;
+                // fused step: the filter and the whole-span test for the lane's four
+                // candidates (two packed pairs); whole-span hits are appended at once
+                // with [a, b] from the raw times, other passes go to the refine queue
+                FSeg2 f01, f23;
+                {
+                    // raw times and entry rows of the lane's candidates (its own smem
+                    // slots, read back only when a record is appended)
+                    float4 a0, b0, a1, b1;
+                    load_cand(c0, c0 < cend, j0, a0, b0);
+                    load_cand(c1, c1 < cend, j1, a1, b1);
+                    f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
+                    W.craw[0][lane] = make_float4(a0.w, b0.w, __uint_as_float(c0 < cend ? __ldg(A.pc.perm + j0) : 0u),
+                                                  __uint_as_float(A.ecell && c0 < cend ? __ldg(A.ecell + j0) : 0u));
+                    W.craw[1][lane] = make_float4(a1.w, b1.w, __uint_as_float(c1 < cend ? __ldg(A.pc.perm + j1) : 0u),
+                                                  __uint_as_float(A.ecell && c1 < cend ? __ldg(A.ecell + j1) : 0u));
+                    load_cand(c2, c2 < cend, j2, a0, b0);
+                    load_cand(c3, c3 < cend, j3, a1, b1);
+                    f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
+                    W.craw[2][lane] = make_float4(a0.w, b0.w, __uint_as_float(c2 < cend ? __ldg(A.pc.perm + j2) : 0u),
+                                                  __uint_as_float(A.ecell && c2 < cend ? __ldg(A.ecell + j2) : 0u));
+                    W.craw[3][lane] = make_float4(a1.w, b1.w, __uint_as_float(c3 < cend ? __ldg(A.pc.perm + j3) : 0u),
+                                                  __uint_as_float(A.ecell && c3 < cend ? __ldg(A.ecell + j3) : 0u));
+                }
+                while (mask) {
+                    const int g = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const float4 n0 = W.q[g][3], n1 = W.q[g][4], n2 = W.q[g][5];
+                    const uint32_t glo = __float_as_uint(n2.y), ghi = __float_as_uint(n2.z);
+                    const float qin = fmaf(-KU, n0.w, A.pc.dlo);
+                    bool m[4], in[4];
+                    filter_abs2x(n0, n1, n1.w, n2.x, qin, f01, df, m[0], m[1], in[0], in[1]);
+                    filter_abs2x(n0, n1, n1.w, n2.x, qin, f23, df, m[2], m[3], in[2], in[3]);
+                    if (glo > base || ghi - base < WIN) {    // slots outside the query's range
+                        const uint32_t r0 = c0 - glo, gw = ghi - glo;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const bool ok = r0 + 32u * k < gw;
+                            m[k] &= ok;
+                            in[k] &= ok;
                         }
-                        if (bp0 | bp1) {
-                            queue_add(W.ws, qn, ps0, (uint32_t)g, ja, lane);
-                            queue_add(W.ws, qn, ps1, (uint32_t)g, jb, lane);
-                            range_drain<EXACT>(&A, W, qn);
+                    }
+                    if (A.ecell) {                         // GPUSpatial: the pair's reference cell only
+                        const uint32_t sq = W.spq[g], sc = W.spc[g];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const bool ok = ref_cell(__float_as_uint(W.craw[k][lane].w), sq, sc);
+                            m[k] &= ok;
+                            in[k] &= ok;
                         }
+                    }
+                    unsigned bi[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        m[k] &= !in[k];
+                        bi[k] = __ballot_sync(FULL, in[k]);
+                    }
+                    const uint32_t nin = __popc(bi[0]) + __popc(bi[1]) + __popc(bi[2]) + __popc(bi[3]);
+                    if (nin) {
+                        const float4 q2 = W.q[g][2];
+                        const uint32_t qid = __float_as_uint(n2.w);
+                        Rec r[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 cr = W.craw[k][lane];
+                            r[k] = Rec{qid, __float_as_uint(cr.z), fmaxf(q2.x, cr.x), fminf(q2.y, cr.y)};
+                        }
+                        appendK<EXACT, 4>(A.pc.o, W.ws, in, bi, r, lane);
+                        direct_hits += nin;
+                        if (lane == g) owner_hits += nin;
+                    }
+                    wpass += nin;
+                    if (__any_sync(FULL, (m[0] | m[1]) | (m[2] | m[3]))) {
+                        const uint32_t q0n = qn;
+                        queue_add4(W.ws, qn, m[0], m[1], m[2], m[3], (uint32_t)g, j0, j1, j2, j3, lane);
+                        wpass += qn - q0n;
+                        range_drain<EXACT>(&A, W, qn);
                     }
                 }
             } else {
@@ -1373,6 +1263,43 @@ __global__ void k_gather_u32(const uint32_t *__restrict__ src, const uint32_t *_
     if (p < n) out[p] = src[idx[p]];
 }
 
+// GPUSpatial schedule entries from the (query, cell) items: entry r = (query row,
+// time-trimmed slice [alo, alo + len) of the cell-ordered copy), its cell and the
+// query box's low corner for the reference-cell rule; sort key = slice start
+// (empty slices last, key empty_key)
+__global__ void k_fsg_sched(uint32_t nrows, const uint32_t *__restrict__ row_q, const uint32_t *__restrict__ row_alo,
+                            const uint32_t *__restrict__ row_len, const uint32_t *__restrict__ row_cxy,
+                            const int4 *__restrict__ qbox, uint32_t empty_key, Sched *__restrict__ out,
+                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals, uint32_t *__restrict__ sp_cell,
+                            uint32_t *__restrict__ sp_qlo, DevStats *st) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long work = 0;
+    uint32_t live = 0;
+    if (r < nrows) {
+        const int4 lo = qbox[2 * row_q[r]];
+        const uint32_t a0 = row_alo[r], len = row_len[r];
+        out[r] = len ? Sched{(uint32_t)lo.w, a0, a0 + len, -1} : Sched{(uint32_t)lo.w, 0u, 0u, 3};
+        keys[r] = len ? a0 : empty_key;
+        vals[r] = r;
+        sp_cell[r] = row_cxy[r];
+        sp_qlo[r] = pack_cell(lo.x, lo.y, lo.z);
+        work = len;
+        live = len ? 1u : 0u;
+    }
+    uint32_t empty = (r < nrows) ? 1u - live : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        work += __shfl_xor_sync(FULL, work, o);
+        live += __shfl_xor_sync(FULL, live, o);
+        empty += __shfl_xor_sync(FULL, empty, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (work) atomicAdd(&st->pair_tests, work);
+        if (live) atomicAdd(&st->cat_cnt[0], live);
+        if (empty) atomicAdd(&st->cat_cnt[4], empty);
+    }
+}
+
 __global__ void k_fsg_count(const float4 *__restrict__ Q, const uint32_t *__restrict__ list, uint32_t n, float d,
                             float T0, float T1, FsgGrid G, uint32_t *__restrict__ nitems, int4 *__restrict__ qbox,
                             unsigned long long *__restrict__ total, unsigned long long *__restrict__ bad) {
@@ -1443,189 +1370,6 @@ __global__ void k_fsg_items(const uint32_t *__restrict__ item_start, uint32_t n,
     }
 }
 
-struct SpatialArgs {
-    PairCtx pc;                      // rec / perm = the cell-ordered copies (indexed by A position)
-    const uint32_t *ecell;           // packed min cell of entry A[i]
-    const uint32_t *grab_row;        // [ngrab + 1] row of the first slot of each grab
-    const uint32_t *cell_off;
-    const int4 *qbox;                // [2 * nlist]: lo (w = query row), hi
-    const uint32_t *row_q, *row_alo, *row_cxy;   // work items (query, cell): query, slice start, packed cell
-    const unsigned long long *slot_start;   // [nrows + 1]
-    const uint32_t *slot_row;        // [slots] row of each slot (small searches), else nullptr
-    unsigned long long slot_lo, slot_hi;   // the slots this launch evaluates (tds_search_part: a sub-range)
-    uint32_t nrows;
-    FsgGrid G;
-};
-
-// Small searches (<= SLOT_ROW_MAX slots): the row of every slot, found by one
-// thread per slot in parallel, so the pair kernel needs one load per row change
-// instead of a dependent binary search (most (query, cell-row) items of a small
-// search are empty after time trimming: on Random-1M-shaped data a row change
-// per slot, each a ~10-level chain of L2 loads, set the kernel time).
-constexpr unsigned long long SLOT_ROW_MAX = 1ull << 22;
-
-__device__ __forceinline__ uint32_t find_row(const unsigned long long *ss, uint32_t lo, uint32_t hi,
-                                             unsigned long long s) {
-    // last r in [lo, hi) with ss[r] <= s
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (ss[mid] <= s) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-// slot_row[k] = row of slot base + k
-__global__ void k_slot_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, unsigned long long base,
-                            uint64_t nslots, uint32_t *__restrict__ slot_row) {
-    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < nslots) slot_row[k] = find_row(ss, 0, nrows, base + k);
-}
-
-// grab_row[k] = row of slot base + k * SP_GRAB (clamped to the last slot < end)
-__global__ void k_grab_rows(const unsigned long long *__restrict__ ss, uint32_t nrows, unsigned long long base,
-                            unsigned long long end, uint64_t ngrab, uint32_t *__restrict__ grab_row) {
-    uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k > ngrab) return;
-    unsigned long long s = base + k * SP_GRAB;
-    if (s >= end) s = end > base ? end - 1 : base;
-    grab_row[k] = find_row(ss, 0, nrows, s);
-}
-
-// Result-size probe of a GPUSpatial search: the fraction of passing pair tests
-// (relative-form filter + the reference-cell rule) on slots sampled evenly over
-// [s_lo, s_hi), one per thread.
-__global__ void k_density_probe_spatial(const unsigned long long *__restrict__ ss, uint32_t nrows,
-                                        unsigned long long s_lo, unsigned long long s_hi,
-                                        const uint32_t *__restrict__ row_q, const uint32_t *__restrict__ row_alo,
-                                        const uint32_t *__restrict__ row_cxy, const int4 *__restrict__ qbox,
-                                        const uint32_t *__restrict__ ecell, const float4 *__restrict__ Q,
-                                        const float4 *__restrict__ frec, float d, float T0, float T1, DevStats *st) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-    const unsigned long long n = s_hi - s_lo;
-    uint32_t pass = 0, tot = 0;
-    if (n) {
-        const unsigned long long sl = s_lo + (unsigned long long)(((unsigned __int128)n * (2 * t + 1)) / (2ull * nt));
-        const uint32_t r = find_row(ss, 0, nrows, sl);
-        const uint32_t i = row_alo[r] + (uint32_t)(sl - ss[r]);
-        const int4 qlo = qbox[2 * row_q[r]];
-        const uint32_t m0 = ecell[i];
-        const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
-        const int rz = max((int)(m0 & 0x3ffu), qlo.z);
-        tot = 1;
-        if (pack_cell(rx, ry, rz) == row_cxy[r]) {
-            const QConst qc = make_qconst(__ldg(Q + 2 * (uint64_t)qlo.w), __ldg(Q + 2 * (uint64_t)qlo.w + 1), T0, T1);
-            pass = filter_pair(make_float4(qc.px, qc.py, qc.pz, qc.t0), make_float4(qc.vx, qc.vy, qc.vz, qc.ext),
-                               qc.t0c, qc.t1c, make_ecand(__ldg(frec + 2 * (uint64_t)i), __ldg(frec + 2 * (uint64_t)i + 1)),
-                               d) ? 1u : 0u;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        pass += __shfl_xor_sync(FULL, pass, o);
-        tot += __shfl_xor_sync(FULL, tot, o);
-    }
-    if ((threadIdx.x & 31) == 0 && tot) {
-        atomicAdd(&st->probe_pass, pass);
-        atomicAdd(&st->probe_total, tot);
-    }
-}
-
-// lane = candidate slot of the flattened (query, cell row) work list; warps grab
-// 32 x SP_PER_LANE consecutive slots at a time (dynamic load balance).
-template <bool EXACT>
-__global__ void __launch_bounds__(PT, SPATIAL_BPS) k_pair_spatial(const __grid_constant__ SpatialArgs A) {
-    __shared__ WarpState sm[PT / 32];
-    const int lane = threadIdx.x & 31;
-    WarpState &W = sm[threadIdx.x >> 5];
-    DevStats *st = A.pc.o.st;
-    const unsigned long long total = A.slot_hi;
-    warp_state_init(W, lane);
-    uint32_t qn = 0;
-    unsigned long long exec = 0, direct_hits = 0;
-    uint32_t cur_p = 0xffffffffu;
-    uint32_t cur_qrow = 0;
-    QConst q = make_qconst(make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 1.f), A.pc.T0, A.pc.T1);
-    int4 qlo = make_int4(0, 0, 0, 0);
-    constexpr int SB = 4;                       // slots per lane per batch (loads hoisted)
-    while (true) {
-        unsigned gi = 0;
-        if (lane == 0) gi = atomicAdd(&st->work_ctr, 1u);
-        gi = __shfl_sync(FULL, gi, 0);
-        const unsigned long long B = A.slot_lo + (unsigned long long)gi * SP_GRAB;
-        if (B >= total) break;
-        const unsigned long long Bend = min(B + SP_GRAB, total);
-        const uint32_t rlo = A.grab_row[gi], rhi = A.grab_row[gi + 1] + 1;
-        // row of this lane's first slot (small search inside the grab's row range);
-        // later slots advance the row linearly (rows are consecutive in slot order)
-        uint32_t r = A.slot_row ? A.slot_row[min(B + lane, Bend - 1) - A.slot_lo]
-                                : find_row(A.slot_start, rlo, rhi, min(B + lane, Bend - 1));
-        unsigned long long r_start = A.slot_start[r], r_next = A.slot_start[r + 1];
-        uint32_t r_alo = A.row_alo[r], r_cxy = A.row_cxy[r], r_p = A.row_q[r];
-        exec += Bend - B;
-#pragma unroll 1
-        for (int u0 = 0; u0 < SP_PER_LANE; u0 += SB) {
-            uint32_t ii[SB], cxy[SB], pp[SB];
-            bool vv[SB];
-#pragma unroll
-            for (int u = 0; u < SB; ++u) {
-                const unsigned long long s = B + (unsigned long long)(u0 + u) * 32 + lane;
-                vv[u] = s < Bend;
-                if (vv[u] && s >= r_next) {
-                    // next item holding slot s (binary search: many (query, cell) items are empty)
-                    r = A.slot_row ? A.slot_row[s - A.slot_lo] : find_row(A.slot_start, r + 1, rhi, s);
-                    r_start = A.slot_start[r];
-                    r_next = A.slot_start[r + 1];
-                    r_alo = A.row_alo[r];
-                    r_cxy = A.row_cxy[r];
-                    r_p = A.row_q[r];
-                }
-                ii[u] = vv[u] ? r_alo + (uint32_t)(s - r_start) : 0u;
-                cxy[u] = r_cxy;
-                pp[u] = r_p;
-            }
-            float4 ea[SB], eb[SB];
-            uint32_t ec[SB];
-#pragma unroll
-            for (int u = 0; u < SB; ++u) {          // coalesced: consecutive slots, consecutive i
-                ea[u] = __ldg(A.pc.rec + 2 * (uint64_t)ii[u]);
-                eb[u] = __ldg(A.pc.rec + 2 * (uint64_t)ii[u] + 1);
-                ec[u] = __ldg(A.ecell + ii[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < SB; ++u) {
-                int kk = 0;
-                if (vv[u]) {
-                    if (pp[u] != cur_p) {
-                        cur_p = pp[u];
-                        qlo = A.qbox[2 * cur_p];
-                        cur_qrow = (uint32_t)qlo.w;
-                        q = make_qconst(__ldg(A.pc.Q + 2 * (uint64_t)cur_qrow),
-                                        __ldg(A.pc.Q + 2 * (uint64_t)cur_qrow + 1), A.pc.T0, A.pc.T1);
-                    }
-                    // duplicate avoidance: test (q, e) only in the first cell (index-space
-                    // min corner) of cells(e) ∩ cells(q) (replaces the host filter of P:558-559)
-                    const uint32_t m0 = ec[u];
-                    const int rx = max((int)(m0 >> 21), qlo.x), ry = max((int)((m0 >> 10) & 0x7ffu), qlo.y);
-                    const int rz = max((int)(m0 & 0x3ffu), qlo.z);
-                    const bool first = pack_cell(rx, ry, rz) == cxy[u];
-                    if (first) kk = filter_pair(make_float4(q.px, q.py, q.pz, q.t0),
-                                                make_float4(q.vx, q.vy, q.vz, q.ext), q.t0c, q.t1c,
-                                                make_ecand(ea[u], eb[u]), A.pc.d) ? 1 : 0;
-                }
-                // passes are queued; the flush classifies (fp32 interval or fp64) 32 at a time
-                queue_add(W, qn, kk == 1, cur_qrow, ii[u], lane);
-            }
-            queue_drain<EXACT>(&A.pc, W, qn, lane);
-        }
-    }
-    __syncwarp();                    // last queue_add writes -> flush reads
-    if (qn) flush_refine<EXACT>(&A.pc, &W, qn);
-    if (W.fn) flush64<EXACT>(&A.pc, &W, W.fn);
-    warp_state_finish<EXACT>(A.pc.o, W, lane);
-    if (lane == 0 && exec) atomicAdd(&st->executed, exec);
-    if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
-}
-
 // ---------------------------------------------------------------------------
 // overflow handling (A10): keep records of complete queries, re-plan the rest
 // ---------------------------------------------------------------------------
@@ -1688,32 +1432,32 @@ __global__ void k_chunk_offsets_u64(const uint32_t *__restrict__ used, uint64_t 
     if (i < n) out[i] = used[i];
 }
 
-// redo flags of schedule entries (range variants) / query list (spatial)
-__global__ void k_redo_flags_sched(const Sched *__restrict__ S, uint32_t n, const uint8_t *__restrict__ redo,
+// overflow re-plan: the schedule entries of the queries in the current batch
+__global__ void k_mark_rows(const uint32_t *__restrict__ rows, uint32_t n, uint8_t *__restrict__ mark) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mark[rows[i]] = 1;
+}
+
+__global__ void k_redo_flags_sched(const Sched *__restrict__ S, uint32_t n, const uint8_t *__restrict__ inbatch,
                                    uint32_t *__restrict__ flag) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) flag[p] = redo[S[p].qid];
+    if (p < n) flag[p] = (S[p].sel != 3 && inbatch[S[p].qid]) ? 1u : 0u;
 }
 
 __global__ void k_compact_sched(const Sched *__restrict__ S, uint32_t n, const uint32_t *__restrict__ flag,
                                 const uint32_t *__restrict__ pos, Sched *__restrict__ out,
-                                const uint32_t *__restrict__ qcount, uint32_t *__restrict__ cnt_out) {
+                                const uint32_t *__restrict__ cell, const uint32_t *__restrict__ qlo,
+                                uint32_t *__restrict__ cell_out, uint32_t *__restrict__ qlo_out) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p < n && flag[p]) {
         out[pos[p]] = S[p];
-        cnt_out[pos[p]] = qcount[S[p].qid];
+        if (cell_out) { cell_out[pos[p]] = cell[p]; qlo_out[pos[p]] = qlo[p]; }
     }
 }
 
-__global__ void k_set_qoff(const Sched *__restrict__ S, uint32_t n, const uint64_t *__restrict__ off,
-                           unsigned long long base, unsigned long long *__restrict__ qoff) {
+__global__ void k_cat_counts(const Sched *__restrict__ S, uint32_t n, DevStats *st) {
     uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) qoff[S[p].qid] = base + off[p];
-}
-
-__global__ void k_u32_to_u64(const uint32_t *__restrict__ a, uint64_t n, uint64_t *__restrict__ b) {
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = a[i];
+    if (p < n) atomicAdd(&st->cat_cnt[S[p].sel + 1], 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -1817,22 +1561,6 @@ __global__ void k_part_bounds(const uint64_t *__restrict__ pre, uint32_t n, uint
     st->pair_tests = pre[hi] - pre[lo];
 }
 
-// GPUSpatial: parts at query granularity; query p's slots start at ss[row_start[p]]
-__global__ void k_part_bounds_spatial(const unsigned long long *__restrict__ ss, const uint32_t *__restrict__ row_start,
-                                      uint32_t n, uint32_t part, uint32_t nparts, DevStats *st) {
-    if (threadIdx.x || blockIdx.x) return;
-    auto f = [&](uint32_t p) { return ss[row_start[p]]; };
-    const unsigned long long total = f(n);
-    const uint32_t lo = part == 0 ? 0u : part_lower_bound(f, n, part_target(total, part, nparts));
-    uint32_t hi = part + 1 >= nparts ? n : part_lower_bound(f, n, part_target(total, part + 1, nparts));
-    if (hi < lo) hi = lo;
-    st->part_lo = lo;
-    st->part_hi = hi;
-    st->part_slot_lo = f(lo);
-    st->part_slot_hi = f(hi);
-    st->pair_tests = f(hi) - f(lo);
-}
-
 inline unsigned nblk(uint64_t n, int nt = 256) { return (unsigned)((n + nt - 1) / nt); }
 
 // ---------------------------------------------------------------------------
@@ -1891,6 +1619,19 @@ int tight_ranges() {
 int fsg_literal() {
     const char *e = getenv("TDS_FSG_LITERAL");
     return (e && e[0] == '1') ? 1 : 0;
+}
+
+template <bool EXACT>
+void launch_range(const RangeArgs &a, cudaStream_t s) {
+    constexpr size_t smem = sizeof(RangeWarpSmem) * (PT / 32);
+    static bool attr_set[64] = {};   // per instantiation and device (first launch)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !attr_set[dev]) {
+        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (dev < 64) attr_set[dev] = true;
+    }
+    k_pair_range<EXACT><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
 }
 
 // build tiles + work items for schedule entries [lo, hi) of the sorted schedule
@@ -1957,8 +1698,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
 
     // ---- A6: queries are validated inside the schedule kernels; GPUTemporal /
     // GPUSpatioTemporal order them by (selector, range start) below, which subsumes
-    // the t_start sort of P:681-682 (range starts are monotone in t_start); FSG
-    // keeps input order
+    // the t_start sort of P:681-682 (range starts are monotone in t_start)
     // TDS_AUTO: schedule GPUSpatioTemporal (counting the GPUTemporal ranges too),
     // then keep whichever plan has the lower estimated cost (below)
     const int req_kind = kind;
@@ -1968,17 +1708,18 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     if (!spatial) { keys = DBuf<uint32_t>(n, s); order = DBuf<uint32_t>(n, s); }
 
     // ---- A7: schedule ---------------------------------------------------------
+    // Every variant ends in a sorted schedule of ns entries (query row, candidate
+    // range, selector) for the pair kernel: one per query for GPUTemporal /
+    // GPUSpatioTemporal (a range of the sorted entries or of X/Y/Z), one per
+    // (query, FSG cell) for GPUSpatial (a time-trimmed slice of the cell-ordered
+    // record copy, with the cell and the query box for the reference-cell rule).
     DBuf<Sched> sched;
+    DBuf<uint32_t> sp_cell, sp_qlo;      // GPUSpatial entries: cell, query-box low corner (packed)
     DBuf<Tile> tiles;
     DBuf<uint32_t> item_start;
     uint32_t ntiles = 0;
-    // spatial work list
-    FsgGrid G{};
-    DBuf<int4> qbox;
-    DBuf<uint32_t> row_start, row_q, row_alo, row_len, row_cxy;
-    DBuf<unsigned long long> slot_start;
-    DBuf<uint32_t> fsg_order;          // GPUSpatial query order (rows of Q)
-    uint32_t nrows = 0;
+    uint32_t ns = n;                     // schedule entries
+    int key_bits = 16;
     if (!spatial) {
         sched = DBuf<Sched>(n, s);
         SchedArgs a{};
@@ -2043,37 +1784,17 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             S.kind = kind;
             return;
         }
-        // sort S by (array selector, range start): one stable radix sort
-        radix_sort_pairs(keys.p, order.p, n, 0, 16, s);
-        {
-            DBuf<Sched> tmp(n, s);
-            k_permute_sched<<<nblk(n), 256, 0, s>>>(sched.p, order.p, n, tmp.p);
-            TDS_CHECK_LAUNCH();
-            std::swap(sched.p, tmp.p);
-        }
-        if (nparts > 1) {
-            // this part's slice of the sorted schedule: equal shares of the exact pair tests
-            DBuf<uint64_t> w(n + 1, s);
-            k_sched_work<<<nblk(n + 1), 256, 0, s>>>(sched.p, n, w.p);
-            TDS_CHECK_LAUNCH();
-            exclusive_scan_u64(w.p, w.p, n + 1, nullptr, s);
-            k_part_bounds<<<1, 32, 0, s>>>(w.p, n, part, nparts, dst.p);
-            TDS_CHECK_LAUNCH();
-            ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s, /*part_range=*/1);
-        } else {
-            ntiles = plan_items(sched.p, 0, n, dst.p, tiles, item_start, s);
-        }
     } else {
+        FsgGrid G{};
         for (int c = 0; c < 3; ++c) { G.o[c] = idx->ext.lo[c]; G.w[c] = idx->w_fsg[c]; G.g[c] = idx->grid[c]; }
-        qbox = DBuf<int4>(2ull * n, s);
-        row_start = DBuf<uint32_t>(n + 1, s);
-        DBuf<uint32_t> nr(n + 1, s);
+        DBuf<int4> qbox(2ull * n, s);
+        DBuf<uint32_t> row_start(n + 1, s), nr(n + 1, s);
         DBuf<unsigned long long> ntot(1, s);
         TDS_CUDA(cudaMemsetAsync(nr.p + n, 0, 4, s));
         TDS_CUDA(cudaMemsetAsync(ntot.p, 0, 8, s));
-        // query order: (t_start, Morton cell of the start point), for L2 reuse of the slices
-        DBuf<uint32_t> kc(n, s), kt(n, s), kt2(n, s);
-        fsg_order = DBuf<uint32_t>(n, s);
+        // query order: (t_start, Morton cell of the start point); equal slices of
+        // queries at the same time end up next to each other after the entry sort
+        DBuf<uint32_t> kc(n, s), kt(n, s), kt2(n, s), fsg_order(n, s);
         k_fsg_order_keys<<<nblk(n), 256, 0, s>>>(Q, n, G, kc.p, kt.p, fsg_order.p);
         TDS_CHECK_LAUNCH();
         radix_sort_pairs(kc.p, fsg_order.p, n, 0, 30, s);
@@ -2086,27 +1807,65 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         unsigned long long items64 = 0;
         TDS_CUDA(cudaMemcpyAsync(&items64, ntot.p, 8, cudaMemcpyDeviceToHost, s));
         TDS_CUDA(cudaStreamSynchronize(s));
-        if (items64 >= (1ull << 32) - 1)
-            fail(TDS_EINVAL, "the d-inflated query boxes cover %llu grid cells (limit 2^32): use a coarser grid",
+        if (items64 >= (1ull << 31))
+            fail(TDS_EINVAL, "the d-inflated query boxes cover %llu grid cells (limit 2^31): use a coarser grid",
                  items64);
-        nrows = (uint32_t)items64;
-        row_q = DBuf<uint32_t>(nrows, s);
-        row_alo = DBuf<uint32_t>(nrows, s);
-        row_len = DBuf<uint32_t>(nrows + 1, s);
-        row_cxy = DBuf<uint32_t>(nrows, s);
-        TDS_CUDA(cudaMemsetAsync(row_len.p + nrows, 0, 4, s));
+        const uint32_t nrows = (uint32_t)items64;
+        DBuf<uint32_t> row_q(nrows, s), row_alo(nrows, s), row_len(nrows + 1, s), row_cxy(nrows, s);
         k_fsg_items<<<nblk((uint64_t)n * 32), 256, 0, s>>>(row_start.p, n, qbox.p, Q, G, idx->cell_off, idx->fsg_rec,
                                                           T0, T1, idx->ext.max_dur, fsg_literal(), row_q.p,
                                                           row_alo.p, row_len.p, row_cxy.p);
         TDS_CHECK_LAUNCH();
-        DBuf<uint64_t> rl64(nrows + 1, s);
-        k_u32_to_u64<<<nblk(nrows + 1), 256, 0, s>>>(row_len.p, nrows + 1, rl64.p);
-        TDS_CHECK_LAUNCH();
-        slot_start = DBuf<unsigned long long>(nrows + 1, s);
-        exclusive_scan_u64(rl64.p, (uint64_t *)slot_start.p, nrows + 1, (uint64_t *)&dst.p->pair_tests, s);
-        if (nparts > 1) {   // this part: the queries whose slots cross equal shares of the total
-            k_part_bounds_spatial<<<1, 32, 0, s>>>(slot_start.p, row_start.p, n, part, nparts, dst.p);
+        // (query, cell) items -> schedule entries, sorted by slice start: the entries
+        // of queries that share a (cell, time) slice form the groups of 32
+        ns = std::max<uint32_t>(nrows, 1u);
+        sched = DBuf<Sched>(ns, s);
+        keys = DBuf<uint32_t>(ns, s);
+        order = DBuf<uint32_t>(ns, s);
+        sp_cell = DBuf<uint32_t>(ns, s);
+        sp_qlo = DBuf<uint32_t>(ns, s);
+        if (nrows == 0) {
+            TDS_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(Sched), s));
+            ns = 0;
+        } else {
+            int lo_bits = 1;
+            while ((1ull << lo_bits) <= idx->A_len) ++lo_bits;     // A_len < 2^31 (build check)
+            key_bits = std::min(lo_bits + 1, 32);
+            k_fsg_sched<<<nblk(nrows), 256, 0, s>>>(nrows, row_q.p, row_alo.p, row_len.p, row_cxy.p, qbox.p,
+                                                    1u << lo_bits, sched.p, keys.p, order.p, sp_cell.p, sp_qlo.p,
+                                                    dst.p);
             TDS_CHECK_LAUNCH();
+        }
+    }
+    if (ns) {
+        // sort the entries by (category, range start): one stable radix sort
+        radix_sort_pairs(keys.p, order.p, ns, 0, key_bits, s);
+        {
+            DBuf<Sched> tmp(ns, s);
+            k_permute_sched<<<nblk(ns), 256, 0, s>>>(sched.p, order.p, ns, tmp.p);
+            TDS_CHECK_LAUNCH();
+            std::swap(sched.p, tmp.p);
+        }
+        if (spatial) {
+            DBuf<uint32_t> tc(ns, s), tq(ns, s);
+            k_gather_u32<<<nblk(ns), 256, 0, s>>>(sp_cell.p, order.p, ns, tc.p);
+            TDS_CHECK_LAUNCH();
+            k_gather_u32<<<nblk(ns), 256, 0, s>>>(sp_qlo.p, order.p, ns, tq.p);
+            TDS_CHECK_LAUNCH();
+            std::swap(sp_cell.p, tc.p);
+            std::swap(sp_qlo.p, tq.p);
+        }
+        if (nparts > 1) {
+            // this part's slice of the sorted schedule: equal shares of the exact pair tests
+            DBuf<uint64_t> w(ns + 1, s);
+            k_sched_work<<<nblk(ns + 1), 256, 0, s>>>(sched.p, ns, w.p);
+            TDS_CHECK_LAUNCH();
+            exclusive_scan_u64(w.p, w.p, ns + 1, nullptr, s);
+            k_part_bounds<<<1, 32, 0, s>>>(w.p, ns, part, nparts, dst.p);
+            TDS_CHECK_LAUNCH();
+            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, s, /*part_range=*/1);
+        } else {
+            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, s);
         }
     }
     tr.mark("schedule");
@@ -2121,16 +1880,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     S.fallback_queries = hs.fallback;
     S.kind = kind;
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
-    unsigned long long slot_lo = 0, slot_hi = hs.pair_tests;   // GPUSpatial slots of this call
-    if (nparts > 1) {
-        if (spatial) {
-            S.n_queries = hs.part_hi - hs.part_lo;
-            slot_lo = hs.part_slot_lo;
-            slot_hi = hs.part_slot_hi;
-        } else {
-            const uint32_t live = (uint32_t)(nq - hs.cat_cnt[4]);
-            S.n_queries = std::min(hs.part_hi, live) > hs.part_lo ? std::min(hs.part_hi, live) - hs.part_lo : 0;
-        }
+    if (nparts > 1 && !spatial) {
+        const uint32_t live = (uint32_t)(nq - hs.cat_cnt[4]);
+        S.n_queries = std::min(hs.part_hi, live) > hs.part_lo ? std::min(hs.part_hi, live) - hs.part_lo : 0;
     }
     // result-size probe (automatic capacity, large searches): the pass fraction of a
     // sample of the pair tests bounds the result count; the pass buffer takes three
@@ -2139,23 +1891,23 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // result and a compaction copy after the pass
     uint64_t est_hits = 0;
     bool probed = false;
-    const unsigned long long probe_pairs = spatial ? slot_hi - slot_lo : hs.pair_tests;
-    if (capacity == 0 && probe_pairs >= CAP_PROBE_MIN) {
+    const float4 *prec = spatial ? idx->fsg_rec : idx->rec;
+    const uint32_t *pperm = spatial ? idx->fsg_perm : idx->perm;
+    if (capacity == 0 && hs.pair_tests >= CAP_PROBE_MIN && ns) {
         TDS_CUDA(cudaMemsetAsync(&dst.p->probe_pass, 0, 8, s));
-        if (!spatial) {
-            k_density_probe<<<32, 256, 0, s>>>(sched.p, n, Q, idx->rec, idx->st_arr[0], idx->st_arr[1],
-                                               idx->st_arr[2], d, T0, T1, dst.p);
-        } else {
-            k_density_probe_spatial<<<32, 256, 0, s>>>(slot_start.p, nrows, slot_lo, slot_hi, row_q.p, row_alo.p,
-                                                       row_cxy.p, qbox.p, idx->fsg_ecell, Q, idx->fsg_rec, d, T0, T1,
-                                                       dst.p);
-        }
+        TDS_CUDA(cudaMemsetAsync(&dst.p->probe_est, 0, 12, s));
+        k_density_probe<<<32, 256, 0, s>>>(sched.p, ns, Q, prec, spatial ? nullptr : idx->st_arr[0],
+                                           spatial ? nullptr : idx->st_arr[1], spatial ? nullptr : idx->st_arr[2], d,
+                                           T0, T1, spatial ? idx->fsg_ecell : nullptr, sp_cell.p, sp_qlo.p, dst.p);
         TDS_CHECK_LAUNCH();
         TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
         TDS_CUDA(cudaStreamSynchronize(s));
-        if (hs.probe_total >= 1024) {
+        if (hs.probe_total >= 1024 && hs.probe_entries) {
+            // unbiased for entries sampled evenly over the schedule: the mean of the
+            // sampled entries' estimated records times the number of entries
             probed = true;
-            est_hits = (uint64_t)((double)probe_pairs * hs.probe_pass / hs.probe_total);
+            const double scale = (double)(nparts > 1 ? hs.part_hi - hs.part_lo : ns) / hs.probe_entries;
+            est_hits = (uint64_t)(hs.probe_est * scale);
         }
         tr.note("probe_est_hits", (double)est_hits);
     }
@@ -2167,8 +1919,17 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         // pools hand out since (abi.cu; no cudaMemGetInfo per search).  Buffers above
         // 1 GB are sized and allocated under a process-wide lock, so concurrent
         // searches (tds_search_many) do not over-commit the device.
-        uint64_t want = probe_pairs + 64;
+        uint64_t want = hs.pair_tests + 64;
         if (probed) want = std::min<uint64_t>(want, 3 * est_hits + CAP_FLOOR);
+        // + one partly filled chunk per warp (chunks of <= 1024 slots are reserved whole),
+        // rounded up to 4 sizes per octave so that later searches reuse the pool's blocks
+        want += (uint64_t)persistent_blocks(RANGE_BPS) * (PT / 32) * 1024;
+        {
+            int e = 0;
+            while ((4ull << e) < want) ++e;
+            const uint64_t q = 1ull << e;                        // want in (4q, 8q]
+            want = (want + q - 1) / q * q;
+        }
         if (want * sizeof(Rec) > (1ull << 30)) big_lock = std::unique_lock<std::mutex>(big_alloc_mutex());
         const uint64_t budget_bytes = device_budget_bytes();
         cap = std::min<uint64_t>(want, (uint64_t)(budget_bytes * 0.45) / sizeof(Rec));
@@ -2176,10 +1937,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         tr.mark(big_lock.owns_lock() ? "budget(locked)" : "budget");
     }
     cap = std::min<uint64_t>(cap, (1ull << 40));
-    const int bps = spatial ? SPATIAL_BPS : RANGE_BPS;
-    const uint64_t nwarps = (uint64_t)persistent_blocks(bps) * (PT / 32);
-    uint32_t CS = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(128, cap / (16 * nwarps)));  // >= 128: appendK
-    CS = (CS + 31) / 32 * 32;
+    const uint64_t nwarps = (uint64_t)persistent_blocks(RANGE_BPS) * (PT / 32);
+    const uint64_t cs_want = std::min<uint64_t>(1024, std::max<uint64_t>(128, cap / (16 * nwarps)));  // >= 128: appendK
+    uint32_t cs_shift = 7;
+    while ((2ull << cs_shift) <= cs_want) ++cs_shift;
+    const uint32_t CS = 1u << cs_shift;             // a power of two: chunk index by shift
     const uint64_t nchunks = (cap + CS - 1) / CS;
     DBuf<Rec> buf;
     for (;;) {
@@ -2201,46 +1963,30 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     TDS_CUDA(cudaMemsetAsync(chunk_used.p, 0, 4 * nchunks, s));
 
     OutArgs o{};
-    o.buf = buf.p; o.cap = cap; o.CS = CS; o.chunk_used = chunk_used.p;
+    o.buf = buf.p; o.cap = cap; o.CS = CS; o.cs_shift = cs_shift; o.chunk_used = chunk_used.p;
     o.redo = redo.p; o.qcount = qcount.p; o.st = dst.p;
+
+    auto range_args = [&](const OutArgs &oo) {
+        RangeArgs a{};
+        a.df = filter_threshold(d);
+        a.tc = time_origin(idx);
+        a.pc = PairCtx{Q, prec, pperm, d, T0, T1, oo, d64, dlo};
+        for (int c = 0; c < 3; ++c) {
+            a.arr[c] = spatial ? nullptr : idx->st_arr[c];
+            a.srec[c] = spatial ? nullptr : idx->st_rec[c];
+        }
+        if (spatial) { a.ecell = idx->fsg_ecell; }
+        return a;
+    };
 
     // ---- A8-A10: pass 1 --------------------------------------------------------
     tr.mark("sync+alloc");
     tm.mark(2);
-    if (!spatial) {
-        RangeArgs a{};
-        a.df = filter_threshold(d);
-        a.tc = time_origin(idx);
-        a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64, dlo};
-        for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
+    if (ns && hs.pair_tests > 0) {
+        RangeArgs a = range_args(o);
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
-        k_pair_range<false><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
-        TDS_CHECK_LAUNCH();
-    } else if (nrows > 0 && hs.pair_tests > 0) {
-        const uint64_t nslots = slot_hi - slot_lo;
-        const uint64_t ngrab = (nslots + SP_GRAB - 1) / SP_GRAB;
-        DBuf<uint32_t> grab_row(ngrab + 1, s);
-        k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(slot_start.p, nrows, slot_lo, slot_hi, ngrab, grab_row.p);
-        TDS_CHECK_LAUNCH();
-        DBuf<uint32_t> slot_row;
-        if (nslots <= SLOT_ROW_MAX) {
-            slot_row = DBuf<uint32_t>(nslots, s);
-            k_slot_rows<<<nblk(nslots), 256, 0, s>>>(slot_start.p, nrows, slot_lo, nslots, slot_row.p);
-            TDS_CHECK_LAUNCH();
-        }
-        SpatialArgs a{};
-        a.slot_row = slot_row.p;
-        a.slot_lo = slot_lo;
-        a.slot_hi = slot_hi;
-        a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64, dlo};
-        a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
-        a.qbox = qbox.p; a.row_q = row_q.p; a.row_alo = row_alo.p; a.row_cxy = row_cxy.p;
-        a.slot_start = slot_start.p; a.nrows = nrows; a.G = G;
-        // persistent grid, but no more blocks than grabs / warps per block: a small
-        // search (Random-1M-shaped: a few hundred grabs) does not launch 444 blocks
-        // that mostly find no work
-        const int sp_blocks = (int)std::min<uint64_t>(persistent_blocks(SPATIAL_BPS), (ngrab + PT / 32 - 1) / (PT / 32));
-        k_pair_spatial<false><<<sp_blocks, PT, 0, s>>>(a);
+        a.sp_cell = sp_cell.p; a.sp_qlo = sp_qlo.p;
+        launch_range<false>(a, s);
         TDS_CHECK_LAUNCH();
     }
     tm.mark(3);
@@ -2305,45 +2051,24 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     exclusive_scan_u64(kept_off.p, kept_off.p, nres + 1, nullptr, s);
     uint64_t nkept = 0;
     TDS_CUDA(cudaMemcpyAsync(&nkept, kept_off.p + nres, 8, cudaMemcpyDeviceToHost, s));
-
-    // redo list with exact counts, in schedule order (range) / input order (spatial)
-    std::vector<uint32_t> hcnt;
-    DBuf<Sched> rsched;
-    DBuf<uint32_t> rlist;              // spatial: redo query rows
-    uint32_t nredo = 0;
-    if (!spatial) {
-        DBuf<uint32_t> flag(n + 1, s), fpos(n + 1, s), cnt(n, s);
-        TDS_CUDA(cudaMemsetAsync(flag.p + n, 0, 4, s));
-        k_redo_flags_sched<<<nblk(n), 256, 0, s>>>(sched.p, n, redo.p, flag.p);
-        TDS_CHECK_LAUNCH();
-        exclusive_scan_u32(flag.p, fpos.p, n + 1, nullptr, s);
-        rsched = DBuf<Sched>(n, s);
-        k_compact_sched<<<nblk(n), 256, 0, s>>>(sched.p, n, flag.p, fpos.p, rsched.p, qcount.p, cnt.p);
-        TDS_CHECK_LAUNCH();
-        TDS_CUDA(cudaMemcpyAsync(&nredo, fpos.p + n, 4, cudaMemcpyDeviceToHost, s));
-        TDS_CUDA(cudaStreamSynchronize(s));
-        hcnt.resize(nredo);
-        if (nredo) TDS_CUDA(cudaMemcpyAsync(hcnt.data(), cnt.p, 4ull * nredo, cudaMemcpyDeviceToHost, s));
-    } else {
-        std::vector<uint8_t> hr(n);
-        std::vector<uint32_t> hq(n);
-        TDS_CUDA(cudaMemcpyAsync(hr.data(), redo.p, n, cudaMemcpyDeviceToHost, s));
-        TDS_CUDA(cudaMemcpyAsync(hq.data(), qcount.p, 4ull * n, cudaMemcpyDeviceToHost, s));
-        TDS_CUDA(cudaStreamSynchronize(s));
-        std::vector<uint32_t> rl;
-        for (uint32_t k = 0; k < n; ++k)
-            if (hr[k]) { rl.push_back(k); hcnt.push_back(hq[k]); }
-        nredo = (uint32_t)rl.size();
-        rlist = DBuf<uint32_t>(nredo, s);
-        if (nredo) TDS_CUDA(cudaMemcpyAsync(rlist.p, rl.data(), 4ull * nredo, cudaMemcpyHostToDevice, s));
-    }
+    // queries to re-run (input order) with their exact record counts
+    std::vector<uint8_t> hr(n);
+    std::vector<uint32_t> hq(n);
+    TDS_CUDA(cudaMemcpyAsync(hr.data(), redo.p, n, cudaMemcpyDeviceToHost, s));
+    TDS_CUDA(cudaMemcpyAsync(hq.data(), qcount.p, 4ull * n, cudaMemcpyDeviceToHost, s));
     TDS_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> rl, hcnt;
     uint64_t redo_total = 0;
-    for (uint32_t c : hcnt) {
-        if (c > cap) fail(TDS_ECAPACITY, "one query produces %u records, more than capacity %llu", c,
-                          (unsigned long long)cap);
-        redo_total += c;
-    }
+    for (uint32_t k = 0; k < n; ++k)
+        if (hr[k]) {
+            if (hq[k] > cap)
+                fail(TDS_ECAPACITY, "one query produces %u records, more than capacity %llu", hq[k],
+                     (unsigned long long)cap);
+            rl.push_back(k);
+            hcnt.push_back(hq[k]);
+            redo_total += hq[k];
+        }
+    const uint32_t nredo = (uint32_t)rl.size();
     const uint64_t total = nkept + redo_total;
     DBuf<Rec> store;
     try {
@@ -2383,133 +2108,72 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     kept_off.reset();
     S.spilled = nkept;
 
-    // per-query exact offsets in redo order
+    // per-query exact offsets (redo order after the kept records)
     DBuf<unsigned long long> qoff(n, s);
     DBuf<uint32_t> qfill(n, s);
     TDS_CUDA(cudaMemsetAsync(qfill.p, 0, 4ull * n, s));
     {
-        std::vector<uint64_t> off(nredo);
+        std::vector<unsigned long long> hoff(n, 0);
         uint64_t acc = nkept;
-        for (uint32_t k = 0; k < nredo; ++k) { off[k] = acc; acc += hcnt[k]; }
-        DBuf<uint64_t> doff(nredo, s);
-        if (nredo) TDS_CUDA(cudaMemcpyAsync(doff.p, off.data(), 8ull * nredo, cudaMemcpyHostToDevice, s));
-        if (!spatial) {
-            if (nredo) k_set_qoff<<<nblk(nredo), 256, 0, s>>>(rsched.p, nredo, doff.p, 0ull, qoff.p);
-        } else {
-            // spatial: scatter offsets by query row
-            std::vector<uint32_t> rl(nredo);
-            if (nredo) TDS_CUDA(cudaMemcpyAsync(rl.data(), rlist.p, 4ull * nredo, cudaMemcpyDeviceToHost, s));
-            TDS_CUDA(cudaStreamSynchronize(s));
-            std::vector<unsigned long long> hq(n, 0);
-            for (uint32_t k = 0; k < nredo; ++k) hq[rl[k]] = off[k];
-            TDS_CUDA(cudaMemcpyAsync(qoff.p, hq.data(), 8ull * n, cudaMemcpyHostToDevice, s));
-        }
-        TDS_CHECK_LAUNCH();
+        for (uint32_t k = 0; k < nredo; ++k) { hoff[rl[k]] = acc; acc += hcnt[k]; }
+        TDS_CUDA(cudaMemcpyAsync(qoff.p, hoff.data(), 8ull * n, cudaMemcpyHostToDevice, s));
         TDS_CUDA(cudaStreamSynchronize(s));
     }
     tm.mark(4);
-    // batches: consecutive redo entries with sum(count) <= cap (paper's incremental
-    // processing of Q)
+    // batches of re-run queries with sum(count) <= cap (the paper's incremental
+    // processing of Q): the schedule entries of the batch's queries
+    // are compacted and re-evaluated, records written at exact per-query offsets
     o.buf = store.p;
     o.qoff = qoff.p;
     o.qfill = qfill.p;
     DBuf<uint32_t> qcount2(n, s);      // counts are recomputed, not needed again
     TDS_CUDA(cudaMemsetAsync(qcount2.p, 0, 4ull * n, s));
     o.qcount = qcount2.p;
+    DBuf<uint8_t> inbatch(n, s);
+    DBuf<uint32_t> dl(std::max<uint32_t>(nredo, 1), s);
+    if (nredo) TDS_CUDA(cudaMemcpyAsync(dl.p, rl.data(), 4ull * nredo, cudaMemcpyHostToDevice, s));
     uint32_t b0 = 0;
     while (b0 < nredo) {
         uint64_t acc = 0;
         uint32_t b1 = b0;
         while (b1 < nredo && acc + hcnt[b1] <= cap) acc += hcnt[b1++];
-        TDS_CUDA(cudaMemsetAsync(&dst.p->work_ctr, 0, 4, s));
-        TDS_CUDA(cudaMemsetAsync(&dst.p->total_slots, 0, 8, s));
-        if (!spatial) {
-            // category counts of the batch: re-derive by planning on the compacted list
-            DBuf<DevStats> bst(1, s);
-            TDS_CUDA(cudaMemsetAsync(bst.p, 0, sizeof(DevStats), s));
-            DBuf<uint32_t> ck(b1 - b0, s);
-            // count categories of [b0, b1)
-            std::vector<Sched> hsched(b1 - b0);
-            TDS_CUDA(cudaMemcpyAsync(hsched.data(), rsched.p + b0, sizeof(Sched) * (b1 - b0),
-                                     cudaMemcpyDeviceToHost, s));
-            TDS_CUDA(cudaStreamSynchronize(s));
-            DevStats hb{};
-            for (auto &e : hsched) hb.cat_cnt[e.sel + 1]++;
-            TDS_CUDA(cudaMemcpyAsync(bst.p, &hb, sizeof hb, cudaMemcpyHostToDevice, s));
+        TDS_CUDA(cudaMemsetAsync(inbatch.p, 0, n, s));
+        k_mark_rows<<<nblk(b1 - b0), 256, 0, s>>>(dl.p + b0, b1 - b0, inbatch.p);
+        TDS_CHECK_LAUNCH();
+        DBuf<uint32_t> flag(ns + 1, s), fpos(ns + 1, s);
+        TDS_CUDA(cudaMemsetAsync(flag.p + ns, 0, 4, s));
+        k_redo_flags_sched<<<nblk(ns), 256, 0, s>>>(sched.p, ns, inbatch.p, flag.p);
+        TDS_CHECK_LAUNCH();
+        exclusive_scan_u32(flag.p, fpos.p, ns + 1, nullptr, s);
+        uint32_t nb = 0;
+        TDS_CUDA(cudaMemcpyAsync(&nb, fpos.p + ns, 4, cudaMemcpyDeviceToHost, s));
+        DBuf<Sched> rsched(std::max<uint32_t>(ns, 1), s);
+        DBuf<uint32_t> rcell, rqlo;
+        if (spatial) { rcell = DBuf<uint32_t>(ns, s); rqlo = DBuf<uint32_t>(ns, s); }
+        k_compact_sched<<<nblk(ns), 256, 0, s>>>(sched.p, ns, flag.p, fpos.p, rsched.p, sp_cell.p, sp_qlo.p, rcell.p,
+                                                 rqlo.p);
+        TDS_CHECK_LAUNCH();
+        // category counts of the batch (for the tile layout)
+        DBuf<DevStats> bst(1, s);
+        TDS_CUDA(cudaMemsetAsync(bst.p, 0, sizeof(DevStats), s));
+        TDS_CUDA(cudaStreamSynchronize(s));
+        if (nb) {
+            k_cat_counts<<<nblk(nb), 256, 0, s>>>(rsched.p, nb, bst.p);
+            TDS_CHECK_LAUNCH();
             DBuf<Tile> bt;
             DBuf<uint32_t> bis;
-            uint32_t bnt = plan_items(rsched.p + b0, 0, b1 - b0, bst.p, bt, bis, s);
-            RangeArgs a{};
-            a.df = filter_threshold(d);
-            a.tc = time_origin(idx);
-            a.pc = PairCtx{Q, idx->rec, idx->perm, d, T0, T1, o, d64, dlo};
+            const uint32_t bnt = plan_items(rsched.p, 0, nb, bst.p, bt, bis, s);
+            RangeArgs a = range_args(o);
             a.pc.o.st = bst.p;
-            for (int c = 0; c < 3; ++c) { a.arr[c] = idx->st_arr[c]; a.srec[c] = idx->st_rec[c]; }
-            a.sched = rsched.p + b0; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
-            k_pair_range<true><<<persistent_blocks(RANGE_BPS), PT, 0, s>>>(a);
+            a.sched = rsched.p; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
+            a.sp_cell = rcell.p; a.sp_qlo = rqlo.p;
+            launch_range<true>(a, s);
             TDS_CHECK_LAUNCH();
             TDS_CUDA(cudaStreamSynchronize(s));
             DevStats hb2;
             TDS_CUDA(cudaMemcpy(&hb2, bst.p, sizeof hb2, cudaMemcpyDeviceToHost));
             S.refined_pairs += hb2.refined;
             S.pairs_executed += hb2.executed;
-        } else {
-            uint32_t nb = b1 - b0;
-            DBuf<int4> bq(2ull * nb, s);
-            DBuf<uint32_t> bnr(nb + 1, s), brs(nb + 1, s);
-            DBuf<unsigned long long> btot(1, s);
-            TDS_CUDA(cudaMemsetAsync(bnr.p + nb, 0, 4, s));
-            TDS_CUDA(cudaMemsetAsync(btot.p, 0, 8, s));
-            k_fsg_count<<<nblk(nb), 256, 0, s>>>(Q, rlist.p + b0, nb, d, T0, T1, G, bnr.p, bq.p, btot.p,
-                                                 &dst.p->bad);
-            TDS_CHECK_LAUNCH();
-            exclusive_scan_u32(bnr.p, brs.p, nb + 1, nullptr, s);
-            uint32_t bnrows = 0;
-            TDS_CUDA(cudaMemcpyAsync(&bnrows, brs.p + nb, 4, cudaMemcpyDeviceToHost, s));
-            TDS_CUDA(cudaStreamSynchronize(s));
-            DBuf<uint32_t> rq(bnrows, s), ra(bnrows, s), rlen(bnrows + 1, s), rc(bnrows, s);
-            TDS_CUDA(cudaMemsetAsync(rlen.p + bnrows, 0, 4, s));
-            k_fsg_items<<<nblk((uint64_t)nb * 32), 256, 0, s>>>(brs.p, nb, bq.p, Q, G, idx->cell_off, idx->fsg_rec, T0,
-                                                                T1, idx->ext.max_dur, fsg_literal(), rq.p, ra.p,
-                                                                rlen.p, rc.p);
-            TDS_CHECK_LAUNCH();
-            DBuf<uint64_t> rl64(bnrows + 1, s);
-            DBuf<unsigned long long> ss(bnrows + 1, s);
-            k_u32_to_u64<<<nblk(bnrows + 1), 256, 0, s>>>(rlen.p, bnrows + 1, rl64.p);
-            TDS_CHECK_LAUNCH();
-            exclusive_scan_u64(rl64.p, (uint64_t *)ss.p, bnrows + 1, nullptr, s);
-            unsigned long long bslots = 0;
-            TDS_CUDA(cudaMemcpyAsync(&bslots, ss.p + bnrows, 8, cudaMemcpyDeviceToHost, s));
-            TDS_CUDA(cudaStreamSynchronize(s));
-            const uint64_t ngrab = (bslots + SP_GRAB - 1) / SP_GRAB;
-            DBuf<uint32_t> grab_row(ngrab + 1, s);
-            k_grab_rows<<<nblk(ngrab + 1), 256, 0, s>>>(ss.p, bnrows, 0ull, bslots, ngrab, grab_row.p);
-            TDS_CHECK_LAUNCH();
-            DBuf<uint32_t> slot_row;
-            if (bslots && bslots <= SLOT_ROW_MAX) {
-                slot_row = DBuf<uint32_t>(bslots, s);
-                k_slot_rows<<<nblk(bslots), 256, 0, s>>>(ss.p, bnrows, 0ull, bslots, slot_row.p);
-                TDS_CHECK_LAUNCH();
-            }
-            SpatialArgs a{};
-            a.slot_row = slot_row.p;
-            a.slot_lo = 0;
-            a.slot_hi = bslots;
-            a.pc = PairCtx{Q, idx->fsg_rec, idx->fsg_perm, d, T0, T1, o, d64, dlo};
-            a.ecell = idx->fsg_ecell; a.cell_off = idx->cell_off; a.grab_row = grab_row.p;
-            a.qbox = bq.p; a.row_q = rq.p; a.row_alo = ra.p; a.row_cxy = rc.p; a.slot_start = ss.p;
-            a.nrows = bnrows; a.G = G;
-            if (bnrows && bslots) {
-                const int sp_blocks =
-                    (int)std::min<uint64_t>(persistent_blocks(SPATIAL_BPS), (ngrab + PT / 32 - 1) / (PT / 32));
-                k_pair_spatial<true><<<sp_blocks, PT, 0, s>>>(a);
-                TDS_CHECK_LAUNCH();
-            }
-            TDS_CUDA(cudaStreamSynchronize(s));
-            DevStats hb2;
-            TDS_CUDA(cudaMemcpy(&hb2, dst.p, sizeof hb2, cudaMemcpyDeviceToHost));
-            S.refined_pairs = hb2.refined;
-            S.pairs_executed = hb2.executed;
         }
         S.passes++;
         b0 = b1;

@@ -518,11 +518,11 @@ def test_tight_range_equals_bin_hull(tds, name, kind, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["tiny", "random-dense-1m"])
-@pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])
-def test_dense4_instantiation_matches_oracle(tds, name, kind, monkeypatch):
-    """The four-candidate dense-window instantiation (chosen by the density probe
-    on large dense searches; forced here with TDS_DENSE4=1 on small ones, with
-    ragged and partial windows) returns the oracle's pair set and intervals."""
+@pytest.mark.parametrize("kind", KINDS)
+def test_dense_windows_match_oracle(tds, name, kind):
+    """Hit-heavy searches run the fused dense-window step (whole-span hits appended
+    at once with [a, b], the rest through the refine queue), with ragged and
+    partial windows: the oracle's pair set and intervals."""
     if name == "tiny":
         w = synth.tiny()
         d = w.d * 3.0
@@ -534,12 +534,9 @@ def test_dense4_instantiation_matches_oracle(tds, name, kind, monkeypatch):
     Q = w.Q[qsel]
     ref = oracle.search(w.D, Q, d)
     idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=w.m_bins, v=w.v_subbins, grid=w.grid)
-    monkeypatch.setenv("TDS_DENSE4", "1")
     got, st = _run(idx, Q, d, kind)
-    monkeypatch.delenv("TDS_DENSE4")
-    base, _ = _run(idx, Q, d, kind)
-    assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(base[0], base[1])))
-    check(got, ref, w.D, Q, d, label=f"{kind} dense4")
+    assert st["n_results"] > 0.15 * st["pair_tests"] or kind == "spatial"    # hit-heavy: dense windows
+    check(got, ref, w.D, Q, d, label=f"{kind} dense windows")
 
 
 @pytest.mark.parametrize("kind", ["temporal", "spatiotemporal"])

@@ -16,4 +16,4 @@ ncu_one() {
 ncu_one ${tag}_ncu_rdense003_t 3 k_pair_range --d 0.03 --variants temporal
 ncu_one ${tag}_ncu_rdense009_t 3 k_pair_range --d 0.09 --variants temporal
 ncu_one ${tag}_ncu_rdense003_st 3 k_pair_range --d 0.03 --variants spatiotemporal
-ncu_one ${tag}_ncu_merger1_spatial 3 k_pair_spatial --config merger --d 1 --variants spatial
+ncu_one ${tag}_ncu_merger1_spatial 3 k_pair_range --config merger --d 1 --variants spatial

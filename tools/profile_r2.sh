@@ -40,6 +40,6 @@ if has ncu; then
   ncu_one rdense003_t 7 k_pair_range
   ncu_one rdense009_t 7 k_pair_range --d 0.09
   ncu_one rdense001_t 7 k_pair_range --d 0.01
-  ncu_one merger1_spatial 2 k_pair_spatial --config merger --variants spatial
+  ncu_one merger1_spatial 2 k_pair_range --config merger --variants spatial
 fi
 ls $out | head -100
