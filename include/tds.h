@@ -77,7 +77,17 @@ typedef struct {
     int32_t v_subbins;  /* v, spatial subbins per dimension per bin, 1 <= v <= floor(extent_c /
                            max per-segment extent_c) for c = x,y,z */
     int32_t grid[3];    /* FSG cells per dimension, >= 1 (50 each in P:1391) */
+    uint32_t flags;     /* 0, or TDS_INDEX_TIME_ORDER (below) */
 } tds_index_params;
+
+/* tds_index_params.flags.  The build renumbers D.  Default: by
+ * temporal bin, and inside a bin by the Morton code of the segment's start cell on
+ * a 1024^3 grid over D's extent, so that the range
+ * kernel's candidate windows are spatially compact and whole windows can be
+ * rejected against a query's box.  TDS_INDEX_TIME_ORDER: by t_start as the paper
+ * states (every bin, range and result is the same; only the order of the entries
+ * inside a bin differs). */
+enum { TDS_INDEX_TIME_ORDER = 1 };
 
 typedef struct tds_index_s *tds_index;
 typedef struct tds_result_s *tds_result;

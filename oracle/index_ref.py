@@ -36,6 +36,43 @@ def temporal_sort(D: np.ndarray):
     return D[perm], perm
 
 
+def morton30(cx, cy, cz) -> np.ndarray:
+    """Morton (Z-order) code of 10-bit cell coordinates: bit k of x, y, z at bits
+    3k + 2, 3k + 1, 3k."""
+    cx, cy, cz = (np.asarray(c, np.int64) for c in (cx, cy, cz))
+    code = np.zeros(np.broadcast(cx, cy, cz).shape, np.int64)
+    for k in range(10):
+        code |= ((cx >> k) & 1) << (3 * k + 2)
+        code |= ((cy >> k) & 1) << (3 * k + 1)
+        code |= ((cz >> k) & 1) << (3 * k)
+    return code
+
+
+def bin_of(D: np.ndarray, m: int) -> np.ndarray:
+    """Temporal bin of every entry (C12): clamp(floor((t_start - t_min) / b), 0, m - 1),
+    b = (t_max - t_min) / m, in fp64."""
+    t0 = D[:, 3].astype(np.float64)
+    t_min, t_max = t0.min(), D[:, 7].astype(np.float64).max()
+    b = (t_max - t_min) / m
+    if not b > 0:
+        b = 1.0
+    return np.clip(np.floor((t0 - t_min) / b), 0, m - 1).astype(np.int64)
+
+
+def spatial_sort(D: np.ndarray, m: int):
+    """The build's default renumbering (the paper's
+    renumbering by t_start, is ``temporal_sort``): by temporal bin,
+    then by the Morton code of the start point's cell on a 1024^3 grid over D's
+    extent (cells decided in fp32, C29); stable, so ties keep the input order.
+    Every bin holds the same entries as under ``temporal_sort``.
+    Returns (D_sorted, perm) with D_sorted[i] = D[perm[i]]."""
+    o, w = grid_geometry(D, (1024, 1024, 1024))
+    cells = [np.array([slab_of(x, o[c], w[c], 1024) for x in D[:, c]]) for c in range(3)]
+    key = morton30(*cells)
+    perm = np.lexsort((np.arange(D.shape[0]), key, bin_of(D, m)))
+    return D[perm], perm
+
+
 def temporal_bins(D_sorted: np.ndarray, m: int):
     """Bins B_j = (B_j^start, B_j^end, B_j^first, B_j^last), j = 0..m-1.
 
@@ -211,13 +248,13 @@ def st_arrays(D_sorted: np.ndarray, bin_of: np.ndarray, m: int, v: int, origin, 
 
 
 def plan(D: np.ndarray, Q: np.ndarray, d: float, m: int, v: int, kind: str = "spatiotemporal",
-         window=(-np.inf, np.inf)):
+         window=(-np.inf, np.inf), order: str = "time"):
     """The schedule entry of every query in the layout
     of tds_plan: (sel, lo, hi) with sel = -1 for the temporal range [lo, hi) of
     sorted entries (GPUTemporal, or the GPUSpatioTemporal fallback), 0/1/2 for
     the range [lo, hi) of X/Y/Z, 3 for no candidates (lo = hi = 0).  Queries
     are clipped to the window and need t0 < t1 after clipping (C5, C8)."""
-    Ds, _ = temporal_sort(D)
+    Ds, _ = temporal_sort(D) if order == "time" else spatial_sort(D, m)
     b = temporal_bins(Ds, m)
     bin_of = b["bin_of"]
     off = np.searchsorted(bin_of, np.arange(m + 1), side="left")        # bin j = sorted ids [off[j], off[j+1])
@@ -302,7 +339,8 @@ def rasterize(mbb_min, mbb_max, origin, width, grid):
 
 def fsg_build(D: np.ndarray, grid, origin, width):
     """G (non-empty cells (h, A_min, A_max) sorted by h) and lookup array A
-    (P:296-299).  Entry ids inside a cell ascending."""
+    (P:296-299).  Entry ids inside a cell by (t_start, id), the order
+    the per-cell time trimming needs (ascending id when D is sorted by t_start)."""
     cells = {}
     for e in range(D.shape[0]):
         mn = np.minimum(D[e, 0:3], D[e, 4:7]).astype(np.float64)
@@ -311,8 +349,9 @@ def fsg_build(D: np.ndarray, grid, origin, width):
             cells.setdefault(linearize(x, y, z, grid), []).append(e)
     G, A = [], []
     for h in sorted(cells):
-        G.append((h, len(A), len(A) + len(cells[h]) - 1))
-        A.extend(cells[h])
+        ids = sorted(cells[h], key=lambda e: (float(D[e, 3]), e))
+        G.append((h, len(A), len(A) + len(ids) - 1))
+        A.extend(ids)
     return np.array(G, dtype=np.int64).reshape(-1, 3), np.array(A, dtype=np.int64)
 
 

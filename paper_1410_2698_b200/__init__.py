@@ -54,7 +54,10 @@ class _SearchReq(ctypes.Structure):
 
 class _Params(ctypes.Structure):
     _fields_ = [("kinds", ctypes.c_uint32), ("m_bins", ctypes.c_int32), ("v_subbins", ctypes.c_int32),
-                ("grid", ctypes.c_int32 * 3)]
+                ("grid", ctypes.c_int32 * 3), ("flags", ctypes.c_uint32)]
+
+
+TIME_ORDER = 1      # tds_index_params.flags: renumber D by t_start (the paper) instead of (bin, Morton)
 
 
 class _Stats(ctypes.Structure):
@@ -169,9 +172,11 @@ def _u32(x):
 class Index:
     """Resident index over the database D (tds_build_index, §4)."""
 
-    def __init__(self, entries, kinds: int = ALL, m: int = 1000, v: int = 1, grid=(50, 50, 50), stream=None):
+    def __init__(self, entries, kinds: int = ALL, m: int = 1000, v: int = 1, grid=(50, 50, 50), stream=None,
+                 time_order: bool = False):
         lib = load_library()
-        p = _Params(int(kinds), int(m), int(v), (ctypes.c_int32 * 3)(*[int(g) for g in grid]))
+        p = _Params(int(kinds), int(m), int(v), (ctypes.c_int32 * 3)(*[int(g) for g in grid]),
+                    TIME_ORDER if time_order else 0)
         ptr, n, keep = _segments(entries)
         h = ctypes.c_void_p()
         _check(lib.tds_build_index(ptr, n, ctypes.byref(p), _stream_ptr(stream), ctypes.byref(h)))

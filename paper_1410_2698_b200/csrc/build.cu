@@ -104,6 +104,32 @@ __global__ void k_time_keys(const float4 *__restrict__ rec, uint64_t n, uint32_t
     }
 }
 
+// spatial renumbering (default order): key of input row i = (temporal bin, Morton
+// code of the start point's cell on a 1024^3 grid over D's extent)
+__device__ __forceinline__ uint32_t spread3b(uint32_t x) {       // 10 bits -> every third bit
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__global__ void k_gather_keys(const uint32_t *__restrict__ src, const uint32_t *__restrict__ idx, uint64_t n,
+                              uint32_t *__restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = src[idx[i]];
+}
+
+__global__ void k_fsg_tkeys(const float4 *__restrict__ rec, const uint32_t *__restrict__ ent, uint64_t len,
+                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) {
+        keys[i] = float_key(rec[2 * (uint64_t)ent[i]].w);
+        vals[i] = (uint32_t)i;
+    }
+}
+
 __global__ void k_gather_records(const float4 *__restrict__ src, const uint32_t *__restrict__ perm, uint64_t n,
                                  float4 *__restrict__ dst) {
     uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one float4 per thread
@@ -134,20 +160,65 @@ __global__ void k_bucket_offsets(const uint32_t *__restrict__ key, uint64_t n, u
     for (int64_t k = prev + 1; k <= cur; ++k) off[k] = (uint32_t)i;
 }
 
-// A3: per bin, one warp reduces max t_end over its members; lo = first member t_start
+// A3: per bin, one warp reduces max t_end and min t_start over its members
+// (+inf / -inf for an empty bin; the min is suffix-filled afterwards)
 __global__ void k_bin_extents(const float4 *__restrict__ rec, uint64_t n, const uint32_t *__restrict__ off, int m,
                               float *__restrict__ bin_lo, float *__restrict__ bin_hi) {
     int j = (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     if (j >= m) return;
     uint32_t a = off[j], b = off[j + 1];
-    float hmax = -INFINITY;
-    for (uint32_t i = a + lane; i < b; i += 32) hmax = fmaxf(hmax, rec[2 * (uint64_t)i + 1].w);
+    float hmax = -INFINITY, lmin = INFINITY;
+    for (uint32_t i = a + lane; i < b; i += 32) {
+        hmax = fmaxf(hmax, rec[2 * (uint64_t)i + 1].w);
+        lmin = fminf(lmin, rec[2 * (uint64_t)i].w);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+    }
     if (lane == 0) {
         bin_hi[j] = hmax;
-        bin_lo[j] = (a < n) ? rec[2 * (uint64_t)a].w : INFINITY;   // empty bins: next bin's first
+        bin_lo[j] = lmin;
+    }
+}
+
+// lo_j = min over bins j' >= j of the members' min t_start (empty bins take the
+// next non-empty bin's; non-decreasing in j), single block of 1024 threads
+__global__ void __launch_bounds__(1024) k_suffix_min(float *__restrict__ lo, int m) {
+    __shared__ float wmin[32];
+    __shared__ float carry_s;
+    if (threadIdx.x == 0) carry_s = INFINITY;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < m; b0 += 1024) {
+        const int k = m - 1 - (b0 + threadIdx.x);                  // walk from the end
+        float x = (k >= 0) ? lo[k] : INFINITY;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = fminf(x, y);
+        }
+        if (lane == 31) wmin[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            float y = wmin[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y = fminf(y, z);
+            }
+            wmin[lane] = y;
+        }
+        __syncthreads();
+        const float carry = carry_s;
+        float r = fminf(x, carry);
+        if (w > 0) r = fminf(r, wmin[w - 1]);
+        if (k >= 0) lo[k] = r;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = r;
+        __syncthreads();
     }
 }
 
@@ -226,6 +297,21 @@ struct StGeom {
     float o[3], w[3];
     int v;
 };
+
+__global__ void k_bin_cell_keys(const float4 *__restrict__ rec, uint64_t n, double t_min, double b, int m,
+                                StGeom M, uint32_t *__restrict__ kb, uint32_t *__restrict__ km,
+                                uint32_t *__restrict__ vals) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 a = rec[2 * i];
+    const double j = floor(((double)a.w - t_min) / b);                 // the bin formula of k_bin_of
+    kb[i] = (uint32_t)(j < 0.0 ? 0 : (j >= (double)m ? m - 1 : (int)j));
+    const uint32_t cx = (uint32_t)cell_of(a.x, M.o[0], M.w[0], 1024), cy = (uint32_t)cell_of(a.y, M.o[1], M.w[1], 1024),
+                   cz = (uint32_t)cell_of(a.z, M.o[2], M.w[2], 1024);
+    km[i] = (spread3b(cx) << 2) | (spread3b(cy) << 1) | spread3b(cz);
+    vals[i] = (uint32_t)i;
+}
+
 
 __global__ void k_count_all(const float4 *__restrict__ rec, uint64_t n, int want_st, StGeom S, int want_fsg,
                             Grid3 G, uint32_t *__restrict__ cx, uint32_t *__restrict__ cy,
@@ -393,10 +479,32 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
 
     tr.mark("validate+sync");
     // ---- A2: stable radix sort by t_start, renumber, gather -----------------
+    // (default: by temporal bin, then Morton code of the start cell; TDS_INDEX_TIME_ORDER:
+    // by t_start; both stable, so ties keep the input order)
+    const int m = idx->m;
+    double t_min = E.t_min, b = ((double)E.t_max - (double)E.t_min) / (double)m;
+    if (!(b > 0.0)) b = 1.0;
+    idx->time_order = (p->flags & TDS_INDEX_TIME_ORDER) != 0;
     DBuf<uint32_t> keys(n, s), perm(n, s);
-    k_time_keys<<<nblk(n), NT, 0, s>>>(in, n, keys.p, perm.p);
-    TDS_CHECK_LAUNCH();
-    radix_sort_pairs(keys.p, perm.p, n, 0, 32, s);
+    if (idx->time_order) {
+        k_time_keys<<<nblk(n), NT, 0, s>>>(in, n, keys.p, perm.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(keys.p, perm.p, n, 0, 32, s);
+    } else {
+        StGeom M{};
+        for (int c = 0; c < 3; ++c) {
+            const float ext = E.hi[c] - E.lo[c];
+            M.o[c] = E.lo[c];
+            M.w[c] = ext > 0.f ? ext / 1024.f : 1.0f;
+        }
+        DBuf<uint32_t> km(n, s), kb2(n, s);
+        k_bin_cell_keys<<<nblk(n), NT, 0, s>>>(in, n, t_min, b, m, M, keys.p, km.p, perm.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(km.p, perm.p, n, 0, 30, s);
+        k_gather_keys<<<nblk(n), NT, 0, s>>>(keys.p, perm.p, n, kb2.p);
+        TDS_CHECK_LAUNCH();
+        radix_sort_pairs(kb2.p, perm.p, n, 0, bits_for((uint64_t)m), s);
+    }
     DBuf<float4> rec(2 * n, s);
     k_gather_records<<<nblk(2 * n), NT, 0, s>>>(in, perm.p, n, rec.p);
     TDS_CHECK_LAUNCH();
@@ -404,9 +512,6 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
 
     tr.mark("tsort+gather");
     // ---- A3: temporal bins ---------------------------------------------------
-    const int m = idx->m;
-    double t_min = E.t_min, b = ((double)E.t_max - (double)E.t_min) / (double)m;
-    if (!(b > 0.0)) b = 1.0;
     DBuf<uint32_t> bin(n, s), bin_off(m + 1, s);
     DBuf<float> bin_lo(m, s), bin_hi(m, s), bin_pmhi(m, s);
     k_bin_of<<<nblk(n), NT, 0, s>>>(rec.p, n, t_min, b, m, bin.p);
@@ -416,6 +521,8 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     k_bin_extents<<<nblk((uint64_t)m * 32), NT, 0, s>>>(rec.p, n, bin_off.p, m, bin_lo.p, bin_hi.p);
     TDS_CHECK_LAUNCH();
     k_prefix_max<<<1, 1024, 0, s>>>(bin_hi.p, bin_pmhi.p, m);
+    TDS_CHECK_LAUNCH();
+    k_suffix_min<<<1, 1024, 0, s>>>(bin_lo.p, m);
     TDS_CHECK_LAUNCH();
 
     tr.mark("bins");
@@ -546,6 +653,21 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     if (want_fsg) {
         const unsigned long long len = tot[3];
         DBuf<uint32_t> off(ncell + 1, s);
+        if (!idx->time_order && len > 1) {
+            // the cells' entries in t_start order (the per-cell time trimming of the
+            // search binary-searches it): stable sort by t_start before the stable
+            // grouping by cell (the sorted D is in (bin, Morton) order)
+            DBuf<uint32_t> tk(len, s), ix(len, s), k2(len, s), v2(len, s);
+            k_fsg_tkeys<<<nblk(len), NT, 0, s>>>(rec.p, fv.p, len, tk.p, ix.p);
+            TDS_CHECK_LAUNCH();
+            radix_sort_pairs(tk, ix, len, 0, 32, s);
+            k_gather_keys<<<nblk(len), NT, 0, s>>>(fk.p, ix.p, len, k2.p);
+            TDS_CHECK_LAUNCH();
+            k_gather_keys<<<nblk(len), NT, 0, s>>>(fv.p, ix.p, len, v2.p);
+            TDS_CHECK_LAUNCH();
+            std::swap(fk.p, k2.p);
+            std::swap(fv.p, v2.p);
+        }
         group_by_key(fk, fv, len, ncell, off.p, s);
         fk.reset();
         DBuf<uint32_t> ecell(len, s);

@@ -94,6 +94,16 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
+// Morton interleave helper: 10 bits -> every third bit
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
 // ---------------------------------------------------------------------------
 // A9: pair test
 // ---------------------------------------------------------------------------
@@ -267,6 +277,39 @@ __device__ __forceinline__ void filter_abs2(float4 n0, float4 n1, float t0c, flo
     upk2(thr2, r0, r1);
     pass0 = (a0 <= b0) & (h0 <= r0);
     pass1 = (a1 <= b1) & (h1 <= r1);
+}
+
+// filter_abs2 for a stationary query (P1 = P0: the supernova case (i) of
+// P:84-88, a point over a time interval): V = -v_e exactly, so
+// A = |v_e|^2 and its reciprocal rA are per-candidate terms computed once per
+// window (rA packed for the pair), and B, t*, y lose the query-velocity terms.
+// Every operation rounds to the same value as in filter_abs2 (negation is exact),
+// so the decisions are bit-identical to the general filter's.
+__device__ __forceinline__ void filter_static2(float4 n0, float t0c, float t1c, const FSeg2 &e, f32x2 rA, float df,
+                                               bool &pass0, bool &pass1) {
+    const float a0 = fmaxf(t0c, e.t0a), b0 = fminf(t1c, e.t1a);
+    const float a1 = fmaxf(t0c, e.t0b), b1 = fminf(t1c, e.t1b);
+    const f32x2 Cx = sub2(bc2(n0.x), e.cx), Cy = sub2(bc2(n0.y), e.cy), Cz = sub2(bc2(n0.z), e.cz);
+    const f32x2 nB = fma2(Cx, e.vx, fma2(Cy, e.vy, mul2(Cz, e.vz)));       // -(C.V)
+    float u0, u1;
+    upk2(mul2(nB, rA), u0, u1);                                              // -(C.V)/A
+    const float s0 = fminf(fmaxf(u0, a0), b0), s1 = fminf(fmaxf(u1, a1), b1);
+    const f32x2 nt = pk2(-s0, -s1);
+    const f32x2 yx = fma2(nt, e.vx, Cx), yy = fma2(nt, e.vy, Cy), yz = fma2(nt, e.vz, Cz);
+    const f32x2 h = fma2(yx, yx, fma2(yy, yy, mul2(yz, yz)));
+    const f32x2 thr = fma2(bc2(KU), add2(bc2(n0.w), e.m), bc2(df));
+    float h0, h1, r0, r1;
+    upk2(h, h0, h1);
+    upk2(mul2(thr, thr), r0, r1);
+    pass0 = (a0 <= b0) & (h0 <= r0);
+    pass1 = (a1 <= b1) & (h1 <= r1);
+}
+
+// reciprocal of |v|^2 for the two candidates of e (stationary queries)
+__device__ __forceinline__ f32x2 static_rA(const FSeg2 &e) {
+    float A0, A1;
+    upk2(fma2(e.vx, e.vx, fma2(e.vy, e.vy, mul2(e.vz, e.vz))), A0, A1);
+    return pk2(rcp_approx(A0), rcp_approx(A1));
 }
 
 // filter_abs2 plus the whole-span test of dense windows: in0 / in1 = both ends of
@@ -648,6 +691,7 @@ struct SchedArgs {
     uint32_t *keys;                  // sort keys: category << 13 | lo >> lo_shift (16 bits)
     uint32_t *vals;                  // identity (sort payload)
     int lo_shift;
+    float mo[3], mw[3];              // Morton grid (1024 cells per dimension over D's extent)
     int count_t;                     // TDS_AUTO: also sum the temporal ranges (pair_tests_t)
     const float4 *rec;               // sorted entries (tight ranges)
     int tight;                       // trim the bin hull to entry-exact ends
@@ -742,7 +786,14 @@ __global__ void k_schedule(SchedArgs A) {
             }
         }
         A.out[p] = S;
-        A.keys[p] = ((uint32_t)(S.sel + 1) << 13) | (S.lo >> A.lo_shift);
+        // sort key: category, range start (top 13 bits), then the Morton code of the
+        // query's start cell (top 16 of 30 bits): the groups of 32 consecutive
+        // entries are then compact in space as well, which the window boxes exploit
+        const uint32_t mx = (uint32_t)cell_of(a.x, A.mo[0], A.mw[0], 1024),
+                       my = (uint32_t)cell_of(a.y, A.mo[1], A.mw[1], 1024),
+                       mz = (uint32_t)cell_of(a.z, A.mo[2], A.mw[2], 1024);
+        const uint32_t mort = (spread3(mx) << 2) | (spread3(my) << 1) | spread3(mz);
+        A.keys[p] = ((uint32_t)(S.sel + 1) << 29) | ((S.lo >> A.lo_shift) << 16) | (mort >> 14);
         A.vals[p] = p;
         atomicAdd(&A.st->cat_cnt[S.sel + 1], 1u);
     }
@@ -850,6 +901,8 @@ struct RangeArgs {
     // cell-ordered record copy): per entry its cell and the query box's low corner
     // (packed), per candidate the min cell of its MBB; null for the range variants
     const uint32_t *sp_cell, *sp_qlo, *ecell;
+    int static_ok;                   // stationary-query filter allowed (default; TDS_NO_STATIC=1: off)
+    int hyst_hi, hyst_lo;            // dense-window hysteresis, % of a window's evaluated pairs passing
 };
 
 // GPUSpatial duplicate avoidance (replaces the host filter of P:558-559): a pair
@@ -919,6 +972,7 @@ struct __align__(16) RangeWarpSmem {
     uint32_t cnt[32];                // records of slot g found by the refine path in this work item
     float4 craw[4][32];              // dense windows: (t0, t1, entry row, min cell) of lane's candidate k
     uint32_t spc[32], spq[32];       // GPUSpatial: cell and query-box low corner of slot g
+    float4 qb[32][2];                // slot g's d-inflated box: (lo, t0c) (hi, t1c)
     uint32_t qn;                     // refine queue fill
 };
 
@@ -968,6 +1022,45 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
         qn -= 32;
         range_refine<EXACT>(A, &W, 32, qn);
     }
+}
+
+// Window box: the bounding box and time span of the
+// window's valid candidates (segment MBBs); a query whose d-inflated box (rounded
+// outward) misses it in some dimension, or whose window-clipped span misses
+// the candidates' span (C5), has no pair within d in the window and is skipped
+// for the whole window.  With the default index order (temporal bin, then Morton
+// code) a window of 128 consecutive candidates is spatially compact.
+struct WBox {
+    float lx, ly, lz, hx, hy, hz, t0, t1;
+};
+
+__device__ __forceinline__ void wbox_init(WBox &w) {
+    w.lx = w.ly = w.lz = w.t0 = INFINITY;
+    w.hx = w.hy = w.hz = w.t1 = -INFINITY;
+}
+
+__device__ __forceinline__ void wbox_add(WBox &w, float4 a, float4 b, bool v) {
+    if (!v) return;
+    w.lx = fminf(w.lx, fminf(a.x, b.x)); w.hx = fmaxf(w.hx, fmaxf(a.x, b.x));
+    w.ly = fminf(w.ly, fminf(a.y, b.y)); w.hy = fmaxf(w.hy, fmaxf(a.y, b.y));
+    w.lz = fminf(w.lz, fminf(a.z, b.z)); w.hz = fmaxf(w.hz, fmaxf(a.z, b.z));
+    w.t0 = fminf(w.t0, a.w); w.t1 = fmaxf(w.t1, b.w);
+}
+
+__device__ __forceinline__ float key_to_float(uint32_t k) {     // inverse of float_key
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ float wmin(float x) { return key_to_float(__reduce_min_sync(FULL, float_key(x))); }
+__device__ __forceinline__ float wmax(float x) { return key_to_float(__reduce_max_sync(FULL, float_key(x))); }
+
+// warp-wide: bit g set iff slot g's box (qlo = (lo, t0c), qhi = (hi, t1c)) meets the window box
+__device__ __forceinline__ unsigned wbox_overlap(const WBox &w, float4 qlo, float4 qhi, bool active) {
+    // every lane takes part in every reduction (no short-circuit around redux.sync)
+    const float hx = wmax(w.hx), lx = wmin(w.lx), hy = wmax(w.hy), ly = wmin(w.ly), hz = wmax(w.hz),
+                lz = wmin(w.lz), t1 = wmax(w.t1), t0 = wmin(w.t0);
+    const bool ov = active & (qlo.x <= hx) & (qhi.x >= lx) & (qlo.y <= hy) & (qhi.y >= ly) & (qlo.z <= hz) &
+                    (qhi.z >= lz) & (qlo.w < t1) & (qhi.w > t0);
+    return __ballot_sync(FULL, ov);
 }
 
 // Mapping: a work item is a group of <= 32
@@ -1034,6 +1127,10 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 W.spc[lane] = active ? A.sp_cell[p] : 0xffffffffu;
                 W.spq[lane] = active ? A.sp_qlo[p] : 0u;
             }
+            W.qb[lane][0] = make_float4(__fsub_rd(fminf(qa.x, qb.x), A.pc.d), __fsub_rd(fminf(qa.y, qb.y), A.pc.d),
+                                        __fsub_rd(fminf(qa.z, qb.z), A.pc.d), qc.t0c);
+            W.qb[lane][1] = make_float4(__fadd_ru(fmaxf(qa.x, qb.x), A.pc.d), __fadd_ru(fmaxf(qa.y, qb.y), A.pc.d),
+                                        __fadd_ru(fmaxf(qa.z, qb.z), A.pc.d), qc.t1c);
             __syncwarp();
         }
         uint32_t wlo = my_lo, whi = my_hi;
@@ -1041,6 +1138,13 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         for (int o = 16; o > 0; o >>= 1) {
             wlo = min(wlo, __shfl_xor_sync(FULL, wlo, o));
             whi = max(whi, __shfl_xor_sync(FULL, whi, o));
+        }
+        // every query of the group stationary (P1 = P0): the sparse windows use
+        // filter_static2 (TDS_NO_STATIC=1 disables it, for the A/B)
+        bool stat = false;
+        {
+            const bool st_q = !active || (__float_as_uint(W.q[lane][1].w) == 0u);   // |v|_1 == +0
+            stat = A.static_ok && __all_sync(FULL, st_q);
         }
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
         uint32_t owner_hits = 0;             // whole-span hits of this lane's query slot (dense path)
@@ -1073,8 +1177,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             // ---- worker side: lane = candidate
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
-            exec += (unsigned long long)(cend - base) * __popc(mask);
             uint32_t wpass = 0;                // filter passes of this window (all queries)
+            WBox wb;
+            wbox_init(wb);
+            unsigned mask_eval = 0;            // queries evaluated in this window
+            // queries whose box misses the window box: skipped for the whole window
+            auto box_skip = [&]() {
+                mask &= wbox_overlap(wb, W.qb[lane][0], W.qb[lane][1], (wmask >> lane) & 1u);
+                mask_eval = mask;
+                exec += (unsigned long long)(cend - base) * __popc(mask);
+            };
             if (dense) {
                 // fused step: the filter and the whole-span test for the lane's four
                 // candidates (two packed pairs); whole-span hits are appended at once
@@ -1086,6 +1198,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     float4 a0, b0, a1, b1;
                     load_cand(c0, c0 < cend, j0, a0, b0);
                     load_cand(c1, c1 < cend, j1, a1, b1);
+                    wbox_add(wb, a0, b0, c0 < cend);
+                    wbox_add(wb, a1, b1, c1 < cend);
                     f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
                     W.craw[0][lane] = make_float4(a0.w, b0.w, __uint_as_float(c0 < cend ? __ldg(A.pc.perm + j0) : 0u),
                                                   __uint_as_float(A.ecell && c0 < cend ? __ldg(A.ecell + j0) : 0u));
@@ -1093,12 +1207,15 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                                                   __uint_as_float(A.ecell && c1 < cend ? __ldg(A.ecell + j1) : 0u));
                     load_cand(c2, c2 < cend, j2, a0, b0);
                     load_cand(c3, c3 < cend, j3, a1, b1);
+                    wbox_add(wb, a0, b0, c2 < cend);
+                    wbox_add(wb, a1, b1, c3 < cend);
                     f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
                     W.craw[2][lane] = make_float4(a0.w, b0.w, __uint_as_float(c2 < cend ? __ldg(A.pc.perm + j2) : 0u),
                                                   __uint_as_float(A.ecell && c2 < cend ? __ldg(A.ecell + j2) : 0u));
                     W.craw[3][lane] = make_float4(a1.w, b1.w, __uint_as_float(c3 < cend ? __ldg(A.pc.perm + j3) : 0u),
                                                   __uint_as_float(A.ecell && c3 < cend ? __ldg(A.ecell + j3) : 0u));
                 }
+                box_skip();
                 while (mask) {
                     const int g = __ffs(mask) - 1;
                     mask &= mask - 1;
@@ -1160,19 +1277,31 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     float4 a0, b0, a1, b1;
                     load_cand(c0, c0 < cend, j0, a0, b0);
                     load_cand(c1, c1 < cend, j1, a1, b1);
+                    wbox_add(wb, a0, b0, c0 < cend);
+                    wbox_add(wb, a1, b1, c1 < cend);
                     f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
                     load_cand(c2, c2 < cend, j2, a0, b0);
                     load_cand(c3, c3 < cend, j3, a1, b1);
+                    wbox_add(wb, a0, b0, c2 < cend);
+                    wbox_add(wb, a1, b1, c3 < cend);
                     f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
                 }
+                box_skip();
+                f32x2 rA01 = 0ull, rA23 = 0ull;
+                if (stat) { rA01 = static_rA(f01); rA23 = static_rA(f23); }
                 while (mask) {
                     const int g = __ffs(mask) - 1;
                     mask &= mask - 1;
                     const float4 n0 = W.q[g][3], n1 = W.q[g][4], n2 = W.q[g][5];
                     const uint32_t glo = __float_as_uint(n2.y), ghi = __float_as_uint(n2.z);
                     bool m0, m1, m2, m3;
-                    filter_abs2(n0, n1, n1.w, n2.x, f01, df, m0, m1);
-                    filter_abs2(n0, n1, n1.w, n2.x, f23, df, m2, m3);
+                    if (stat) {
+                        filter_static2(n0, n1.w, n2.x, f01, rA01, df, m0, m1);
+                        filter_static2(n0, n1.w, n2.x, f23, rA23, df, m2, m3);
+                    } else {
+                        filter_abs2(n0, n1, n1.w, n2.x, f01, df, m0, m1);
+                        filter_abs2(n0, n1, n1.w, n2.x, f23, df, m2, m3);
+                    }
                     // warp-uniform: unless the query's range covers all WIN candidate slots
                     // (then all are valid: ghi <= whi), test each slot against the range
                     // (c < ghi <= whi implies c < cend: no separate validity test)
@@ -1190,7 +1319,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
             // back to the sparse path below HYST_LO % (hysteresis: a window mix near one
             // threshold would toggle between the paths)
-            dense = 100u * wpass >= (uint32_t)(dense ? HYST_LO : HYST_HI) * __popc(wmask) * (cend - base);
+            if (mask_eval)                     // (a window every query skipped says nothing)
+                dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * (cend - base);
             base = cend;
         }
         // ---- item end: the queue refers to this group's slots
@@ -1236,14 +1366,6 @@ __device__ __forceinline__ void query_box(float4 a, float4 b, float d, const Fsg
 // so that warps working at the same time read the same (cell, time) slices and
 // the slices are reused from L2.  Keys for two stable radix sorts (cell first,
 // then t_start).
-__device__ __forceinline__ uint32_t spread3(uint32_t x) {      // 10 bits -> every third bit
-    x &= 0x3ffu;
-    x = (x | (x << 16)) & 0x030000ffu;
-    x = (x | (x << 8)) & 0x0300f00fu;
-    x = (x | (x << 4)) & 0x030c30c3u;
-    x = (x | (x << 2)) & 0x09249249u;
-    return x;
-}
 
 __global__ void k_fsg_order_keys(const float4 *__restrict__ Q, uint32_t n, FsgGrid G, uint32_t *__restrict__ kcell,
                                  uint32_t *__restrict__ kt, uint32_t *__restrict__ vals) {
@@ -1358,7 +1480,7 @@ __global__ void k_fsg_items(const uint32_t *__restrict__ item_start, uint32_t n,
         const int z = lo.z + (int)(c % nz), y = lo.y + (int)((c / nz) % ny), x = lo.x + (int)(c / (nz * ny));
         const uint64_t h = ((uint64_t)x * G.g[1] + y) * G.g[2] + z;
         uint32_t a0 = cell_off[h], a1 = cell_off[h + 1];
-        if (!literal && a0 < a1) {
+        if (!literal && a0 < a1) {                 // a cell's entries are in t_start order (build)
             a1 = cell_time_bound(frec, a0, a1, t1c, true);      // first t_start >= t1c
             a0 = cell_time_bound(frec, a0, a1, tlo, false);     // first t_start > t0c - max_dur
         }
@@ -1742,10 +1864,16 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         // the order only shapes the groups of 32 (the category must be exact): the
         // top 13 bits of the range start suffice, so the key has 16 bits = 2 passes
         a.lo_shift = std::max(0, lo_bits - 13);
+        for (int c = 0; c < 3; ++c) {
+            const float ext = idx->ext.hi[c] - idx->ext.lo[c];
+            a.mo[c] = idx->ext.lo[c];
+            a.mw[c] = ext > 0.f ? ext / 1024.f : 1.0f;
+        }
+        key_bits = 32;
         a.st = dst.p;
         a.count_t = (req_kind == TDS_AUTO && a.use_st) ? 1 : 0;
         a.rec = idx->rec;
-        a.tight = tight_ranges();
+        a.tight = tight_ranges() && idx->time_order;      // needs t_start order inside the bins
         k_schedule<<<nblk(n), 256, 0, s>>>(a);
         TDS_CHECK_LAUNCH();
         if (a.count_t) {
@@ -1976,6 +2104,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.srec[c] = spatial ? nullptr : idx->st_rec[c];
         }
         if (spatial) { a.ecell = idx->fsg_ecell; }
+        const char *ns_env = getenv("TDS_NO_STATIC");
+        a.static_ok = (ns_env && ns_env[0] == '1') ? 0 : 1;
+        const char *hh = getenv("TDS_HYST_HI"), *hl = getenv("TDS_HYST_LO");   // tuning (A/B)
+        a.hyst_hi = hh ? atoi(hh) : HYST_HI;
+        a.hyst_lo = hl ? atoi(hl) : HYST_LO;
         return a;
     };
 

@@ -118,6 +118,7 @@ struct tds_index_s {
     uint64_t n_cells = 0;
     int device = 0;
     uint64_t mem_budget = 0;        // device bytes available for result buffers (at build)
+    bool time_order = false;        // entries renumbered by t_start (else by (bin, Morton))
 };
 
 namespace tds {

@@ -41,7 +41,7 @@ BASE_SEED = 1410269800
 __all__ = [
     "Workload", "BASE_SEED", "random_walk", "tiny", "random_1m", "random_1m_s1",
     "random_dense", "merger", "scale_out", "query_stride", "segments_from_positions",
-    "dense_cube_side_kpc", "CONFIGS", "make_workload",
+    "dense_cube_side_kpc", "CONFIGS", "make_workload", "stationary_queries",
 ]
 
 
@@ -277,6 +277,25 @@ def scale_out(n_traj: int = 250_000, n_steps: int = 400, seed: int = BASE_SEED +
     return Workload("scale-out", D, Q, d, 10000, 4, (50, 50, 50), tD, tQ,
                     f"100M database at Random-1M density (cube {box:.0f}); query trajectories every "
                     f"{query_stride}th, shard {rank}/{world}")
+
+
+def stationary_queries(D: np.ndarray, n_points: int, n_steps: int, seed: int = BASE_SEED + 5) -> np.ndarray:
+    """Stationary-point queries (the paper's case (i), "a supernova explosion at a
+    point over a time interval"): ``n_points`` fixed positions, each the
+    start point of a random entry of D, observed over ``n_steps`` consecutive
+    unit-time segments from that entry's t_start (P1 = P0 in every segment).
+    float32 [n_points * n_steps, 8]."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    rows = rng.integers(0, D.shape[0], size=n_points)
+    p = D[rows, 0:3].astype(np.float32)
+    t = D[rows, 3].astype(np.float64)
+    Q = np.empty((n_points, n_steps, 8), dtype=np.float32)
+    for k in range(n_steps):
+        Q[:, k, 0:3] = p
+        Q[:, k, 4:7] = p
+        Q[:, k, 3] = (t + k).astype(np.float32)
+        Q[:, k, 7] = (t + k + 1).astype(np.float32)
+    return Q.reshape(-1, 8)
 
 
 CONFIGS = {

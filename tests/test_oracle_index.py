@@ -257,3 +257,30 @@ def test_st_arrays_and_plan_hand_example():
     # a window that clips the query to nothing
     assert tuple(ir.plan(D, Q[:1], 0.25, 2, 2, "temporal", window=(0.5, 1.0))[0]) == (-1, 0, 2)
     assert tuple(ir.plan(D, Q[:1], 0.25, 2, 2, "temporal", window=(0.8, 1.0))[0]) == (3, 0, 0)
+
+
+def test_morton30_hand_values():
+    # bit k of x, y, z -> bits 3k+2, 3k+1, 3k
+    assert ir.morton30([1, 0, 0, 1, 2, 1023], [0, 1, 0, 1, 0, 1023], [0, 0, 1, 1, 0, 1023]).tolist() == \
+        [4, 2, 1, 7, 32, (1 << 30) - 1]
+
+
+def test_spatial_sort_hand_example():
+    """Default renumbering: by temporal bin, then Morton code of the start cell on
+    a 1024^3 grid over the extent.  Extent [0, 1024]^3 -> unit cells."""
+    D = np.array([[2, 0, 0, 0.0, 2, 0, 0, 1],       # bin 0, cell (2,0,0) -> 32
+                  [0, 0, 1, 0.5, 0, 0, 1, 1.5],     # bin 0, (0,0,1) -> 1
+                  [1, 1, 1, 0.2, 1, 1, 1, 1.2],     # bin 0, (1,1,1) -> 7
+                  [0, 0, 0, 3.0, 0, 0, 0, 4.0],     # bin 1, (0,0,0) -> 0
+                  [0, 1, 0, 2.5, 1024, 1024, 1024, 3.5],   # bin 1, (0,1,0) -> 2
+                  [0, 0, 1, 0.1, 0, 0, 1, 1.1]],    # bin 0, (0,0,1) -> 1, after row 1 (stable)
+                 np.float32)
+    Ds, perm = ir.spatial_sort(D, 2)               # t in [0, 4]: b = 2, bins t0 < 2 | >= 2
+    assert perm.tolist() == [1, 5, 2, 0, 3, 4]
+    assert ir.temporal_sort(D)[1].tolist() == [0, 5, 2, 1, 4, 3]
+    # the same entries per bin under both orders
+    b_s = ir.temporal_bins(Ds, 2)
+    b_t = ir.temporal_bins(ir.temporal_sort(D)[0], 2)
+    for j in range(2):
+        assert b_s["B_first"][j] == b_t["B_first"][j] and b_s["B_last"][j] == b_t["B_last"][j]
+        assert b_s["B_end"][j] == b_t["B_end"][j]

@@ -8,7 +8,7 @@ tag=${1:-r2}; shift || true
 what=${*:-all}
 out=gpurun_out/prof; mkdir -p $out
 has() { [[ " $what " == *" all "* || " $what " == *" $1 "* ]]; }
-run() { local name=$1; shift; timeout 1500 python bench.py "$@" > $out/${tag}_bench_$name.json 2> $out/${tag}_bench_$name.err;
+run() { local name=$1; shift; timeout 600 python bench.py "$@" > $out/${tag}_bench_$name.json 2> $out/${tag}_bench_$name.err;
         tail -1 $out/${tag}_bench_$name.json | cut -c1-160; }
 ncu_one() {   # name skip kernel-regex bench-args...
   local name=$1 skip=$2 kern=$3; shift 3
