@@ -412,24 +412,22 @@ def run_tds(args, ws, rank, local):
     r.close()
     del cols
 
-    # ---- e2e through the public API with host buffers: Q copied in from pinned
-    # memory inside tds_search, records fetched to pinned host memory, every step
+    # ---- e2e through the public API with host buffers: tds_search_stream takes the
+    # queries from pinned host memory (copied in chunk by chunk inside the call) and
+    # leaves the records in pinned host memory (copied out while the next chunk is
+    # searched); the step ends when this rank's records are readable on the host
     e2e = None
     if not args.no_e2e:
-        n_out = per_kind[head]["results_rank0"]
-        hbuf = torch.empty((4, max(n_out, 1)), dtype=torch.int32).pin_memory()
-        outs = (hbuf[0].numpy(), hbuf[1].numpy(), hbuf[2].numpy().view(np.float32), hbuf[3].numpy().view(np.float32))
+        chunk = max(1, -(-nQ // 4))
         e2e_ms, d2h = [], []
         for k in range(args.steps + 1):
             flush.zero_()
             barrier()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            r = search(head, host=True)
-            n = r.count
-            o = outs if n <= hbuf.shape[1] else None
-            r.fetch(device=False, stream=stream.cuda_stream, out=None if o is None else tuple(x[:n] for x in o))
-            torch.cuda.synchronize(dev)
+            r = idx.search_stream(Qh, w.d, kind=head, chunk=chunk, stream=stream.cuda_stream, part=rank, nparts=ws)
+            blocks = r.host_records()                           # host-resident records (zero-copy)
+            n = sum(len(b) for b in blocks)
             el = 1e3 * (time.perf_counter() - t0)
             r.close()
             barrier()
@@ -439,9 +437,9 @@ def run_tds(args, ws, rank, local):
         tot = reduce_over_ranks(dist, sum(e2e_ms), dev, "max")
         e2e = {"value": nQ * len(e2e_ms) / (tot / 1e3), "unit": "query segments/s",
                "h2d_bytes_per_step": int(w.Q.nbytes), "d2h_bytes_per_step": int(statistics.median(d2h)),
-               "variant": head,
-               "timing": "host wall clock around tds_search (host queries) + tds_fetch_results (host "
-                         "destination), synchronize on both sides, max over ranks; index resident"}
+               "variant": head, "api": f"tds_search_stream (chunks of {chunk} queries, copies overlapped)",
+               "timing": "host wall clock around tds_search_stream (queries from pinned host memory, records "
+                         "into pinned host memory), synchronize on both sides, max over ranks; index resident"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

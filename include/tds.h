@@ -208,6 +208,30 @@ int tds_plan(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, doubl
 int tds_time_partition(const float *t_start, uint64_t n, uint32_t part, uint32_t nparts, void *stream,
                        uint32_t *rows, uint64_t *n_rows);
 
+/*
+ * tds_search_stream — tds_search of a query set in HOST memory, processed
+ * `chunk` queries at a time (the chunked processing of a large query set of
+ * the prior work): while chunk k is searched on the
+ * device, chunk k+1 is copied in and chunk k-1's records are copied out to
+ * pinned host memory, on a second stream.  The device holds two chunks of
+ * queries and one chunk's records at a time, so Q and the result may exceed
+ * device memory.
+ *   queries : nq segments in host memory (pinned: copied directly; pageable:
+ *             through a pinned bounce buffer)
+ *   chunk   : queries per chunk (>= 1)
+ *   part, nparts : as tds_search_part, applied to every chunk (0, 1: all)
+ * The result is host-resident: query ids are rows of the full query set;
+ * tds_fetch_results copies from host memory (sorted fetches and device
+ * destinations upload the records first); tds_merge_trajectories is not
+ * available for it (TDS_EINVAL).  tds_stats sums the chunks' counters;
+ * ms_total is wall-clock time.  Other arguments and errors as tds_search
+ * (TDS_EINVAL also for device-resident queries and chunk == 0).
+ * Synchronises stream.
+ */
+int tds_search_stream(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start,
+                      float t_end, uint64_t chunk, uint32_t part, uint32_t nparts, void *stream, tds_result *out,
+                      uint64_t *n_results);
+
 /* one request of tds_search_many: the arguments of tds_search */
 typedef struct tds_search_req {
     int kind;
@@ -277,6 +301,13 @@ int tds_result_stats(tds_result r, tds_stats *out);
 
 /* tds_result_count — number of records in r. */
 uint64_t tds_result_count(tds_result r);
+
+/* tds_result_host_block — zero-copy access to a host-resident result
+ * (tds_search_stream): block i (i = 0, 1, ... until *count == 0 and *records
+ * == NULL) holds *count records of 16 B, (query_id, entry_id, t_in, t_out) as
+ * uint32, uint32, float, float, in pinned host memory owned by r (valid until
+ * tds_result_free).  Errors: TDS_EINVAL (NULL, or not a host-resident result). */
+int tds_result_host_block(tds_result r, uint64_t i, const void **records, uint64_t *count);
 
 void tds_result_free(tds_result r);
 void tds_index_free(tds_index idx);

@@ -35,7 +35,8 @@ _EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",
                "tds_result_free", "tds_index_free", "tds_last_error", "tds_index_export", "tds_index_info",
                "tds_version", "tds_kernel_launches", "tds_merge_trajectories", "tds_search_many",
-               "tds_search_part", "tds_plan", "tds_time_partition", "tds_trim", "tds_test_inject_enomem"]
+               "tds_search_part", "tds_plan", "tds_time_partition", "tds_trim", "tds_test_inject_enomem",
+               "tds_search_stream", "tds_result_host_block"]
 
 
 class TdsError(RuntimeError):
@@ -86,6 +87,9 @@ def load_library(path: str = LIB_PATH):
                                ctypes.POINTER(u64)]
     lib.tds_search_part.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, ctypes.c_uint32,
                                     ctypes.c_uint32, vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
+    lib.tds_search_stream.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, u64, ctypes.c_uint32,
+                                      ctypes.c_uint32, vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
+    lib.tds_result_host_block.argtypes = [vp, u64, ctypes.POINTER(vp), ctypes.POINTER(u64)]
     lib.tds_time_partition.argtypes = [vp, u64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, ctypes.POINTER(u64)]
     lib.tds_plan.argtypes = [vp, i32, vp, u64, ctypes.c_double, f32, f32, vp, vp, vp, vp]
     lib.tds_fetch_results.argtypes = [vp, u64, u64, vp, vp, vp, vp, i32, i32, vp]
@@ -110,7 +114,8 @@ def load_library(path: str = LIB_PATH):
                                    ctypes.POINTER(ctypes.c_uint32)]
     for name in ("tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats",
                  "tds_index_export", "tds_index_info", "tds_merge_trajectories", "tds_search_many",
-                 "tds_search_part", "tds_plan", "tds_time_partition"):
+                 "tds_search_part", "tds_plan", "tds_time_partition", "tds_search_stream",
+                 "tds_result_host_block"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -201,6 +206,21 @@ class Index:
         else:
             _check(lib.tds_search(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), int(capacity),
                                   _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
+        del keep
+        return Result(h, n.value)
+
+    def search_stream(self, queries, d: float, window=(-math.inf, math.inf), kind="temporal", chunk: int = 1 << 16,
+                      stream=None, part: int = 0, nparts: int = 1) -> "Result":
+        """tds_search_stream: ``queries`` in host memory (numpy or CPU tensor),
+        searched ``chunk`` queries at a time with the copies overlapped; the
+        result is host-resident."""
+        lib = load_library()
+        k = KINDS[kind] if isinstance(kind, str) else int(kind)
+        ptr, nq, keep = _segments(queries)
+        h = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        _check(lib.tds_search_stream(self._h, k, ptr, nq, float(d), float(window[0]), float(window[1]), int(chunk),
+                                     int(part), int(nparts), _stream_ptr(stream), ctypes.byref(h), ctypes.byref(n)))
         del keep
         return Result(h, n.value)
 
@@ -306,6 +326,24 @@ class Result:
         _check(lib.tds_fetch_results(self._h, int(first), cnt, *ptrs, 1 if device else 0, 1 if sorted else 0,
                                      _stream_ptr(stream)))
         return q, e, ti, to
+
+    REC_DTYPE = np.dtype([("qid", "<u4"), ("eid", "<u4"), ("t_in", "<f4"), ("t_out", "<f4")])
+
+    def host_records(self) -> list:
+        """Zero-copy numpy views (structured dtype REC_DTYPE) of the blocks of a
+        host-resident result (tds_search_stream), valid until close()."""
+        lib = load_library()
+        out = []
+        i = 0
+        while True:
+            p = ctypes.c_void_p()
+            n = ctypes.c_uint64()
+            _check(lib.tds_result_host_block(self._h, i, ctypes.byref(p), ctypes.byref(n)))
+            if not n.value:
+                return out
+            buf = (ctypes.c_char * (16 * n.value)).from_address(p.value)
+            out.append(np.frombuffer(buf, dtype=self.REC_DTYPE))
+            i += 1
 
     def merge_trajectories(self, q_traj, e_traj, gap: float = 0.0, stream=None) -> "Result":
         """Trajectory-level answer (tds_merge_trajectories): records become

@@ -1,5 +1,6 @@
 // abi.cu — the extern "C" boundary declared in include/tds.h: argument
 // checking, host/device input detection, error reporting, handle lifetime.
+#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -110,11 +111,69 @@ void dfree(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
-// release the memory both pools of the current device hold unused (tds_trim)
+// Pinned host blocks for host-resident results (tds_search_stream): pinning
+// GBs of host memory costs ~0.1-0.3 s per GB, so freed blocks are cached (up to
+// PINNED_KEEP bytes) and reused by later results of the same or smaller size.
+constexpr uint64_t PINNED_KEEP = 64ull << 30;
+std::map<void *, uint64_t> &g_pin_size();
+static std::mutex g_pin_mu;
+static std::multimap<uint64_t, void *> g_pin_cache;
+static uint64_t g_pin_bytes = 0;
+
+void *pinned_alloc(uint64_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_cache.lower_bound(bytes);
+        if (it != g_pin_cache.end() && it->first <= 2 * bytes + (64ull << 20)) {
+            void *p = it->second;
+            g_pin_bytes -= it->first;
+            g_pin_cache.erase(it);
+            return p;
+        }
+    }
+    const uint64_t sz = std::max<uint64_t>(bytes, 1) + (bytes >> 3);     // room to be reused by larger results
+    void *p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, sz, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(TDS_ENOMEM, "cudaHostAlloc(%llu bytes): %s", (unsigned long long)sz, cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_size()[p] = sz;
+    return p;
+}
+
+std::map<void *, uint64_t> &g_pin_size() {
+    static std::map<void *, uint64_t> m;
+    return m;
+}
+
+void pinned_free(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    const uint64_t sz = g_pin_size()[p];
+    if (g_pin_bytes + sz <= PINNED_KEEP) {
+        g_pin_cache.emplace(sz, p);
+        g_pin_bytes += sz;
+    } else {
+        g_pin_size().erase(p);
+        cudaFreeHost(p);
+    }
+}
+
+// release the memory both pools of the current device hold unused, and the cached
+// pinned host blocks (tds_trim)
 void trim_pools() {
     cudaDeviceSynchronize();          // stream-ordered frees must have happened
     for (int w = 0; w < 2; ++w)
         if (cudaMemPool_t pool = device_pool(w)) cudaMemPoolTrimTo(pool, 0);
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (auto &kv : g_pin_cache) {
+        g_pin_size().erase(kv.second);
+        cudaFreeHost(kv.second);
+    }
+    g_pin_cache.clear();
+    g_pin_bytes = 0;
 }
 
 void *dalloc_big(size_t bytes, cudaStream_t s);
@@ -479,6 +538,43 @@ int tds_time_partition(const float *t_start, uint64_t n, uint32_t part, uint32_t
     ABI_CATCH
 }
 
+int tds_search_stream(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start,
+                      float t_end, uint64_t chunk, uint32_t part, uint32_t nparts, void *stream, tds_result *out,
+                      uint64_t *n_results) {
+    NvtxRange nvtx_range("tds_search_stream");
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!out) fail(TDS_EINVAL, "NULL argument");
+    *out = nullptr;
+    check_search_args(idx, kind, d, t_start, t_end);
+    if (nq > 0 && !queries) fail(TDS_EINVAL, "NULL query pointer");
+    if (((uintptr_t)queries & 15) != 0) fail(TDS_EINVAL, "segment array must be 16-byte aligned");
+    if (chunk == 0) fail(TDS_EINVAL, "chunk == 0");
+    if (nparts < 1 || part >= nparts) fail(TDS_EINVAL, "part %u of %u", part, nparts);
+    cudaPointerAttributes at{};
+    if (nq > 0 && cudaPointerGetAttributes(&at, queries) == cudaSuccess &&
+        (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged))
+        fail(TDS_EINVAL, "tds_search_stream takes queries in host memory (use tds_search for device queries)");
+    cudaGetLastError();
+    tds_result_s *r = new tds_result_s();
+    cudaGetDevice(&r->device);
+    try {
+        tds::SearchOpts opt;
+        opt.part = part;
+        opt.nparts = nparts;
+        tds::search_stream(idx, kind, reinterpret_cast<const float4 *>(queries), nq, d, t_start, t_end, chunk,
+                           (cudaStream_t)stream, r, opt);
+    } catch (...) {
+        free_result(r);
+        delete r;
+        throw;
+    }
+    *out = r;
+    if (n_results) *n_results = r->n;
+    return TDS_OK;
+    ABI_CATCH
+}
+
 int tds_plan(tds_index idx, int kind, const tds_seg *queries, uint64_t nq, double d, float t_start, float t_end,
              void *stream, int32_t *sel, uint32_t *lo, uint32_t *hi) {
     NvtxRange nvtx_range("tds_plan");
@@ -633,6 +729,7 @@ int tds_merge_trajectories(tds_result r, const uint32_t *q_traj, uint64_t nq, co
     if (ne != r->ne) fail(TDS_EINVAL, "e_traj has %llu ids, the index has %llu entries", (unsigned long long)ne,
                           (unsigned long long)r->ne);
     if (!(gap >= 0.f) || !isfinite(gap)) fail(TDS_EINVAL, "gap = %g must be finite and >= 0", (double)gap);
+    if (r->host) fail(TDS_EINVAL, "the result of tds_search_stream is host-resident: fetch it and merge on the host");
     cudaStream_t s = (cudaStream_t)stream;
     tds_result_s *m = new tds_result_s();
     cudaGetDevice(&m->device);
@@ -666,6 +763,22 @@ int tds_result_stats(tds_result r, tds_stats *out) {
 }
 
 uint64_t tds_result_count(tds_result r) { return r ? r->n : 0; }
+
+int tds_result_host_block(tds_result r, uint64_t i, const void **records, uint64_t *count) {
+    ABI_TRY
+    tds::set_error(0, "");
+    if (!r || !records || !count) fail(TDS_EINVAL, "NULL argument");
+    if (!r->host) fail(TDS_EINVAL, "not a host-resident result (tds_search_stream)");
+    if (i >= r->host_blocks.size()) {
+        *records = nullptr;
+        *count = 0;
+        return TDS_OK;
+    }
+    *records = r->host_blocks[i].first;
+    *count = r->host_blocks[i].second;
+    return TDS_OK;
+    ABI_CATCH
+}
 
 void tds_result_free(tds_result r) {
     if (!r) return;

@@ -31,10 +31,10 @@ constexpr int PT = 256;                  // threads per block of the pair kernel
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 #ifndef TDS_HYST_HI
-#define TDS_HYST_HI 50
+#define TDS_HYST_HI 25
 #endif
 #ifndef TDS_HYST_LO
-#define TDS_HYST_LO 25
+#define TDS_HYST_LO 12
 #endif
 constexpr int HYST_HI = TDS_HYST_HI, HYST_LO = TDS_HYST_LO;
 constexpr unsigned long long CAP_PROBE_MIN = 1ull << 24;     // result-size probe above this many pair tests
@@ -405,9 +405,8 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
     if (!(a < b)) return 0;                                    // C5
     const float L = b - a, aq = a - q0.w, ae = a - e0.w;
     const float dpx = q0.x - e0.x, dpy = q0.y - e0.y, dpz = q0.z - e0.z;
-    const float Dx = fmaf(-ae, vex, fmaf(aq, q1.x, dpx));
-    const float Dy = fmaf(-ae, vey, fmaf(aq, q1.y, dpy));
-    const float Dz = fmaf(-ae, vez, fmaf(aq, q1.z, dpz));
+    const float ix = fmaf(aq, q1.x, dpx), iy = fmaf(aq, q1.y, dpy), iz = fmaf(aq, q1.z, dpz);
+    const float Dx = fmaf(-ae, vex, ix), Dy = fmaf(-ae, vey, iy), Dz = fmaf(-ae, vez, iz);
     const float Vx = q1.x - vex, Vy = q1.y - vey, Vz = q1.z - vez;
     // position error over the span: eD at s = 0 (roundings of dp, a - t0, the
     // velocities (<= 4u each) and the two FMAs), eV per unit s (velocities and V)
@@ -438,16 +437,31 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
     const float rem = fmaxf(fmaf(dhi, dhi, -hu), 0.f);
     const float w = sqrt_approx(rem * rA);
     const float lo = su - w, hi = su + w;
-    // error of the unclamped ends: root sensitivity d eP / (A w) to the position
-    // error, + roundings of h_u and d^2, of B (3u |D|_1 |V|_1 / A), of s_u and w
-    const float dlt = fmaf(U, fabsf(su) + w,
-                           1.5f * fmaf(fmaf(dhi, eP0, (4.5f * U) * dhi * dhi), rcp_approx(A * w),
-                                       fmaf((3.f * U) * D1 * W1, rA, U * fmaf(7.f, fabsf(su), 5.f * w))));
+    // error of an unclamped end s (first order, x1.25): the root moves
+    // by (y . dP)/(A w) for a position error dP at the root, y = D + s V the relative
+    // position there (|y| = d), dP_i <= eD_i + L eV_i per component (roundings of dp,
+    // a - t0, the velocities (<= 5u each) and the FMAs); + the roundings of h_u and
+    // d^2 (4u d^2 / (A w)), of s_u (7u |s_u| + 2u sum|D_i V_i| / A), of w (3u w),
+    // and u (|s_u| + w) for s_u -+ w
+    const float ex = U * fmaf(6.f, fabsf(aq * q1.x) + fabsf(ae * vex), fabsf(Dx) + fabsf(ix) + fabsf(dpx)) +
+                     L * U * fmaf(5.f, fabsf(q1.x) + fabsf(vex), fabsf(Vx));
+    const float ey = U * fmaf(6.f, fabsf(aq * q1.y) + fabsf(ae * vey), fabsf(Dy) + fabsf(iy) + fabsf(dpy)) +
+                     L * U * fmaf(5.f, fabsf(q1.y) + fabsf(vey), fabsf(Vy));
+    const float ez = U * fmaf(6.f, fabsf(aq * q1.z) + fabsf(ae * vez), fabsf(Dz) + fabsf(iz) + fabsf(dpz)) +
+                     L * U * fmaf(5.f, fabsf(q1.z) + fabsf(vez), fabsf(Vz));
+    const float rAw = rcp_approx(A * w);
+    const float sdv = fabsf(Dx * Vx) + fabsf(Dy * Vy) + fabsf(Dz * Vz);
+    const float common = fmaf((4.f * U) * dhi * dhi, rAw, fmaf(7.f * U, fabsf(su), fmaf((2.f * U) * sdv, rA, (3.f * U) * w)));
+    const float rnd = U * (fabsf(su) + w);
+    const float yl = fabsf(fmaf(lo, Vx, Dx)) * ex + fabsf(fmaf(lo, Vy, Dy)) * ey + fabsf(fmaf(lo, Vz, Dz)) * ez;
+    const float yh = fabsf(fmaf(hi, Vx, Dx)) * ex + fabsf(fmaf(hi, Vy, Dy)) * ey + fabsf(fmaf(hi, Vz, Dz)) * ez;
+    const float dlt_lo = fmaf(1.25f, fmaf(yl, rAw, common), rnd);
+    const float dlt_hi = fmaf(1.25f, fmaf(yh, rAw, common), rnd);
     tin = a + fminf(fmaxf(lo, 0.f), L);
     tout = a + fminf(fmaxf(hi, 0.f), L);
     const float tol = 8e-6f * L;
-    const bool in_ok = (lo + dlt < 0.f) || (dlt <= tol);
-    const bool out_ok = (hi - dlt > L) || (dlt <= tol);
+    const bool in_ok = (lo + dlt_lo < 0.f) || (dlt_lo <= tol);
+    const bool out_ok = (hi - dlt_hi > L) || (dlt_hi <= tol);
     return (in_ok && out_ok) ? 2 : 1;
 }
 
@@ -970,7 +984,11 @@ struct __align__(16) RangeWarpSmem {
                                      // and the absolute form (c, m) (v, t0c') (t1c', lo, hi, qid)
     WarpState ws;                    // append chunk, refine queue (slot g, sorted position j), fp64 queue
     uint32_t cnt[32];                // records of slot g found by the refine path in this work item
-    float4 craw[4][32];              // dense windows: (t0, t1, entry row, min cell) of lane's candidate k
+    struct __align__(16) Cand {      // the window's candidates (slot = lane + 32 k), relative form
+        float4 p;                    // (x0, y0, z0, t0)
+        float4 v;                    // (vx, vy, vz, t1)
+        uint4 id;                    // (entry row, sorted / cell-ordered position j, min cell, -)
+    } cw[WIN];
     uint32_t spc[32], spq[32];       // GPUSpatial: cell and query-box low corner of slot g
     float4 qb[32][2];                // slot g's d-inflated box: (lo, t0c) (hi, t1c)
     uint32_t qn;                     // refine queue fill
@@ -983,22 +1001,23 @@ template <bool EXACT>
 __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, uint32_t n, uint32_t base) {
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
-    const uint32_t g = v ? W->ws.rq[base + lane] : 0u, j = v ? W->ws.rj[base + lane] : 0u;
+    const uint32_t g = v ? W->ws.rq[base + lane] : 0u, slot = v ? W->ws.rj[base + lane] : 0u;
     __syncwarp();                    // queue slots read: later queue additions may reuse them
     float tin = 0.f, tout = 0.f;
     int k = 0;
     uint32_t qid = 0;
+    const uint4 id = W->cw[slot].id;  // (entry row, position j, min cell)
     if (v) {
         const float4 q0 = W->q[g][0], q1 = W->q[g][1], q2 = W->q[g][2];
         qid = __float_as_uint(W->q[g][5].w);
-        if (!A->ecell || ref_cell(__ldg(A->ecell + j), W->spq[g], W->spc[g])) {
-            const ECand e = make_ecand(__ldg(A->pc.rec + 2 * (uint64_t)j), __ldg(A->pc.rec + 2 * (uint64_t)j + 1));
-            k = refine_rel(q0, q1, q2.x, q2.y, make_float4(e.px, e.py, e.pz, e.t0), e.t1, e.vx, e.vy, e.vz, A->pc.dlo,
-                           A->pc.d, tin, tout);
+        if (!A->ecell || ref_cell(id.z, W->spq[g], W->spc[g])) {
+            const float4 ep = W->cw[slot].p, ev = W->cw[slot].v;
+            k = refine_rel(q0, q1, q2.x, q2.y, ep, ev.w, ev.x, ev.y, ev.z, A->pc.dlo, A->pc.d, tin, tout);
         }
     }
+    const uint32_t j = id.y;
     const bool hit = (k == 2), need64 = (k == 1);
-    const Rec r{qid, hit ? __ldg(A->pc.perm + j) : 0u, tin, tout};
+    const Rec r{qid, hit ? id.x : 0u, tin, tout};
     append<EXACT>(A->pc.o, W->ws, hit, r, lane);
     if (hit) atomicAdd(&W->cnt[g], 1u);
     const unsigned hm = __ballot_sync(FULL, hit), m64 = __ballot_sync(FULL, need64);
@@ -1187,34 +1206,46 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 mask_eval = mask;
                 exec += (unsigned long long)(cend - base) * __popc(mask);
             };
+            // ---- the window: the lane's four candidates as absolute-form filter terms
+            // (registers, two packed pairs) and in the relative form with their rows
+            // (shared memory slots lane + 32 k, read by the refine step)
+            FSeg2 f01, f23;
+            {
+                auto stage = [&](int k, uint32_t c, uint32_t j, float4 a, float4 b, const FSeg &f) {
+                    const bool v = c < cend;
+                    RangeWarpSmem::Cand &cd = W.cw[lane + 32 * k];
+                    cd.p = a;
+                    cd.v = make_float4(f.vx, f.vy, f.vz, b.w);        // make_ecand's velocity (same rcp)
+                    cd.id = make_uint4(v ? __ldg(A.pc.perm + j) : 0u, j, (A.ecell && v) ? __ldg(A.ecell + j) : 0u, 0u);
+                };
+                float4 a0, b0, a1, b1;
+                load_cand(c0, c0 < cend, j0, a0, b0);
+                load_cand(c1, c1 < cend, j1, a1, b1);
+                wbox_add(wb, a0, b0, c0 < cend);
+                wbox_add(wb, a1, b1, c1 < cend);
+                {
+                    const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
+                    f01 = make_fseg2(fa, fb);
+                    stage(0, c0, j0, a0, b0, fa);
+                    stage(1, c1, j1, a1, b1, fb);
+                }
+                load_cand(c2, c2 < cend, j2, a0, b0);
+                load_cand(c3, c3 < cend, j3, a1, b1);
+                wbox_add(wb, a0, b0, c2 < cend);
+                wbox_add(wb, a1, b1, c3 < cend);
+                {
+                    const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
+                    f23 = make_fseg2(fa, fb);
+                    stage(2, c2, j2, a0, b0, fa);
+                    stage(3, c3, j3, a1, b1, fb);
+                }
+                __syncwarp();
+            }
+            const uint32_t s0 = lane, s1 = lane + 32, s2 = lane + 64, s3 = lane + 96;   // window slots
             if (dense) {
                 // fused step: the filter and the whole-span test for the lane's four
                 // candidates (two packed pairs); whole-span hits are appended at once
                 // with [a, b] from the raw times, other passes go to the refine queue
-                FSeg2 f01, f23;
-                {
-                    // raw times and entry rows of the lane's candidates (its own smem
-                    // slots, read back only when a record is appended)
-                    float4 a0, b0, a1, b1;
-                    load_cand(c0, c0 < cend, j0, a0, b0);
-                    load_cand(c1, c1 < cend, j1, a1, b1);
-                    wbox_add(wb, a0, b0, c0 < cend);
-                    wbox_add(wb, a1, b1, c1 < cend);
-                    f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-                    W.craw[0][lane] = make_float4(a0.w, b0.w, __uint_as_float(c0 < cend ? __ldg(A.pc.perm + j0) : 0u),
-                                                  __uint_as_float(A.ecell && c0 < cend ? __ldg(A.ecell + j0) : 0u));
-                    W.craw[1][lane] = make_float4(a1.w, b1.w, __uint_as_float(c1 < cend ? __ldg(A.pc.perm + j1) : 0u),
-                                                  __uint_as_float(A.ecell && c1 < cend ? __ldg(A.ecell + j1) : 0u));
-                    load_cand(c2, c2 < cend, j2, a0, b0);
-                    load_cand(c3, c3 < cend, j3, a1, b1);
-                    wbox_add(wb, a0, b0, c2 < cend);
-                    wbox_add(wb, a1, b1, c3 < cend);
-                    f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-                    W.craw[2][lane] = make_float4(a0.w, b0.w, __uint_as_float(c2 < cend ? __ldg(A.pc.perm + j2) : 0u),
-                                                  __uint_as_float(A.ecell && c2 < cend ? __ldg(A.ecell + j2) : 0u));
-                    W.craw[3][lane] = make_float4(a1.w, b1.w, __uint_as_float(c3 < cend ? __ldg(A.pc.perm + j3) : 0u),
-                                                  __uint_as_float(A.ecell && c3 < cend ? __ldg(A.ecell + j3) : 0u));
-                }
                 box_skip();
                 while (mask) {
                     const int g = __ffs(mask) - 1;
@@ -1238,7 +1269,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                         const uint32_t sq = W.spq[g], sc = W.spc[g];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            const bool ok = ref_cell(__float_as_uint(W.craw[k][lane].w), sq, sc);
+                            const bool ok = ref_cell(W.cw[lane + 32 * k].id.z, sq, sc);
                             m[k] &= ok;
                             in[k] &= ok;
                         }
@@ -1256,8 +1287,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                         Rec r[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            const float4 cr = W.craw[k][lane];
-                            r[k] = Rec{qid, __float_as_uint(cr.z), fmaxf(q2.x, cr.x), fminf(q2.y, cr.y)};
+                            const RangeWarpSmem::Cand &cd = W.cw[lane + 32 * k];
+                            r[k] = Rec{qid, cd.id.x, fmaxf(q2.x, cd.p.w), fminf(q2.y, cd.v.w)};
                         }
                         appendK<EXACT, 4>(A.pc.o, W.ws, in, bi, r, lane);
                         direct_hits += nin;
@@ -1266,26 +1297,12 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     wpass += nin;
                     if (__any_sync(FULL, (m[0] | m[1]) | (m[2] | m[3]))) {
                         const uint32_t q0n = qn;
-                        queue_add4(W.ws, qn, m[0], m[1], m[2], m[3], (uint32_t)g, j0, j1, j2, j3, lane);
+                        queue_add4(W.ws, qn, m[0], m[1], m[2], m[3], (uint32_t)g, s0, s1, s2, s3, lane);
                         wpass += qn - q0n;
                         range_drain<EXACT>(&A, W, qn);
                     }
                 }
             } else {
-                FSeg2 f01, f23;
-                {
-                    float4 a0, b0, a1, b1;
-                    load_cand(c0, c0 < cend, j0, a0, b0);
-                    load_cand(c1, c1 < cend, j1, a1, b1);
-                    wbox_add(wb, a0, b0, c0 < cend);
-                    wbox_add(wb, a1, b1, c1 < cend);
-                    f01 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-                    load_cand(c2, c2 < cend, j2, a0, b0);
-                    load_cand(c3, c3 < cend, j3, a1, b1);
-                    wbox_add(wb, a0, b0, c2 < cend);
-                    wbox_add(wb, a1, b1, c3 < cend);
-                    f23 = make_fseg2(make_fseg(a0, b0, A.tc), make_fseg(a1, b1, A.tc));
-                }
                 box_skip();
                 f32x2 rA01 = 0ull, rA23 = 0ull;
                 if (stat) { rA01 = static_rA(f01); rA23 = static_rA(f23); }
@@ -1311,7 +1328,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     }
                     if (!__any_sync(FULL, (m0 | m1) | (m2 | m3))) continue;
                     const uint32_t q0n = qn;
-                    queue_add4(W.ws, qn, m0, m1, m2, m3, (uint32_t)g, j0, j1, j2, j3, lane);
+                    queue_add4(W.ws, qn, m0, m1, m2, m3, (uint32_t)g, s0, s1, s2, s3, lane);
                     wpass += qn - q0n;
                     range_drain<EXACT>(&A, W, qn);
                 }
@@ -1319,6 +1336,11 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
             // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
             // back to the sparse path below HYST_LO % (hysteresis: a window mix near one
             // threshold would toggle between the paths)
+            if (qn) {                          // the queue refers to this window's slots
+                __syncwarp();
+                range_refine<EXACT>(&A, &W, qn, 0);
+                qn = 0;
+            }
             if (mask_eval)                     // (a window every query skipped says nothing)
                 dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * (cend - base);
             base = cend;
@@ -1631,6 +1653,32 @@ __global__ void k_fetch_flat(const Rec *__restrict__ rs, const uint32_t *__restr
     if (eid) eid[j] = r.eid;
     if (tin) tin[j] = r.t_in;
     if (tout) tout[j] = r.t_out;
+}
+
+// records of one chunk's result with the chunk's first query row added to the
+// query ids (tds_search_stream), from the chunked or the contiguous form
+__global__ void k_pack_chunked(const Rec *__restrict__ buf, uint32_t CS, uint64_t nchunks,
+                               const uint32_t *__restrict__ used, const uint64_t *__restrict__ off, uint32_t qoff,
+                               Rec *__restrict__ out) {
+    const uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= nchunks) return;
+    const uint32_t u = used[c];
+    const uint64_t o = off[c];
+    for (uint32_t k = lane; k < u; k += 32) {
+        Rec r = buf[c * CS + k];
+        r.qid += qoff;
+        out[o + k] = r;
+    }
+}
+
+__global__ void k_pack_flat(const Rec *__restrict__ in, uint64_t n, uint32_t qoff, Rec *__restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        Rec r = in[i];
+        r.qid += qoff;
+        out[i] = r;
+    }
 }
 
 __global__ void k_rec_field(const Rec *__restrict__ rs, uint64_t n, int which, const uint32_t *__restrict__ order,
@@ -2330,6 +2378,39 @@ void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint3
                                                    (unsigned long long)r->n);
     r->stream = s;
     if (count == 0) return;
+    if (r->host) {
+        // host-resident records (tds_search_stream): unsorted host destinations are
+        // filled on the host; otherwise the range is uploaded and fetched as a store
+        if (!dst_dev && !sorted) {
+            uint64_t pos = 0, j = 0;
+            for (auto &bk : r->host_blocks) {
+                const uint64_t lo = std::max(first, pos), hi = std::min(first + count, pos + bk.second);
+                for (uint64_t i = lo; i < hi; ++i, ++j) {
+                    const Rec &x = bk.first[i - pos];
+                    if (qid) qid[j] = x.qid;
+                    if (eid) eid[j] = x.eid;
+                    if (tin) tin[j] = x.t_in;
+                    if (tout) tout[j] = x.t_out;
+                }
+                pos += bk.second;
+            }
+            return;
+        }
+        tds_result_s tmp;
+        tmp.chunked = false;
+        tmp.n = r->n;
+        tmp.stream = s;
+        DBuf<Rec> all(r->n, s, r->n * sizeof(Rec) > (256ull << 20));
+        uint64_t pos = 0;
+        for (auto &bk : r->host_blocks) {
+            TDS_CUDA(cudaMemcpyAsync(all.p + pos, bk.first, bk.second * sizeof(Rec), cudaMemcpyHostToDevice, s));
+            pos += bk.second;
+        }
+        tmp.store = all.p;
+        fetch(&tmp, first, count, qid, eid, tin, tout, dst_dev, sorted, s);
+        TDS_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     // device staging for host destinations
     DBuf<uint32_t> dq, de;
     DBuf<float> di, doo;
@@ -2385,7 +2466,117 @@ void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint3
     }
 }
 
+// tds_search_stream (the chunked processing of Q of the prior work,
+// P:178-183): queries in host memory, `chunk` at a time.  The copy stream uploads
+// chunk k+1 while chunk k is searched on `s`, and copies chunk k's records
+// (query ids offset to rows of the full set) into pinned host memory while
+// chunk k+1 is searched, so the device holds two query chunks and one chunk's
+// records at a time; the result is host-resident.
+void search_stream(tds_index_s *idx, int kind, const float4 *qh, uint64_t nq, double d64, float T0, float T1,
+                   uint64_t chunk, cudaStream_t s, tds_result_s *res, const SearchOpts &opt) {
+    res->host = true;
+    res->chunked = false;
+    res->stream = s;
+    res->nq = nq;
+    res->ne = idx->n;
+    res->n = 0;
+    tds_stats &S = res->stats;
+    memset(&S, 0, sizeof S);
+    if (nq == 0) return;
+    chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, nq));
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, qh) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    cudaStream_t cs = nullptr;
+    TDS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    struct StreamGuard { cudaStream_t c; ~StreamGuard() { cudaStreamSynchronize(c); cudaStreamDestroy(c); } } sg{cs};
+    cudaEvent_t up[2], used[2], packed;
+    for (auto &e : up) TDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : used) TDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TDS_CUDA(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t *a; cudaEvent_t *b; cudaEvent_t c;
+        ~EvGuard() { for (int i = 0; i < 2; ++i) { cudaEventDestroy(a[i]); cudaEventDestroy(b[i]); } cudaEventDestroy(c); }
+    } eg{up, used, packed};
+    DBuf<float4> qb[2] = {DBuf<float4>(2 * chunk, s), DBuf<float4>(2 * chunk, s)};
+    TDS_CUDA(cudaStreamSynchronize(s));                 // buffers allocated before the copy stream uses them
+    // pageable queries go through a pinned bounce buffer (one per device buffer)
+    std::vector<float4 *> bounce(2, nullptr);
+    struct BounceGuard { std::vector<float4 *> &b; ~BounceGuard() { for (auto p : b) if (p) cudaFreeHost(p); } } bg{bounce};
+    if (!pinned)
+        for (auto &p : bounce) TDS_CUDA(cudaHostAlloc((void **)&p, 2 * chunk * sizeof(float4), cudaHostAllocDefault));
+    const uint64_t nch = (nq + chunk - 1) / chunk;
+    auto upload = [&](uint64_t k) {
+        const uint64_t q0 = k * chunk, nk = std::min(chunk, nq - q0);
+        const int b = (int)(k & 1);
+        TDS_CUDA(cudaStreamWaitEvent(cs, used[b], 0));  // the search of chunk k-2 is done with it
+        const float4 *src = qh + 2 * q0;
+        if (!pinned) {
+            TDS_CUDA(cudaEventSynchronize(used[b]));    // the bounce buffer's last copy has completed
+            memcpy(bounce[b], src, nk * sizeof(tds_seg));
+            src = bounce[b];
+        }
+        TDS_CUDA(cudaMemcpyAsync(qb[b].p, src, nk * sizeof(tds_seg), cudaMemcpyHostToDevice, cs));
+        TDS_CUDA(cudaEventRecord(up[b], cs));
+    };
+    for (int b = 0; b < 2; ++b) TDS_CUDA(cudaEventRecord(used[b], s));
+    upload(0);
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t k = 0; k < nch; ++k) {
+        const uint64_t q0 = k * chunk, nk = std::min(chunk, nq - q0);
+        const int b = (int)(k & 1);
+        if (k + 1 < nch) upload(k + 1);
+        TDS_CUDA(cudaStreamWaitEvent(s, up[b], 0));
+        tds_result_s r;
+        try {
+            search(idx, kind, qb[b].p, nk, d64, T0, T1, 0, s, &r, opt);
+        } catch (...) {
+            free_result(&r);
+            throw;
+        }
+        TDS_CUDA(cudaEventRecord(used[b], s));
+        // this chunk's records, query ids offset, to a device staging buffer, then to
+        // pinned host memory on the copy stream (overlapping the next search)
+        const uint64_t nr = r.n;
+        if (nr) {
+            DBuf<Rec> st(nr, s, nr * sizeof(Rec) > (256ull << 20));
+            if (r.chunked)
+                k_pack_chunked<<<nblk(r.nchunks * 32), 256, 0, s>>>(r.buf, r.CS, r.nchunks, r.chunk_used, r.chunk_off,
+                                                                    (uint32_t)q0, st.p);
+            else
+                k_pack_flat<<<nblk(nr), 256, 0, s>>>(r.store, nr, (uint32_t)q0, st.p);
+            TDS_CHECK_LAUNCH();
+            TDS_CUDA(cudaEventRecord(packed, s));
+            free_result(&r);
+            Rec *hb = reinterpret_cast<Rec *>(pinned_alloc(nr * sizeof(Rec)));
+            res->host_blocks.emplace_back(hb, nr);
+            TDS_CUDA(cudaStreamWaitEvent(cs, packed, 0));
+            TDS_CUDA(cudaMemcpyAsync(hb, st.p, nr * sizeof(Rec), cudaMemcpyDeviceToHost, cs));
+            st.s = cs;                                   // freed after the copy, in copy-stream order
+        } else {
+            free_result(&r);
+        }
+        res->n += nr;
+        S.pair_tests += r.stats.pair_tests;
+        S.pairs_executed += r.stats.pairs_executed;
+        S.refined_pairs += r.stats.refined_pairs;
+        S.passes += r.stats.passes;
+        S.fallback_queries += r.stats.fallback_queries;
+        S.n_queries += r.stats.n_queries;
+        S.ms_pairs += r.stats.ms_pairs;
+        S.ms_schedule += r.stats.ms_schedule;
+        S.kind = r.stats.kind;
+    }
+    TDS_CUDA(cudaStreamSynchronize(cs));
+    TDS_CUDA(cudaStreamSynchronize(s));
+    S.n_results = res->n;
+    S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void free_result(tds_result_s *r) {
+    if (!r->host_blocks.empty()) cudaStreamSynchronize(r->stream);   // copies into the blocks are done
+    for (auto &b : r->host_blocks) pinned_free(b.first);
+    r->host_blocks.clear();
     cudaStream_t s = r->stream;      // ordered after the last fetch on that stream
     if (r->buf) dfree(r->buf, s);
     if (r->chunk_used) dfree(r->chunk_used, s);

@@ -54,6 +54,8 @@ void count_launch();
 // ---------------------------------------------------------------------------
 void *dalloc(size_t bytes, cudaStream_t s);
 void *dalloc_big(size_t bytes, cudaStream_t s);   // large result buffers (separate pool)
+void *pinned_alloc(uint64_t bytes);                // pinned host blocks (cached)
+void pinned_free(void *p);
 void dfree(void *p, cudaStream_t s);
 
 template <class T>
@@ -234,6 +236,9 @@ struct tds_result_s {
     int device = 0;
     cudaStream_t stream = 0;          // stream of the last operation (frees are ordered after it)
     uint64_t nq = 0, ne = 0;          // query / entry counts of the search (trajectory merge checks)
+    // host-resident form (tds_search_stream): records in pinned host blocks
+    std::vector<std::pair<tds::Rec *, uint64_t>> host_blocks;
+    bool host = false;
 };
 
 namespace tds {
@@ -242,6 +247,9 @@ struct SearchOpts {
     int32_t *plan_sel = nullptr;              // tds_plan: host outputs per query row (range variants);
     uint32_t *plan_lo = nullptr, *plan_hi = nullptr;   // set -> schedule only, no pair kernel
 };
+// tds_search_stream: host queries in chunks, records to pinned host memory (search.cu)
+void search_stream(tds_index_s *idx, int kind, const float4 *q_host, uint64_t nq, double d, float T0, float T1,
+                   uint64_t chunk, cudaStream_t s, tds_result_s *res, const SearchOpts &opt);
 void search(tds_index_s *idx, int kind, const float4 *q, uint64_t nq, double d, float T0, float T1,
             uint64_t capacity, cudaStream_t s, tds_result_s *res, const SearchOpts &opt = SearchOpts());
 void fetch(tds_result_s *r, uint64_t first, uint64_t count, uint32_t *qid, uint32_t *eid, float *tin,
