@@ -327,6 +327,11 @@ const char *tds_last_error(void);
  *  10 fsg_A     uint32[len]     lookup array A of sorted-entry ids
  *  11 extents   float[16]       t_min, t_max, lo[3], hi[3], maxext[3], w_st[3], max_dur, pad
  *  12 sorted_t0 float[n]        t_start of the sorted entries
+ *  13 wb_rec / 14-16 wb_x, wb_y, wb_z / 17 wb_fsg  float[8 * ceil(len / 128)]
+ *               window boxes over the candidate orders (sorted entries, X/Y/Z, the
+ *               FSG cell-ordered copy): per aligned window of 128 positions
+ *               (min x, min y, min z, min t_start, max x, max y, max z, max t_end)
+ *               of its segments (the range kernel's window test)
  * Writes min(cap_bytes, size) bytes to dst (may be NULL to query the size) and the
  * full size to *n_bytes.  Errors: TDS_EINVAL (unknown / unbuilt array).
  */

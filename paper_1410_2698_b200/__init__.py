@@ -28,8 +28,10 @@ KINDS = {"temporal": TEMPORAL, "spatial": SPATIAL, "spatiotemporal": SPATIOTEMPO
 STATUS = {0: "TDS_OK", 1: "TDS_EINVAL", 2: "TDS_EDATA", 3: "TDS_ENOMEM", 4: "TDS_ECAPACITY", 5: "TDS_ECUDA"}
 
 EXPORT = {"perm": 0, "bin_off": 1, "bin_hi": 2, "st_x": 3, "st_y": 4, "st_z": 5, "st_off_x": 6,
-          "st_off_y": 7, "st_off_z": 8, "fsg_cell_off": 9, "fsg_A": 10, "extents": 11, "sorted_t0": 12}
-_EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float32}
+          "st_off_y": 7, "st_off_z": 8, "fsg_cell_off": 9, "fsg_A": 10, "extents": 11, "sorted_t0": 12,
+          "wb_rec": 13, "wb_x": 14, "wb_y": 15, "wb_z": 16, "wb_fsg": 17}
+_EXPORT_DT = {"bin_hi": np.float32, "extents": np.float32, "sorted_t0": np.float32, "wb_rec": np.float32,
+              "wb_x": np.float32, "wb_y": np.float32, "wb_z": np.float32, "wb_fsg": np.float32}
 
 # every symbol include/tds.h declares
 ABI_SYMBOLS = ["tds_build_index", "tds_search", "tds_fetch_results", "tds_result_stats", "tds_result_count",

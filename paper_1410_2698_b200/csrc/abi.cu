@@ -831,6 +831,13 @@ int tds_index_export(tds_index idx, int what, void *dst, uint64_t cap_bytes, uin
             for (uint64_t i = 0; i < idx->n; ++i) tmp[i] = r[2 * i].w;
             src = tmp.data(); bytes = 4 * idx->n; host = true; break;
         }
+        case 13: case 14: case 15: case 16: case 17: {   // window boxes
+            const float4 *wb = what == 13 ? idx->wb_rec : what == 17 ? idx->wb_fsg : idx->wb_st[what - 14];
+            const uint64_t len = what == 13 ? idx->n : what == 17 ? idx->A_len : idx->st_len[what - 14];
+            src = wb;
+            bytes = wb ? 32 * ((len + tds::WBOX_W - 1) / tds::WBOX_W) : 0;
+            break;
+        }
         default: fail(TDS_EINVAL, "unknown export %d", what);
     }
     if (!src && what != 11 && what != 12) fail(TDS_EINVAL, "array %d was not built", what);

@@ -139,6 +139,39 @@ __global__ void k_gather_records(const float4 *__restrict__ src, const uint32_t 
     }
 }
 
+// window boxes: one warp per aligned window of WBOX_W candidate positions (lane
+// takes positions lane + 32 k); the segments' MBB and time span, reduced over
+// order-preserving keys (exact min / max of the stored floats)
+__global__ void k_window_boxes(const float4 *__restrict__ rec, const uint32_t *__restrict__ arr, uint64_t len,
+                               float4 *__restrict__ out) {
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (len + WBOX_W - 1) / WBOX_W;
+    if (w >= nw) return;                       // warp-uniform
+    uint32_t lx = 0xffffffffu, ly = 0xffffffffu, lz = 0xffffffffu, lt = 0xffffffffu;
+    uint32_t hx = 0, hy = 0, hz = 0, ht = 0;
+#pragma unroll
+    for (int k = 0; k < (int)(WBOX_W / 32); ++k) {
+        const uint64_t c = w * WBOX_W + lane + 32 * k;
+        if (c < len) {
+            const uint64_t j = arr ? arr[c] : c;
+            const float4 a = rec[2 * j], b = rec[2 * j + 1];
+            lx = min(lx, float_key(fminf(a.x, b.x))); hx = max(hx, float_key(fmaxf(a.x, b.x)));
+            ly = min(ly, float_key(fminf(a.y, b.y))); hy = max(hy, float_key(fmaxf(a.y, b.y)));
+            lz = min(lz, float_key(fminf(a.z, b.z))); hz = max(hz, float_key(fmaxf(a.z, b.z)));
+            lt = min(lt, float_key(a.w));             ht = max(ht, float_key(b.w));
+        }
+    }
+    lx = __reduce_min_sync(0xffffffffu, lx); ly = __reduce_min_sync(0xffffffffu, ly);
+    lz = __reduce_min_sync(0xffffffffu, lz); lt = __reduce_min_sync(0xffffffffu, lt);
+    hx = __reduce_max_sync(0xffffffffu, hx); hy = __reduce_max_sync(0xffffffffu, hy);
+    hz = __reduce_max_sync(0xffffffffu, hz); ht = __reduce_max_sync(0xffffffffu, ht);
+    if (lane == 0) {
+        out[2 * w] = make_float4(key_float(lx), key_float(ly), key_float(lz), key_float(lt));
+        out[2 * w + 1] = make_float4(key_float(hx), key_float(hy), key_float(hz), key_float(ht));
+    }
+}
+
 // A3: bin of each sorted entry, literal (P:575-576 with reading C12), in fp64
 __global__ void k_bin_of(const float4 *__restrict__ rec, uint64_t n, double t_min, double b, int m,
                          uint32_t *__restrict__ bin) {
@@ -385,6 +418,17 @@ __global__ void k_emit_all(const float4 *__restrict__ rec, uint64_t n, int want_
 }
 
 inline unsigned nblk(uint64_t n, int nt = NT) { return (unsigned)((n + nt - 1) / nt); }
+
+float4 *window_boxes(const float4 *rec, const uint32_t *arr, uint64_t len, cudaStream_t s) {
+    const uint64_t nw = (len + WBOX_W - 1) / WBOX_W;
+    DBuf<float4> wb(std::max<uint64_t>(2 * nw, 2), s);
+    if (nw) {
+        k_window_boxes<<<nblk(nw * 32), NT, 0, s>>>(rec, arr, len, wb.p);
+        TDS_CHECK_LAUNCH();
+    }
+    return wb.release();
+}
+
 
 
 int bits_for(uint64_t nk) {
@@ -643,6 +687,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
                 idx->st_rec[c] = srec.release();
             }
             sk[c].reset();
+            idx->wb_st[c] = window_boxes(rec.p, sv[c].p, len, s);
             idx->st_arr[c] = sv[c].release();
             idx->st_len[c] = len;
             idx->st_off[c] = off.release();
@@ -675,6 +720,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
         DBuf<uint32_t> fperm(len, s);
         k_fsg_materialise<<<nblk(len), NT, 0, s>>>(rec.p, perm.p, fv.p, len, G, frec.p, fperm.p, ecell.p);
         TDS_CHECK_LAUNCH();
+        idx->wb_fsg = window_boxes(frec.p, nullptr, len, s);
         idx->fsg_ecell = ecell.release();
         idx->fsg_rec = frec.release();
         idx->fsg_perm = fperm.release();
@@ -686,6 +732,7 @@ void build_index(const tds_seg *entries, uint64_t n, const tds_index_params *p, 
     bin.s = s;
     tr.mark("st+fsg");
 
+    idx->wb_rec = window_boxes(rec.p, nullptr, n, s);
     idx->rec = rec.release();
     idx->perm = perm.release();
     idx->bin_off = bin_off.release();
@@ -710,6 +757,8 @@ void free_index(tds_index_s *idx) {
     f(idx->rec); f(idx->perm); f(idx->bin_off); f(idx->bin_lo); f(idx->bin_hi); f(idx->bin_pmhi);
     for (int c = 0; c < 3; ++c) { f(idx->st_arr[c]); f(idx->st_off[c]); f(idx->st_rec[c]); }
     f(idx->cell_off); f(idx->fsg_A); f(idx->fsg_ecell); f(idx->fsg_rec); f(idx->fsg_perm);
+    f(idx->wb_rec); f(idx->wb_fsg);
+    for (int c = 0; c < 3; ++c) f(idx->wb_st[c]);
     cudaStreamSynchronize(s);
 }
 

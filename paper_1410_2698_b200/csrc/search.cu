@@ -26,6 +26,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PT = 256;                  // threads per block of the pair kernels
+#ifndef TDS_APPEND_FAST
+#define TDS_APPEND_FAST 1                // appendK: warp-uniform fast path when the batch fits the chunk
+#endif
 #ifndef TDS_RANGE_BPS
 #define TDS_RANGE_BPS 2
 #endif
@@ -41,6 +44,7 @@ constexpr unsigned long long CAP_PROBE_MIN = 1ull << 24;     // result-size prob
 constexpr uint64_t CAP_FLOOR = 1ull << 22;                   // records: floor of the probed capacity
 constexpr double ST_PAIR_COST = 1.5;     // TDS_AUTO: GPUSpatioTemporal cost per pair test / GPUTemporal's
 constexpr uint32_t WIN = 128;            // range kernel window: 4 candidates per lane
+static_assert(WIN == WBOX_W, "the range kernel's windows are the index's window-box windows");
 // fp32 filter margin: eta = KU * M with M an l1 magnitude bound of the pair
 // (derived bound 20 u M, u = 2^-24; 64 u used)
 constexpr float KU = 64.0f / 16777216.0f;
@@ -586,20 +590,32 @@ __device__ __forceinline__ void appendK(const OutArgs &o, WarpState &W, const bo
         }
     }
     const unsigned lt = (1u << lane) - 1u;
-    uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base;
-    uint32_t pre = used;
+    if (TDS_APPEND_FAST && !full && used + k <= size) {   // warp-uniform: the whole batch fits the chunk
+        uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base + used;
+        uint32_t pre = 0;
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-        const uint32_t slot = pre + __popc(hm[i] & lt);
-        if (h[i]) {
-            if (!full && slot < size) {
-                out[slot] = make_uint4(r[i].qid, r[i].eid, __float_as_uint(r[i].t_in), __float_as_uint(r[i].t_out));
-            } else {
-                o.redo[r[i].qid] = 1;
-                atomicAdd(&o.st->dropped, 1ull);
-            }
+        for (int i = 0; i < K; ++i) {
+            if (h[i])
+                out[pre + __popc(hm[i] & lt)] =
+                    make_uint4(r[i].qid, r[i].eid, __float_as_uint(r[i].t_in), __float_as_uint(r[i].t_out));
+            pre += __popc(hm[i]);
         }
-        pre += __popc(hm[i]);
+    } else {
+        uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base;
+        uint32_t pre = used;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const uint32_t slot = pre + __popc(hm[i] & lt);
+            if (h[i]) {
+                if (!full && slot < size) {
+                    out[slot] = make_uint4(r[i].qid, r[i].eid, __float_as_uint(r[i].t_in), __float_as_uint(r[i].t_out));
+                } else {
+                    o.redo[r[i].qid] = 1;
+                    atomicAdd(&o.st->dropped, 1ull);
+                }
+            }
+            pre += __popc(hm[i]);
+        }
     }
     if (!full) used = min(used + k, size);
     __syncwarp();
@@ -877,7 +893,9 @@ __global__ void k_make_tiles(const Sched *__restrict__ S, uint32_t n_base, uint3
             hi = max(hi, __shfl_xor_sync(FULL, hi, o));
         }
         T.tb = tb; T.te = te; T.sel = sel;
-        if (lo < hi) { T.ulo = lo; T.uhi = hi; } else { T.ulo = T.uhi = 0; }
+        // union start aligned down to a window (WIN): the kernel's windows are the
+        // index's window-box windows (the slots' own ranges mask the extra candidates)
+        if (lo < hi) { T.ulo = lo & ~(WIN - 1); T.uhi = hi; } else { T.ulo = T.uhi = 0; }
     }
     if (lane == 0) {
         tiles[t] = T;
@@ -892,7 +910,8 @@ __global__ void k_tile_chunks(uint32_t *len_to_chunks, uint32_t ntiles, const un
                               DevStats *st, uint32_t target_items) {
     unsigned long long tl = *total_len;
     unsigned long long ch = (tl + target_items - 1) / (target_items ? target_items : 1);
-    ch = ch < 64 ? 64 : (ch > 8192 ? 8192 : ch);
+    ch = ch < WIN ? WIN : (ch > 8192 ? 8192 : ch);
+    ch = (ch + WIN - 1) / WIN * WIN;          // chunks of whole windows
     uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) st->ch = (uint32_t)ch;
     if (t < ntiles) len_to_chunks[t] = (uint32_t)((len_to_chunks[t] + ch - 1) / ch);
@@ -915,6 +934,9 @@ struct RangeArgs {
     // cell-ordered record copy): per entry its cell and the query box's low corner
     // (packed), per candidate the min cell of its MBB; null for the range variants
     const uint32_t *sp_cell, *sp_qlo, *ecell;
+    // window boxes of the candidate order: [0] the sorted (GPUSpatial: cell-ordered)
+    // records, [1 + c] X/Y/Z order (tile category sel = c)
+    const float4 *wb[4];
     int static_ok;                   // stationary-query filter allowed (default; TDS_NO_STATIC=1: off)
     int hyst_hi, hyst_lo;            // dense-window hysteresis, % of a window's evaluated pairs passing
 };
@@ -1043,45 +1065,6 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
     }
 }
 
-// Window box: the bounding box and time span of the
-// window's valid candidates (segment MBBs); a query whose d-inflated box (rounded
-// outward) misses it in some dimension, or whose window-clipped span misses
-// the candidates' span (C5), has no pair within d in the window and is skipped
-// for the whole window.  With the default index order (temporal bin, then Morton
-// code) a window of 128 consecutive candidates is spatially compact.
-struct WBox {
-    float lx, ly, lz, hx, hy, hz, t0, t1;
-};
-
-__device__ __forceinline__ void wbox_init(WBox &w) {
-    w.lx = w.ly = w.lz = w.t0 = INFINITY;
-    w.hx = w.hy = w.hz = w.t1 = -INFINITY;
-}
-
-__device__ __forceinline__ void wbox_add(WBox &w, float4 a, float4 b, bool v) {
-    if (!v) return;
-    w.lx = fminf(w.lx, fminf(a.x, b.x)); w.hx = fmaxf(w.hx, fmaxf(a.x, b.x));
-    w.ly = fminf(w.ly, fminf(a.y, b.y)); w.hy = fmaxf(w.hy, fmaxf(a.y, b.y));
-    w.lz = fminf(w.lz, fminf(a.z, b.z)); w.hz = fmaxf(w.hz, fmaxf(a.z, b.z));
-    w.t0 = fminf(w.t0, a.w); w.t1 = fmaxf(w.t1, b.w);
-}
-
-__device__ __forceinline__ float key_to_float(uint32_t k) {     // inverse of float_key
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-__device__ __forceinline__ float wmin(float x) { return key_to_float(__reduce_min_sync(FULL, float_key(x))); }
-__device__ __forceinline__ float wmax(float x) { return key_to_float(__reduce_max_sync(FULL, float_key(x))); }
-
-// warp-wide: bit g set iff slot g's box (qlo = (lo, t0c), qhi = (hi, t1c)) meets the window box
-__device__ __forceinline__ unsigned wbox_overlap(const WBox &w, float4 qlo, float4 qhi, bool active) {
-    // every lane takes part in every reduction (no short-circuit around redux.sync)
-    const float hx = wmax(w.hx), lx = wmin(w.lx), hy = wmax(w.hy), ly = wmin(w.ly), hz = wmax(w.hz),
-                lz = wmin(w.lz), t1 = wmax(w.t1), t0 = wmin(w.t0);
-    const bool ov = active & (qlo.x <= hx) & (qhi.x >= lx) & (qlo.y <= hy) & (qhi.y >= ly) & (qlo.z <= hz) &
-                    (qhi.z >= lz) & (qlo.w < t1) & (qhi.w > t0);
-    return __ballot_sync(FULL, ov);
-}
-
 // Mapping: a work item is a group of <= 32
 // consecutive schedule entries (one category) and a chunk of the union of their
 // candidate ranges.  Lane g owns query slot g of the group (its constants are
@@ -1181,31 +1164,39 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 b = __ldg(src + 1);
             }
         };
-        uint32_t base = wlo;
+        const float4 *wbt = A.wb[T.sel + 1];
+        uint32_t base = wlo & ~(WIN - 1);      // windows aligned with the index's window boxes
         while (base < whi) {
             const uint32_t cend = min(base + WIN, whi);
             unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
-            const unsigned wmask = mask;
             if (!mask) {                       // skip the gap to the next range start
                 uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
-                base = nxt;
+                if (nxt == 0xffffffffu) break;
+                base = nxt & ~(WIN - 1);
                 continue;
             }
+            // window box (built with the index): queries whose d-inflated box misses
+            // it in some dimension, or whose window-clipped span misses its time span
+            // (C5), have no pair within d in the window; if none is left the window's
+            // candidates are never loaded
+            {
+                const float4 *wp = wbt + 2 * (size_t)(base / WIN);
+                const float4 bl = __ldg(wp), bh = __ldg(wp + 1);
+                const float4 ql = W.qb[lane][0], qh = W.qb[lane][1];
+                const bool ov = ((mask >> lane) & 1u) & (ql.x <= bh.x) & (qh.x >= bl.x) & (ql.y <= bh.y) &
+                                (qh.y >= bl.y) & (ql.z <= bh.z) & (qh.z >= bl.z) & (ql.w < bh.w) & (qh.w > bl.w);
+                mask = __ballot_sync(FULL, ov);
+            }
+            if (!mask) { base = cend; continue; }
+            const unsigned mask_eval = mask;   // queries evaluated in this window
+            const uint32_t wn = cend - max(base, wlo);   // candidates of the window inside the union
+            exec += (unsigned long long)wn * __popc(mask);
             // ---- worker side: lane = candidate
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
             uint32_t wpass = 0;                // filter passes of this window (all queries)
-            WBox wb;
-            wbox_init(wb);
-            unsigned mask_eval = 0;            // queries evaluated in this window
-            // queries whose box misses the window box: skipped for the whole window
-            auto box_skip = [&]() {
-                mask &= wbox_overlap(wb, W.qb[lane][0], W.qb[lane][1], (wmask >> lane) & 1u);
-                mask_eval = mask;
-                exec += (unsigned long long)(cend - base) * __popc(mask);
-            };
             // ---- the window: the lane's four candidates as absolute-form filter terms
             // (registers, two packed pairs) and in the relative form with their rows
             // (shared memory slots lane + 32 k, read by the refine step)
@@ -1221,8 +1212,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 float4 a0, b0, a1, b1;
                 load_cand(c0, c0 < cend, j0, a0, b0);
                 load_cand(c1, c1 < cend, j1, a1, b1);
-                wbox_add(wb, a0, b0, c0 < cend);
-                wbox_add(wb, a1, b1, c1 < cend);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f01 = make_fseg2(fa, fb);
@@ -1231,8 +1220,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 }
                 load_cand(c2, c2 < cend, j2, a0, b0);
                 load_cand(c3, c3 < cend, j3, a1, b1);
-                wbox_add(wb, a0, b0, c2 < cend);
-                wbox_add(wb, a1, b1, c3 < cend);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f23 = make_fseg2(fa, fb);
@@ -1246,7 +1233,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 // fused step: the filter and the whole-span test for the lane's four
                 // candidates (two packed pairs); whole-span hits are appended at once
                 // with [a, b] from the raw times, other passes go to the refine queue
-                box_skip();
                 while (mask) {
                     const int g = __ffs(mask) - 1;
                     mask &= mask - 1;
@@ -1303,7 +1289,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     }
                 }
             } else {
-                box_skip();
                 f32x2 rA01 = 0ull, rA23 = 0ull;
                 if (stat) { rA01 = static_rA(f01); rA23 = static_rA(f23); }
                 while (mask) {
@@ -1327,6 +1312,13 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                         m0 &= r0 < gw; m1 &= r0 + 32 < gw; m2 &= r0 + 64 < gw; m3 &= r0 + 96 < gw;
                     }
                     if (!__any_sync(FULL, (m0 | m1) | (m2 | m3))) continue;
+                    if (A.ecell) {                         // GPUSpatial: the pair's reference cell only
+                        const uint32_t sq = W.spq[g], sc = W.spc[g];
+                        m0 &= ref_cell(W.cw[s0].id.z, sq, sc);
+                        m1 &= ref_cell(W.cw[s1].id.z, sq, sc);
+                        m2 &= ref_cell(W.cw[s2].id.z, sq, sc);
+                        m3 &= ref_cell(W.cw[s3].id.z, sq, sc);
+                    }
                     const uint32_t q0n = qn;
                     queue_add4(W.ws, qn, m0, m1, m2, m3, (uint32_t)g, s0, s1, s2, s3, lane);
                     wpass += qn - q0n;
@@ -1341,8 +1333,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 range_refine<EXACT>(&A, &W, qn, 0);
                 qn = 0;
             }
-            if (mask_eval)                     // (a window every query skipped says nothing)
-                dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * (cend - base);
+            dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * wn;
             base = cend;
         }
         // ---- item end: the queue refers to this group's slots
@@ -1794,6 +1785,8 @@ int fsg_literal() {
 template <bool EXACT>
 void launch_range(const RangeArgs &a, cudaStream_t s) {
     constexpr size_t smem = sizeof(RangeWarpSmem) * (PT / 32);
+    // RANGE_BPS resident blocks per SM: 228 KB of shared memory per SM, 1 KB reserved per block
+    static_assert(RANGE_BPS * (smem + 1024) <= 228 * 1024, "range kernel shared memory exceeds RANGE_BPS blocks/SM");
     static bool attr_set[64] = {};   // per instantiation and device (first launch)
     int dev = 0;
     cudaGetDevice(&dev);
@@ -2152,6 +2145,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.srec[c] = spatial ? nullptr : idx->st_rec[c];
         }
         if (spatial) { a.ecell = idx->fsg_ecell; }
+        a.wb[0] = spatial ? idx->wb_fsg : idx->wb_rec;
+        for (int c = 0; c < 3; ++c) a.wb[1 + c] = spatial ? nullptr : idx->wb_st[c];
         const char *ns_env = getenv("TDS_NO_STATIC");
         a.static_ok = (ns_env && ns_env[0] == '1') ? 0 : 1;
         const char *hh = getenv("TDS_HYST_HI"), *hl = getenv("TDS_HYST_LO");   // tuning (A/B)

@@ -121,6 +121,13 @@ struct tds_index_s {
     int device = 0;
     uint64_t mem_budget = 0;        // device bytes available for result buffers (at build)
     bool time_order = false;        // entries renumbered by t_start (else by (bin, Morton))
+    // window boxes (DESIGN.md §7 "Window boxes"): per aligned window of WBOX_W
+    // consecutive candidate positions, (min x, min y, min z, min t0), (max x,
+    // max y, max z, max t1) of the segments there; the range kernel tests a
+    // group's query boxes against it before loading the window
+    float4 *wb_rec = nullptr;                            // [2 ceil(n / WBOX_W)] over rec
+    float4 *wb_st[3] = {nullptr, nullptr, nullptr};      // over rec[X[i]], rec[Y[i]], rec[Z[i]]
+    float4 *wb_fsg = nullptr;                            // over the cell-ordered copy fsg_rec
 };
 
 namespace tds {
@@ -138,6 +145,8 @@ __host__ __device__ __forceinline__ uint32_t float_key(float f) {
 #endif
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+
+constexpr uint32_t WBOX_W = 128;    // window-box granularity = the range kernel's window
 
 // slab / cell of coordinate c: clamp(floor((c - o) / w), 0, g - 1) in fp32 RN.
 // The SAME expression is used for entries (build) and queries (search): it is

@@ -198,6 +198,36 @@ def test_index_build_matches_paper_structures(tds, tiny, order):
         assert cell_off[h] == a0 and cell_off[h + 1] == a1 + 1
 
 
+def _window_boxes_np(D, rows, W=128):
+    """Per aligned window of W candidate positions: the segments' MBB and time span."""
+    nw = (len(rows) + W - 1) // W
+    out = np.empty((nw, 8), np.float32)
+    for k in range(nw):
+        s = D[rows[k * W:(k + 1) * W]]
+        out[k, 0:3] = np.minimum(s[:, 0:3], s[:, 4:7]).min(axis=0)
+        out[k, 3] = s[:, 3].min()
+        out[k, 4:7] = np.maximum(s[:, 0:3], s[:, 4:7]).max(axis=0)
+        out[k, 7] = s[:, 7].max()
+    return out
+
+
+@pytest.mark.parametrize("order", ["time", "spatial"])
+def test_window_boxes_match_segment_mbbs(tds, tiny, order):
+    """The index's window boxes (the range kernel skips a window whose box no
+    query box meets) equal the MBB / time span of the segments of each aligned
+    128-position window, for every candidate order, ragged last window included."""
+    w, _ = tiny
+    idx = tds.Index(_cuda(w.D), kinds=tds.ALL, m=7, v=2, grid=(4, 3, 5), time_order=(order == "time"))
+    perm = idx.export("perm").astype(np.int64)
+    assert len(perm) % 128 != 0
+    assert np.array_equal(idx.export("wb_rec").reshape(-1, 8), _window_boxes_np(w.D, perm))
+    for c in "xyz":
+        ids = idx.export("st_" + c).astype(np.int64)
+        assert np.array_equal(idx.export("wb_" + c).reshape(-1, 8), _window_boxes_np(w.D, perm[ids]))
+    A = idx.export("fsg_A").astype(np.int64)
+    assert np.array_equal(idx.export("wb_fsg").reshape(-1, 8), _window_boxes_np(w.D, perm[A]))
+
+
 def test_admissible_v_matches_index_ref(tds, tiny):
     """the build accepts v up to index_ref.admissible_v (same v in all
     dimensions, so the smallest bound) and rejects the next."""

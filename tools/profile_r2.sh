@@ -2,7 +2,7 @@
 # Round-2 evidence on the GPU box (one GPU): bench lines, the launch list of the
 # default bench, and ncu --set full (with the source page) of the dominant pair
 # kernels.  Outputs under gpurun_out/prof/ (summaries are copied to profiles/).
-#   tools/profile_r2.sh [tag] [what...]   what = bench | launches | ncu | all (default)
+#   tools/profile_r2.sh [tag] [what...]   what = bench | launches | ncu | dram | all (default)
 set -u
 tag=${1:-r2}; shift || true
 what=${*:-all}
@@ -41,5 +41,12 @@ if has ncu; then
   ncu_one rdense009_t 7 k_pair_range --d 0.09
   ncu_one rdense001_t 7 k_pair_range --d 0.01
   ncu_one merger1_spatial 2 k_pair_range --config merger --variants spatial
+  ncu_one merger5_spatial 2 k_pair_range --config merger --d 5 --variants spatial
+  ncu_one merger5_st 2 k_pair_range --config merger --d 5 --variants spatiotemporal
+fi
+if has dram; then   # single-pass DRAM bytes at the full bench configurations -> profiles/ncu_traffic.json
+  for v in spatiotemporal temporal; do for d in 0.01 0.03 0.09; do tools/ncu_dram.sh $d $v random-dense; done; done
+  for v in spatiotemporal temporal spatial; do tools/ncu_dram.sh 1 $v merger; tools/ncu_dram.sh 5 $v merger; done
+  for v in spatiotemporal temporal spatial; do tools/ncu_dram.sh 50 $v random-1m; done
 fi
 ls $out | head -100
