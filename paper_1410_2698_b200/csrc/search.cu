@@ -929,6 +929,7 @@ struct RangeArgs {
     const uint32_t *item_start;      // [ntiles+1]
     uint32_t ntiles;
     float df;                        // filter_abs threshold: d * (1 + 2^-20), rounded up
+    float d2u;                       // d^2 rounded up (window-box distance test)
     float tc;                        // filter_abs time origin (middle of the index's time extent)
     // GPUSpatial through this kernel (entries = (query, FSG cell) slices of the
     // cell-ordered record copy): per entry its cell and the query box's low corner
@@ -1011,8 +1012,9 @@ struct __align__(16) RangeWarpSmem {
         float4 v;                    // (vx, vy, vz, t1)
         uint4 id;                    // (entry row, sorted / cell-ordered position j, min cell, -)
     } cw[WIN];
+    uint32_t nid[WIN];               // GPUSpatioTemporal: ids X[c] of the next window (cp.async)
     uint32_t spc[32], spq[32];       // GPUSpatial: cell and query-box low corner of slot g
-    float4 qb[32][2];                // slot g's d-inflated box: (lo, t0c) (hi, t1c)
+    float4 qb[32][2];                // slot g's segment MBB and clipped span: (lo, t0c) (hi, t1c)
     uint32_t qn;                     // refine queue fill
 };
 
@@ -1129,10 +1131,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 W.spc[lane] = active ? A.sp_cell[p] : 0xffffffffu;
                 W.spq[lane] = active ? A.sp_qlo[p] : 0u;
             }
-            W.qb[lane][0] = make_float4(__fsub_rd(fminf(qa.x, qb.x), A.pc.d), __fsub_rd(fminf(qa.y, qb.y), A.pc.d),
-                                        __fsub_rd(fminf(qa.z, qb.z), A.pc.d), qc.t0c);
-            W.qb[lane][1] = make_float4(__fadd_ru(fmaxf(qa.x, qb.x), A.pc.d), __fadd_ru(fmaxf(qa.y, qb.y), A.pc.d),
-                                        __fadd_ru(fmaxf(qa.z, qb.z), A.pc.d), qc.t1c);
+            W.qb[lane][0] = make_float4(fminf(qa.x, qb.x), fminf(qa.y, qb.y), fminf(qa.z, qb.z), qc.t0c);
+            W.qb[lane][1] = make_float4(fmaxf(qa.x, qb.x), fmaxf(qa.y, qb.y), fmaxf(qa.z, qb.z), qc.t1c);
             __syncwarp();
         }
         uint32_t wlo = my_lo, whi = my_hi;
@@ -1153,49 +1153,91 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         // records: sorted entries (temporal), the materialised X/Y/Z-ordered copy
         // (TDS_ST_MATERIALISE=1: streamed, independent of the id load), or rec[X[i]]
         const float4 *srec = (T.sel >= 0) ? A.srec[T.sel] : nullptr;
-        auto load_cand = [&](uint32_t c, bool v, uint32_t &j, float4 &a, float4 &b) {
+        // candidate k of the lane in the window at base: position c = base + lane + 32 k;
+        // GPUSpatioTemporal's ids X[c] were loaded one window ahead (nj)
+        auto load_cand = [&](uint32_t c, bool v, uint32_t jid, uint32_t &j, float4 &a, float4 &b) {
             j = 0;
             a = make_float4(0.f, 0.f, 0.f, 0.f);
             b = make_float4(0.f, 0.f, 0.f, 1.f);
             if (v) {
-                j = arr ? __ldg(arr + c) : c;
+                j = arr ? jid : c;
                 const float4 *src = srec ? srec + 2 * (uint64_t)c : A.pc.rec + 2 * (uint64_t)j;
                 a = __ldg(src);
                 b = __ldg(src + 1);
             }
         };
         const float4 *wbt = A.wb[T.sel + 1];
-        uint32_t base = wlo & ~(WIN - 1);      // windows aligned with the index's window boxes
-        while (base < whi) {
-            const uint32_t cend = min(base + WIN, whi);
-            unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
-            if (!mask) {                       // skip the gap to the next range start
-                uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
+        // the first window at or after b (aligned) that some query of the group
+        // needs: its range meets the window and its box passes the window-box test;
+        // 0xffffffff if none
+        auto find_window = [&](uint32_t b, unsigned &m) -> uint32_t {
+            while (b < whi) {
+                const uint32_t ce = min(b + WIN, whi);
+                unsigned mm = __ballot_sync(FULL, my_lo < ce && my_hi > b);
+                if (!mm) {                     // skip the gap to the next range start
+                    uint32_t nxt = (my_lo >= ce && my_lo < my_hi) ? my_lo : 0xffffffffu;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
-                if (nxt == 0xffffffffu) break;
-                base = nxt & ~(WIN - 1);
-                continue;
-            }
-            // window box (built with the index): queries whose d-inflated box misses
-            // it in some dimension, or whose window-clipped span misses its time span
-            // (C5), have no pair within d in the window; if none is left the window's
-            // candidates are never loaded
-            {
-                const float4 *wp = wbt + 2 * (size_t)(base / WIN);
+                    for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
+                    if (nxt == 0xffffffffu) return 0xffffffffu;
+                    b = nxt & ~(WIN - 1);
+                    continue;
+                }
+                // window box (built with the index): a pair within d at time t has
+                // P_q(t) in the query segment's MBB and P_e(t) in the window box, so a
+                // query whose MBB is farther than d from the box (Euclidean box-box
+                // distance, gaps and squares rounded down, compared with d^2 rounded
+                // up), or whose window-clipped span misses the box's time span (C5),
+                // has no pair in the window; a window no query needs is never loaded
+                const float4 *wp = wbt + 2 * (size_t)(b / WIN);
                 const float4 bl = __ldg(wp), bh = __ldg(wp + 1);
                 const float4 ql = W.qb[lane][0], qh = W.qb[lane][1];
-                const bool ov = ((mask >> lane) & 1u) & (ql.x <= bh.x) & (qh.x >= bl.x) & (ql.y <= bh.y) &
-                                (qh.y >= bl.y) & (ql.z <= bh.z) & (qh.z >= bl.z) & (ql.w < bh.w) & (qh.w > bl.w);
-                mask = __ballot_sync(FULL, ov);
+                const float gx = fmaxf(0.f, fmaxf(__fsub_rd(ql.x, bh.x), __fsub_rd(bl.x, qh.x)));
+                const float gy = fmaxf(0.f, fmaxf(__fsub_rd(ql.y, bh.y), __fsub_rd(bl.y, qh.y)));
+                const float gz = fmaxf(0.f, fmaxf(__fsub_rd(ql.z, bh.z), __fsub_rd(bl.z, qh.z)));
+                const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+                const bool ov = ((mm >> lane) & 1u) & (g2 <= A.d2u) & (ql.w < bh.w) & (qh.w > bl.w);
+                mm = __ballot_sync(FULL, ov);
+                if (mm) { m = mm; return b; }
+                b = ce;
             }
-            if (!mask) { base = cend; continue; }
+            return 0xffffffffu;
+        };
+        // GPUSpatioTemporal: the ids of a window's candidates, copied one window
+        // ahead into shared memory (cp.async: no registers held across the window)
+        auto load_ids = [&](uint32_t b) {
+            if (arr && !srec) {
+                const uint32_t e = min(b + WIN, whi);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t c = b + lane + 32 * k;
+                    if (c < e) {
+                        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&W.nid[lane + 32 * k]);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(arr + c) : "memory");
+                    } else {
+                        W.nid[lane + 32 * k] = 0u;
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        };
+        auto ids_ready = [&]() {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+        };
+        unsigned mask = 0;
+        uint32_t base = find_window(wlo & ~(WIN - 1), mask);
+        if (base != 0xffffffffu) load_ids(base);
+        while (base != 0xffffffffu) {
+            const uint32_t cend = min(base + WIN, whi);
             const unsigned mask_eval = mask;   // queries evaluated in this window
             const uint32_t wn = cend - max(base, wlo);   // candidates of the window inside the union
             exec += (unsigned long long)wn * __popc(mask);
             // ---- worker side: lane = candidate
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
+            if (arr && !srec) ids_ready();
+            const uint32_t i0 = arr ? W.nid[lane] : 0u, i1 = arr ? W.nid[lane + 32] : 0u,
+                           i2 = arr ? W.nid[lane + 64] : 0u, i3 = arr ? W.nid[lane + 96] : 0u;
             uint32_t wpass = 0;                // filter passes of this window (all queries)
             // ---- the window: the lane's four candidates as absolute-form filter terms
             // (registers, two packed pairs) and in the relative form with their rows
@@ -1210,16 +1252,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     cd.id = make_uint4(v ? __ldg(A.pc.perm + j) : 0u, j, (A.ecell && v) ? __ldg(A.ecell + j) : 0u, 0u);
                 };
                 float4 a0, b0, a1, b1;
-                load_cand(c0, c0 < cend, j0, a0, b0);
-                load_cand(c1, c1 < cend, j1, a1, b1);
+                load_cand(c0, c0 < cend, i0, j0, a0, b0);
+                load_cand(c1, c1 < cend, i1, j1, a1, b1);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f01 = make_fseg2(fa, fb);
                     stage(0, c0, j0, a0, b0, fa);
                     stage(1, c1, j1, a1, b1, fb);
                 }
-                load_cand(c2, c2 < cend, j2, a0, b0);
-                load_cand(c3, c3 < cend, j3, a1, b1);
+                load_cand(c2, c2 < cend, i2, j2, a0, b0);
+                load_cand(c3, c3 < cend, i3, j3, a1, b1);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f23 = make_fseg2(fa, fb);
@@ -1227,6 +1269,24 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     stage(3, c3, j3, a1, b1, fb);
                 }
                 __syncwarp();
+            }
+            // look ahead: the next window the group needs; its records (and entry
+            // rows) are prefetched into L2 while this window is evaluated
+            // (GPUSpatioTemporal: its ids are loaded now, its records prefetched
+            // after the filter step)
+            unsigned nmask = 0;
+            const uint32_t nbase = find_window(cend, nmask);
+            if (nbase != 0xffffffffu) {
+                if (!arr || srec) {
+                    const uint32_t c = nbase + 4 * lane;   // 4 records = one 128-B line per lane
+                    if (c < whi) {
+                        const float4 *src = srec ? srec + 2 * (uint64_t)c : A.pc.rec + 2 * (uint64_t)c;
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+                        if (lane < 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.perm + nbase + 32 * lane));
+                    }
+                } else {
+                    load_ids(nbase);
+                }
             }
             const uint32_t s0 = lane, s1 = lane + 32, s2 = lane + 64, s3 = lane + 96;   // window slots
             if (dense) {
@@ -1325,6 +1385,17 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     range_drain<EXACT>(&A, W, qn);
                 }
             }
+            if (arr && !srec && nbase != 0xffffffffu) {    // GPUSpatioTemporal: the next window's records
+                ids_ready();
+                const uint32_t e = min(nbase + WIN, whi);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (nbase + lane + 32 * k < e) {
+                        const uint32_t id = W.nid[lane + 32 * k];
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.rec + 2 * (uint64_t)id));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.perm + id));
+                    }
+            }
             // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
             // back to the sparse path below HYST_LO % (hysteresis: a window mix near one
             // threshold would toggle between the paths)
@@ -1334,7 +1405,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 qn = 0;
             }
             dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * wn;
-            base = cend;
+            base = nbase;
+            mask = nmask;
         }
         // ---- item end: the queue refers to this group's slots
         if (qn) {
@@ -2138,6 +2210,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     auto range_args = [&](const OutArgs &oo) {
         RangeArgs a{};
         a.df = filter_threshold(d);
+        {
+            float d2 = d * d;                              // d (float, rounded up) squared, rounded up
+            if ((double)d2 < (double)d * (double)d) d2 = nextafterf(d2, INFINITY);
+            a.d2u = d2;
+        }
         a.tc = time_origin(idx);
         a.pc = PairCtx{Q, prec, pperm, d, T0, T1, oo, d64, dlo};
         for (int c = 0; c < 3; ++c) {
