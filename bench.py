@@ -369,6 +369,7 @@ def run_tds(args, ws, rank, local):
             "pair_tests": int(pt_all), "results": int(res_all),
             "pair_kernel_ms": pk, "pair_tests_rank0": int(pt[0]), "results_rank0": int(st["n_results"]),
             "pairs_executed": int(st["pairs_executed"]), "refined_pairs_fp64": int(st["refined_pairs"]),
+            "refined_pairs_fp32": int(st["refined32"]), "direct_records": int(st["direct_records"]),
             "passes": int(st["passes"]), "fallback_queries": int(st["fallback_queries"]),
             "ms_schedule": statistics.median(r[kind][2]["ms_schedule"] for r in recs),
             "pair_kernel_share_of_search": pk / statistics.median(ms),

@@ -110,6 +110,8 @@ typedef struct {
     int32_t reserved;
     uint64_t pair_tests_alt;    /* TDS_AUTO: scheduled pair tests of the variant not chosen (else 0) */
     uint64_t capacity;          /* records the pass buffer held (after any halving on ENOMEM) */
+    uint64_t refined32;         /* filter passes evaluated by the fp32 interval step (refine) */
+    uint64_t direct_records;    /* records appended by the whole-span test of dense windows */
 } tds_stats;
 
 /*

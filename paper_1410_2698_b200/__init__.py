@@ -68,7 +68,7 @@ class _Stats(ctypes.Structure):
                                                "refined_pairs", "passes", "spilled", "fallback_queries")] + \
                [(k, ctypes.c_float) for k in ("ms_schedule", "ms_pairs", "ms_compact", "ms_total")] + \
                [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("pair_tests_alt", ctypes.c_uint64),
-                ("capacity", ctypes.c_uint64)]
+                ("capacity", ctypes.c_uint64), ("refined32", ctypes.c_uint64), ("direct_records", ctypes.c_uint64)]
 
 
 _lib = None

@@ -54,6 +54,8 @@ struct DevStats {
     unsigned long long hits;         // records produced (kept or dropped)
     unsigned long long dropped;      // records dropped (buffer full)
     unsigned long long refined;      // pairs evaluated in fp64
+    unsigned long long refined32;    // filter passes evaluated by refine_rel
+    unsigned long long direct;       // records appended by the whole-span test
     unsigned long long executed;     // lane-pair slots evaluated
     unsigned long long pair_tests;   // algorithmic candidate pairs
     unsigned long long fallback;     // ST temporal fallbacks
@@ -492,7 +494,7 @@ constexpr int RQ_CAP = 192;          // refine queue capacity (32 + up to 5 x 32
 struct WarpState {
     unsigned long long ap_base;
     uint32_t ap_used, ap_size, ap_full;
-    uint32_t refined, hits;
+    uint32_t refined, hits, r32;
     uint32_t fn;                     // fp64 queue fill (< 32 between flushes)
     uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: group slot, candidate (sorted / cell-ordered position)
     uint32_t fq[64], fj[64];         // fp64 queue: pairs the fp32 stages could not decide
@@ -500,7 +502,7 @@ struct WarpState {
 
 __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
     if (lane == 0) {
-        W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0; W.fn = 0;
+        W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0; W.fn = 0; W.r32 = 0;
     }
     __syncwarp();
 }
@@ -638,6 +640,7 @@ __device__ __forceinline__ void warp_state_finish(const OutArgs &o, WarpState &W
     if (lane == 0) {
         if (!EXACT && !W.ap_full && W.ap_size) o.chunk_used[W.ap_base >> o.cs_shift] = W.ap_used;
         if (W.refined) atomicAdd(&o.st->refined, (unsigned long long)W.refined);
+        if (W.r32) atomicAdd(&o.st->refined32, (unsigned long long)W.r32);
         if (W.hits) atomicAdd(&o.st->hits, (unsigned long long)W.hits);
     }
 }
@@ -1012,7 +1015,6 @@ struct __align__(16) RangeWarpSmem {
         float4 v;                    // (vx, vy, vz, t1)
         uint4 id;                    // (entry row, sorted / cell-ordered position j, min cell, -)
     } cw[WIN];
-    uint32_t nid[WIN];               // GPUSpatioTemporal: ids X[c] of the next window (cp.async)
     uint32_t spc[32], spq[32];       // GPUSpatial: cell and query-box low corner of slot g
     float4 qb[32][2];                // slot g's segment MBB and clipped span: (lo, t0c) (hi, t1c)
     uint32_t qn;                     // refine queue fill
@@ -1052,7 +1054,7 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
         W->ws.fj[pos] = j;
     }
     __syncwarp();
-    if (lane == 0) { W->ws.hits += __popc(hm); W->ws.fn = fn + __popc(m64); }
+    if (lane == 0) { W->ws.hits += __popc(hm); W->ws.fn = fn + __popc(m64); W->ws.r32 += n; }
     __syncwarp();
     if (fn + __popc(m64) >= 32) flush64<EXACT>(&A->pc, &W->ws, 32);
 }
@@ -1153,91 +1155,54 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
         // records: sorted entries (temporal), the materialised X/Y/Z-ordered copy
         // (TDS_ST_MATERIALISE=1: streamed, independent of the id load), or rec[X[i]]
         const float4 *srec = (T.sel >= 0) ? A.srec[T.sel] : nullptr;
-        // candidate k of the lane in the window at base: position c = base + lane + 32 k;
-        // GPUSpatioTemporal's ids X[c] were loaded one window ahead (nj)
-        auto load_cand = [&](uint32_t c, bool v, uint32_t jid, uint32_t &j, float4 &a, float4 &b) {
+        auto load_cand = [&](uint32_t c, bool v, uint32_t &j, float4 &a, float4 &b) {
             j = 0;
             a = make_float4(0.f, 0.f, 0.f, 0.f);
             b = make_float4(0.f, 0.f, 0.f, 1.f);
             if (v) {
-                j = arr ? jid : c;
+                j = arr ? __ldg(arr + c) : c;
                 const float4 *src = srec ? srec + 2 * (uint64_t)c : A.pc.rec + 2 * (uint64_t)j;
                 a = __ldg(src);
                 b = __ldg(src + 1);
             }
         };
         const float4 *wbt = A.wb[T.sel + 1];
-        // the first window at or after b (aligned) that some query of the group
-        // needs: its range meets the window and its box passes the window-box test;
-        // 0xffffffff if none
-        auto find_window = [&](uint32_t b, unsigned &m) -> uint32_t {
-            while (b < whi) {
-                const uint32_t ce = min(b + WIN, whi);
-                unsigned mm = __ballot_sync(FULL, my_lo < ce && my_hi > b);
-                if (!mm) {                     // skip the gap to the next range start
-                    uint32_t nxt = (my_lo >= ce && my_lo < my_hi) ? my_lo : 0xffffffffu;
+        uint32_t base = wlo & ~(WIN - 1);      // windows aligned with the index's window boxes
+        while (base < whi) {
+            const uint32_t cend = min(base + WIN, whi);
+            unsigned mask = __ballot_sync(FULL, my_lo < cend && my_hi > base);
+            if (!mask) {                       // skip the gap to the next range start
+                uint32_t nxt = (my_lo >= cend && my_lo < my_hi) ? my_lo : 0xffffffffu;
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
-                    if (nxt == 0xffffffffu) return 0xffffffffu;
-                    b = nxt & ~(WIN - 1);
-                    continue;
-                }
-                // window box (built with the index): a pair within d at time t has
-                // P_q(t) in the query segment's MBB and P_e(t) in the window box, so a
-                // query whose MBB is farther than d from the box (Euclidean box-box
-                // distance, gaps and squares rounded down, compared with d^2 rounded
-                // up), or whose window-clipped span misses the box's time span (C5),
-                // has no pair in the window; a window no query needs is never loaded
-                const float4 *wp = wbt + 2 * (size_t)(b / WIN);
+                for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
+                if (nxt == 0xffffffffu) break;
+                base = nxt & ~(WIN - 1);
+                continue;
+            }
+            // window box (built with the index): a pair within d at time t has
+            // P_q(t) in the query segment's MBB and P_e(t) in the window box, so a
+            // query whose MBB is farther than d from the box (Euclidean box-box
+            // distance, gaps and squares rounded down, compared with d^2 rounded
+            // up), or whose window-clipped span misses the box's time span (C5), has
+            // no pair in the window; if no query is left the window is never loaded
+            {
+                const float4 *wp = wbt + 2 * (size_t)(base / WIN);
                 const float4 bl = __ldg(wp), bh = __ldg(wp + 1);
                 const float4 ql = W.qb[lane][0], qh = W.qb[lane][1];
                 const float gx = fmaxf(0.f, fmaxf(__fsub_rd(ql.x, bh.x), __fsub_rd(bl.x, qh.x)));
                 const float gy = fmaxf(0.f, fmaxf(__fsub_rd(ql.y, bh.y), __fsub_rd(bl.y, qh.y)));
                 const float gz = fmaxf(0.f, fmaxf(__fsub_rd(ql.z, bh.z), __fsub_rd(bl.z, qh.z)));
                 const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
-                const bool ov = ((mm >> lane) & 1u) & (g2 <= A.d2u) & (ql.w < bh.w) & (qh.w > bl.w);
-                mm = __ballot_sync(FULL, ov);
-                if (mm) { m = mm; return b; }
-                b = ce;
+                const bool ov = ((mask >> lane) & 1u) & (g2 <= A.d2u) & (ql.w < bh.w) & (qh.w > bl.w);
+                mask = __ballot_sync(FULL, ov);
             }
-            return 0xffffffffu;
-        };
-        // GPUSpatioTemporal: the ids of a window's candidates, copied one window
-        // ahead into shared memory (cp.async: no registers held across the window)
-        auto load_ids = [&](uint32_t b) {
-            if (arr && !srec) {
-                const uint32_t e = min(b + WIN, whi);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t c = b + lane + 32 * k;
-                    if (c < e) {
-                        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&W.nid[lane + 32 * k]);
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(arr + c) : "memory");
-                    } else {
-                        W.nid[lane + 32 * k] = 0u;
-                    }
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-        };
-        auto ids_ready = [&]() {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-        };
-        unsigned mask = 0;
-        uint32_t base = find_window(wlo & ~(WIN - 1), mask);
-        if (base != 0xffffffffu) load_ids(base);
-        while (base != 0xffffffffu) {
-            const uint32_t cend = min(base + WIN, whi);
+            if (!mask) { base = cend; continue; }
             const unsigned mask_eval = mask;   // queries evaluated in this window
             const uint32_t wn = cend - max(base, wlo);   // candidates of the window inside the union
             exec += (unsigned long long)wn * __popc(mask);
             // ---- worker side: lane = candidate
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
-            if (arr && !srec) ids_ready();
-            const uint32_t i0 = arr ? W.nid[lane] : 0u, i1 = arr ? W.nid[lane + 32] : 0u,
-                           i2 = arr ? W.nid[lane + 64] : 0u, i3 = arr ? W.nid[lane + 96] : 0u;
             uint32_t wpass = 0;                // filter passes of this window (all queries)
             // ---- the window: the lane's four candidates as absolute-form filter terms
             // (registers, two packed pairs) and in the relative form with their rows
@@ -1252,16 +1217,16 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     cd.id = make_uint4(v ? __ldg(A.pc.perm + j) : 0u, j, (A.ecell && v) ? __ldg(A.ecell + j) : 0u, 0u);
                 };
                 float4 a0, b0, a1, b1;
-                load_cand(c0, c0 < cend, i0, j0, a0, b0);
-                load_cand(c1, c1 < cend, i1, j1, a1, b1);
+                load_cand(c0, c0 < cend, j0, a0, b0);
+                load_cand(c1, c1 < cend, j1, a1, b1);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f01 = make_fseg2(fa, fb);
                     stage(0, c0, j0, a0, b0, fa);
                     stage(1, c1, j1, a1, b1, fb);
                 }
-                load_cand(c2, c2 < cend, i2, j2, a0, b0);
-                load_cand(c3, c3 < cend, i3, j3, a1, b1);
+                load_cand(c2, c2 < cend, j2, a0, b0);
+                load_cand(c3, c3 < cend, j3, a1, b1);
                 {
                     const FSeg fa = make_fseg(a0, b0, A.tc), fb = make_fseg(a1, b1, A.tc);
                     f23 = make_fseg2(fa, fb);
@@ -1269,24 +1234,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     stage(3, c3, j3, a1, b1, fb);
                 }
                 __syncwarp();
-            }
-            // look ahead: the next window the group needs; its records (and entry
-            // rows) are prefetched into L2 while this window is evaluated
-            // (GPUSpatioTemporal: its ids are loaded now, its records prefetched
-            // after the filter step)
-            unsigned nmask = 0;
-            const uint32_t nbase = find_window(cend, nmask);
-            if (nbase != 0xffffffffu) {
-                if (!arr || srec) {
-                    const uint32_t c = nbase + 4 * lane;   // 4 records = one 128-B line per lane
-                    if (c < whi) {
-                        const float4 *src = srec ? srec + 2 * (uint64_t)c : A.pc.rec + 2 * (uint64_t)c;
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
-                        if (lane < 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.perm + nbase + 32 * lane));
-                    }
-                } else {
-                    load_ids(nbase);
-                }
             }
             const uint32_t s0 = lane, s1 = lane + 32, s2 = lane + 64, s3 = lane + 96;   // window slots
             if (dense) {
@@ -1385,17 +1332,6 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                     range_drain<EXACT>(&A, W, qn);
                 }
             }
-            if (arr && !srec && nbase != 0xffffffffu) {    // GPUSpatioTemporal: the next window's records
-                ids_ready();
-                const uint32_t e = min(nbase + WIN, whi);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (nbase + lane + 32 * k < e) {
-                        const uint32_t id = W.nid[lane + 32 * k];
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.rec + 2 * (uint64_t)id));
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.pc.perm + id));
-                    }
-            }
             // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
             // back to the sparse path below HYST_LO % (hysteresis: a window mix near one
             // threshold would toggle between the paths)
@@ -1405,8 +1341,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
                 qn = 0;
             }
             dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * wn;
-            base = nbase;
-            mask = nmask;
+            base = cend;
         }
         // ---- item end: the queue refers to this group's slots
         if (qn) {
@@ -1424,7 +1359,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_const
     if (W.ws.fn) flush64<EXACT>(&A.pc, &W.ws, W.ws.fn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
     if (lane == 0 && exec) atomicAdd(&st->executed, exec);
-    if (lane == 0 && direct_hits) atomicAdd(&st->hits, direct_hits);
+    if (lane == 0 && direct_hits) { atomicAdd(&st->hits, direct_hits); atomicAdd(&st->direct, direct_hits); }
 }
 
 // ---------------------------------------------------------------------------
@@ -2248,6 +2183,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     TDS_CUDA(cudaStreamSynchronize(s));
     S.passes = 1;
     S.refined_pairs = hs.refined;
+    S.refined32 = hs.refined32;
+    S.direct_records = hs.direct;
     S.pairs_executed = hs.executed;
 
     // only the first nres chunks were ever reserved (reservations are sequential)
@@ -2426,6 +2363,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             DevStats hb2;
             TDS_CUDA(cudaMemcpy(&hb2, bst.p, sizeof hb2, cudaMemcpyDeviceToHost));
             S.refined_pairs += hb2.refined;
+            S.refined32 += hb2.refined32;
+            S.direct_records += hb2.direct;
             S.pairs_executed += hb2.executed;
         }
         S.passes++;
@@ -2632,6 +2571,8 @@ void search_stream(tds_index_s *idx, int kind, const float4 *qh, uint64_t nq, do
         S.pair_tests += r.stats.pair_tests;
         S.pairs_executed += r.stats.pairs_executed;
         S.refined_pairs += r.stats.refined_pairs;
+        S.refined32 += r.stats.refined32;
+        S.direct_records += r.stats.direct_records;
         S.passes += r.stats.passes;
         S.fallback_queries += r.stats.fallback_queries;
         S.n_queries += r.stats.n_queries;
