@@ -7,7 +7,7 @@ import os
 import sys
 
 raw, config, d, kernel, variant = sys.argv[1:6]
-rows = list(csv.reader(open(raw)))
+rows = [r for r in csv.reader(open(raw)) if r and not r[0].startswith("==")]
 vals = dict(zip(rows[0], rows[2]))
 units = dict(zip(rows[0], rows[1]))
 
