@@ -403,9 +403,11 @@ __device__ __forceinline__ bool pair64(float4 qa, float4 qb, float4 ea, float4 e
 // Refine one queued pair in the relative form (P(t) = P0 + (t - t0) v) with
 // first-order error bounds evaluated from the pair's own magnitudes (DESIGN.md
 // §5 "refine"): 0 = miss, 1 = undecided (fp64), 2 = certain hit with an fp32
-// interval within 8e-6 (b - a) of the exact one.  dlo / dhi: d rounded down / up.
+// interval within 8e-6 (b - a) of the exact one.  dlo / dhi: d rounded down / up;
+// d2h + d2l = d^2 (fp32 head and remainder).
 __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float t1c, float4 e0, float t1e, float vex,
-                                          float vey, float vez, float dlo, float dhi, float &tin, float &tout) {
+                                          float vey, float vez, float dlo, float dhi, float d2h, float d2l, float &tin,
+                                          float &tout) {
     constexpr float U = 1.0f / 16777216.0f;
     const float a = fmaxf(t0c, e0.w), b = fminf(t1c, t1e);
     if (!(a < b)) return 0;                                    // C5
@@ -438,31 +440,44 @@ __device__ __forceinline__ int refine_rel(float4 q0, float4 q1, float t0c, float
     const float h = fmaf(yx, yx, fmaf(yy, yy, yz * yz));
     if (!(h <= dout * dout)) return 0;                         // certain miss
     if (!(din > 0.f && h < din2)) return 1;                    // near the threshold
+    // the interval: roots of A s^2 + 2 B s + Cd = 0 (Cd = |D|^2 - d^2) in the
+    // cancellation-free form q = -(B + sgn(B) sqrt(Delta)), Delta = A (d^2 - h_u)
+    // = B^2 - A Cd, roots q / A and Cd / q (the form s_u -+ w loses the digits of
+    // s_u and w when both are large against the span: DESIGN.md §5)
     const float ux = fmaf(su, Vx, Dx), uy = fmaf(su, Vy, Dy), uz = fmaf(su, Vz, Dz);
     const float hu = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    const float rem = fmaxf(fmaf(dhi, dhi, -hu), 0.f);
-    const float w = sqrt_approx(rem * rA);
-    const float lo = su - w, hi = su + w;
-    // error of an unclamped end s (first order, x1.25): the root moves
-    // by (y . dP)/(A w) for a position error dP at the root, y = D + s V the relative
-    // position there (|y| = d), dP_i <= eD_i + L eV_i per component (roundings of dp,
-    // a - t0, the velocities (<= 5u each) and the FMAs); + the roundings of h_u and
-    // d^2 (4u d^2 / (A w)), of s_u (7u |s_u| + 2u sum|D_i V_i| / A), of w (3u w),
-    // and u (|s_u| + w) for s_u -+ w
+    const float rem = fmaxf((d2h - hu) + d2l, 0.f);
+    const float sq = sqrt_approx(A * rem);                     // sqrt(Delta) = A w = |y . V| at a root
+    const bool bpos = B >= 0.f;
+    const float q = bpos ? -(B + sq) : sq - B;
+    const float rq = rcp_approx(q), rsq = rcp_approx(sq);
+    const float Cd = (ha - d2h) - d2l;
+    const float rbig = q * rA, rsmall = Cd * rq;
+    const float lo = bpos ? rbig : rsmall, hi = bpos ? rsmall : rbig;
+    // rounding error of each root for the computed D, V (first order): q from B
+    // (3u sum|D_i V_i|), sqrt(Delta) (A: 3u, d^2 - h_u: 5u h_u + 2.1u rem, the
+    // product, sqrt.approx: 2u) and its own rounding; q / A adds A, rcp and the
+    // product (6u); Cd / q adds Cd (3u |D|^2 + 2.1u |Cd|), rcp and the product
+    const float sdv = fabsf(Dx * Vx) + fabsf(Dy * Vy) + fabsf(Dz * Vz);
+    const float dq = fmaf(3.f * U, sdv, fmaf(5.05f * U, sq, fmaf((2.5f * U) * hu, A * rsq, U * fabsf(q))));
+    const float eq = dq * fabsf(rq);
+    const float ebig = fabsf(rbig) * (eq + 6.f * U);
+    const float esmall = fmaf(U * fmaf(3.f, ha, 2.1f * fabsf(Cd)), fabsf(rq), fabsf(rsmall) * (eq + 3.f * U));
+    // input errors (the roundings of D and V against the exact motion): a root
+    // moves by (y . dP) / |y . V| = (y . dP) / sqrt(Delta) for a position error
+    // dP at the root, y = D + s V the relative position there (|y| = d), dP_i <=
+    // eD_i + L eV_i per component (roundings of dp, a - t0, the velocities (<= 5u
+    // each) and the FMAs)
     const float ex = U * fmaf(6.f, fabsf(aq * q1.x) + fabsf(ae * vex), fabsf(Dx) + fabsf(ix) + fabsf(dpx)) +
                      L * U * fmaf(5.f, fabsf(q1.x) + fabsf(vex), fabsf(Vx));
     const float ey = U * fmaf(6.f, fabsf(aq * q1.y) + fabsf(ae * vey), fabsf(Dy) + fabsf(iy) + fabsf(dpy)) +
                      L * U * fmaf(5.f, fabsf(q1.y) + fabsf(vey), fabsf(Vy));
     const float ez = U * fmaf(6.f, fabsf(aq * q1.z) + fabsf(ae * vez), fabsf(Dz) + fabsf(iz) + fabsf(dpz)) +
                      L * U * fmaf(5.f, fabsf(q1.z) + fabsf(vez), fabsf(Vz));
-    const float rAw = rcp_approx(A * w);
-    const float sdv = fabsf(Dx * Vx) + fabsf(Dy * Vy) + fabsf(Dz * Vz);
-    const float common = fmaf((4.f * U) * dhi * dhi, rAw, fmaf(7.f * U, fabsf(su), fmaf((2.f * U) * sdv, rA, (3.f * U) * w)));
-    const float rnd = U * (fabsf(su) + w);
     const float yl = fabsf(fmaf(lo, Vx, Dx)) * ex + fabsf(fmaf(lo, Vy, Dy)) * ey + fabsf(fmaf(lo, Vz, Dz)) * ez;
     const float yh = fabsf(fmaf(hi, Vx, Dx)) * ex + fabsf(fmaf(hi, Vy, Dy)) * ey + fabsf(fmaf(hi, Vz, Dz)) * ez;
-    const float dlt_lo = fmaf(1.25f, fmaf(yl, rAw, common), rnd);
-    const float dlt_hi = fmaf(1.25f, fmaf(yh, rAw, common), rnd);
+    const float dlt_lo = 1.25f * fmaf(yl, rsq, bpos ? ebig : esmall);
+    const float dlt_hi = 1.25f * fmaf(yh, rsq, bpos ? esmall : ebig);
     tin = a + fminf(fmaxf(lo, 0.f), L);
     tout = a + fminf(fmaxf(hi, 0.f), L);
     const float tol = 8e-6f * L;
@@ -653,6 +668,7 @@ struct PairCtx {                     // what the fp64 path needs
     OutArgs o;
     double d64;                      // the caller's threshold (fp64 path)
     float dlo;                       // d rounded down to float (certain-hit tests of refine_rel)
+    float d2h, d2l;                  // d^2 = d2h + d2l (fp32 head and the rounded remainder: refine_rel roots)
 };
 
 // Evaluate queued pairs 0..n-1 in fp64 (lane k takes pair k) and append the hits.
@@ -1038,7 +1054,8 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
         qid = __float_as_uint(W->q[g][5].w);
         if (!A->ecell || ref_cell(id.z, W->spq[g], W->spc[g])) {
             const float4 ep = W->cw[slot].p, ev = W->cw[slot].v;
-            k = refine_rel(q0, q1, q2.x, q2.y, ep, ev.w, ev.x, ev.y, ev.z, A->pc.dlo, A->pc.d, tin, tout);
+            k = refine_rel(q0, q1, q2.x, q2.y, ep, ev.w, ev.x, ev.y, ev.z, A->pc.dlo, A->pc.d, A->pc.d2h, A->pc.d2l,
+                           tin, tout);
         }
     }
     const uint32_t j = id.y;
@@ -2151,7 +2168,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.d2u = d2;
         }
         a.tc = time_origin(idx);
-        a.pc = PairCtx{Q, prec, pperm, d, T0, T1, oo, d64, dlo};
+        const double dd = d64 * d64;
+        const float d2h = (float)dd, d2l = (float)(dd - (double)d2h);
+        a.pc = PairCtx{Q, prec, pperm, d, T0, T1, oo, d64, dlo, d2h, d2l};
         for (int c = 0; c < 3; ++c) {
             a.arr[c] = spatial ? nullptr : idx->st_arr[c];
             a.srec[c] = spatial ? nullptr : idx->st_rec[c];
