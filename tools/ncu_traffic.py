@@ -22,6 +22,6 @@ path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 t = json.load(open(path)) if os.path.exists(path) else {}
 t[f"{config}|{d}|{kernel}|{variant}"] = {"dram_bytes": rd + wr, "read": rd, "write": wr,
                                          "duration": vals.get("gpu__time_duration.sum"),
-                                         "source": os.path.basename(raw)}
+                                         "source": (os.environ.get("TAG", "") + " " + os.path.basename(raw)).strip()}
 json.dump(t, open(path, "w"), indent=1, sort_keys=True)
 print(f"{config}|{d}|{kernel}|{variant}: {rd + wr:.4g} B")
