@@ -25,7 +25,10 @@ namespace tds {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int PT = 256;                  // threads per block of the pair kernels
+#ifndef TDS_RANGE_PT
+#define TDS_RANGE_PT 256
+#endif
+constexpr int PT = TDS_RANGE_PT;         // threads per block of the pair kernel
 #ifndef TDS_APPEND_FAST
 #define TDS_APPEND_FAST 1                // appendK: warp-uniform fast path when the batch fits the chunk
 #endif
@@ -514,7 +517,7 @@ struct WarpState {
     uint32_t ap_used, ap_size, ap_full;
     uint32_t refined, hits, r32;
     uint32_t fn;                     // fp64 queue fill (< 32 between flushes)
-    uint32_t rq[RQ_CAP], rj[RQ_CAP]; // refine queue: group slot, candidate (sorted / cell-ordered position)
+    uint16_t rq[RQ_CAP];             // refine queue: group slot g | window slot << 5
     uint32_t fq[64], fj[64];         // fp64 queue: pairs the fp32 stages could not decide
 };
 
@@ -718,13 +721,13 @@ __device__ __forceinline__ void queue_add4(WarpState &W, uint32_t &qn, bool m0, 
     const unsigned b2 = __ballot_sync(FULL, m2), b3 = __ballot_sync(FULL, m3);
     const unsigned lt = (1u << lane) - 1u;
     uint32_t p = qn;
-    if (m0) { const uint32_t k = p + __popc(b0 & lt); W.rq[k] = qid; W.rj[k] = j0; }
+    if (m0) W.rq[p + __popc(b0 & lt)] = (uint16_t)(qid | (j0 << 5));
     p += __popc(b0);
-    if (m1) { const uint32_t k = p + __popc(b1 & lt); W.rq[k] = qid; W.rj[k] = j1; }
+    if (m1) W.rq[p + __popc(b1 & lt)] = (uint16_t)(qid | (j1 << 5));
     p += __popc(b1);
-    if (m2) { const uint32_t k = p + __popc(b2 & lt); W.rq[k] = qid; W.rj[k] = j2; }
+    if (m2) W.rq[p + __popc(b2 & lt)] = (uint16_t)(qid | (j2 << 5));
     p += __popc(b2);
-    if (m3) { const uint32_t k = p + __popc(b3 & lt); W.rq[k] = qid; W.rj[k] = j3; }
+    if (m3) W.rq[p + __popc(b3 & lt)] = (uint16_t)(qid | (j3 << 5));
     qn = p + __popc(b3);
 }
 
@@ -1046,7 +1049,7 @@ template <bool EXACT>
 __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, uint32_t n, uint32_t base) {
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
-    const uint32_t g = v ? W->ws.rq[base + lane] : 0u, slot = v ? W->ws.rj[base + lane] : 0u;
+    const uint32_t e = v ? W->ws.rq[base + lane] : 0u, g = e & 31u, slot = e >> 5;
     __syncwarp();                    // queue slots read: later queue additions may reuse them
     float tin = 0.f, tout = 0.f;
     int k = 0;
@@ -1101,7 +1104,12 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
 // windows (hysteresis on the window's pass fraction): the fused relative-form
 // step dense_test2 appends whole-span hits at once and queues the rest.
 template <bool EXACT>
-__global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(const __grid_constant__ RangeArgs A) {
+#ifdef TDS_RANGE_MAXNREG
+__global__ void __maxnreg__(TDS_RANGE_MAXNREG) k_pair_range(
+#else
+__global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
+#endif
+    const __grid_constant__ RangeArgs A) {
     extern __shared__ __align__(16) unsigned char range_smem[];     // PT / 32 x RangeWarpSmem (> 48 KB)
     const int lane = threadIdx.x & 31;
     RangeWarpSmem &W = reinterpret_cast<RangeWarpSmem *>(range_smem)[threadIdx.x >> 5];
