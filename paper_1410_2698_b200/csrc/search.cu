@@ -39,6 +39,9 @@ constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range 
 #ifndef TDS_ITEMS_PER_WARP
 #define TDS_ITEMS_PER_WARP 32             // measured: 4 -> 32 = -14 % (d=0.03 ST) .. -22 % (d=0.01); 64+ no better
 #endif
+#ifndef TDS_PRED_STORE
+#define TDS_PRED_STORE 1                 // appendK: predicated record stores (inline PTX)
+#endif
 #ifndef TDS_HYST_HI
 #define TDS_HYST_HI 25
 #endif
@@ -528,6 +531,18 @@ __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
     __syncwarp();
 }
 
+// predicated 16-B record store (no branch around it): the result buffer is
+// write-only in the pair kernel, so the store needs no ordering with other accesses
+__device__ __forceinline__ void st_rec_if(bool h, uint4 *p, const Rec &r) {
+#if TDS_PRED_STORE
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.v4.u32 [%1], {%2, %3, %4, %5};\n\t}"
+                 :: "r"((int)h), "l"(p), "r"(r.qid), "r"(r.eid), "r"(__float_as_uint(r.t_in)),
+                    "r"(__float_as_uint(r.t_out)));
+#else
+    if (h) *p = make_uint4(r.qid, r.eid, __float_as_uint(r.t_in), __float_as_uint(r.t_out));
+#endif
+}
+
 // warp-wide: every lane calls with its own hit flag / record.  Pass 1 appends
 // into chunks of CS slots reserved with one atomic per chunk (warp-aggregated,
 // no per-record global atomics); EXACT (re-plan passes) writes the record at
@@ -567,7 +582,11 @@ __device__ __forceinline__ void append(const OutArgs &o, WarpState &W, bool hit,
         }
     }
     const uint32_t rk = __popc(hm & ((1u << lane) - 1u));
-    if (hit) {
+    if (TDS_APPEND_FAST && !full && used + k <= size) {   // warp-uniform: the batch fits the chunk
+        uint4 *out = reinterpret_cast<uint4 *>(o.buf) + (base + used);
+        asm("mov.b64 %0, %0;" : "+l"(out));
+        st_rec_if(hit, out + rk, r);
+    } else if (hit) {
         if (!full && used + rk < size) {
             reinterpret_cast<uint4 *>(o.buf)[base + used + rk] =
                 make_uint4(r.qid, r.eid, __float_as_uint(r.t_in), __float_as_uint(r.t_out));
@@ -614,13 +633,12 @@ __device__ __forceinline__ void appendK(const OutArgs &o, WarpState &W, const bo
     }
     const unsigned lt = (1u << lane) - 1u;
     if (TDS_APPEND_FAST && !full && used + k <= size) {   // warp-uniform: the whole batch fits the chunk
-        uint4 *out = reinterpret_cast<uint4 *>(o.buf) + base + used;
+        uint4 *out = reinterpret_cast<uint4 *>(o.buf) + (base + used);
+        asm("mov.b64 %0, %0;" : "+l"(out));   // opaque base: one IMAD.WIDE per record address
         uint32_t pre = 0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-            if (h[i])
-                out[pre + __popc(hm[i] & lt)] =
-                    make_uint4(r[i].qid, r[i].eid, __float_as_uint(r[i].t_in), __float_as_uint(r[i].t_out));
+            st_rec_if(h[i], out + (pre + __popc(hm[i] & lt)), r[i]);
             pre += __popc(hm[i]);
         }
     } else {
@@ -1059,7 +1077,8 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
         const float4 q0 = W->q[g][0], q1 = W->q[g][1], q2 = W->q[g][2];
         qid = __float_as_uint(W->q[g][5].w);
         if (!A->ecell || ref_cell(id.z, W->spq[g], W->spc[g])) {
-            const float4 ep = W->cw[slot].p, ev = W->cw[slot].v;
+            const float4 ep = W->cw[slot].p;
+            const float4 ev = W->cw[slot].v;
             k = refine_rel(q0, q1, q2.x, q2.y, ep, ev.w, ev.x, ev.y, ev.z, A->pc.dlo, A->pc.d, A->pc.d2h, A->pc.d2l,
                            tin, tout);
         }
