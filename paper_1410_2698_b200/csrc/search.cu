@@ -37,7 +37,7 @@ constexpr int PT = TDS_RANGE_PT;         // threads per block of the pair kernel
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 #ifndef TDS_ITEMS_PER_WARP
-#define TDS_ITEMS_PER_WARP 32             // measured: 4 -> 32 = -14 % (d=0.03 ST) .. -22 % (d=0.01); 64+ no better
+#define TDS_ITEMS_PER_WARP 48             // measured: 4 -> 32 = -14 % (d=0.03 ST) .. -22 % (d=0.01); 48: -2 % Merger, else +-0.5 %
 #endif
 #ifndef TDS_PRED_STORE
 #define TDS_PRED_STORE 1                 // appendK: predicated record stores (inline PTX)
@@ -953,11 +953,22 @@ __global__ void k_tile_chunks(uint32_t *len_to_chunks, uint32_t ntiles, const un
                               DevStats *st, uint32_t target_items) {
     unsigned long long tl = *total_len;
     unsigned long long ch = (tl + target_items - 1) / (target_items ? target_items : 1);
-    ch = ch < WIN ? WIN : (ch > 8192 ? 8192 : ch);
+    ch = ch < WIN ? WIN : ch;                 // items <= target_items + ntiles (the item -> tile map)
     ch = (ch + WIN - 1) / WIN * WIN;          // chunks of whole windows
     uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) st->ch = (uint32_t)ch;
     if (t < ntiles) len_to_chunks[t] = (uint32_t)((len_to_chunks[t] + ch - 1) / ch);
+}
+
+// item -> tile map (one warp per tile fills its items): the pair kernel finds an
+// item's tile with one load instead of a binary search over item_start
+__global__ void k_item_tiles(const uint32_t *__restrict__ item_start, uint32_t ntiles, uint32_t *__restrict__ item_tile,
+                             uint32_t cap) {
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    const uint32_t a = item_start[t], b = min(item_start[t + 1], cap);
+    for (uint32_t i = a + lane; i < b; i += 32) item_tile[i] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -970,6 +981,7 @@ struct RangeArgs {
     const Sched *sched;
     const Tile *tiles;
     const uint32_t *item_start;      // [ntiles+1]
+    const uint32_t *item_tile;       // [items] tile of each work item
     uint32_t ntiles;
     float df;                        // filter_abs threshold: d * (1 + 2^-20), rounded up
     float d2u;                       // d^2 rounded up (window-box distance test)
@@ -1147,11 +1159,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
         if (lane == 0) item = atomicAdd(&st->work_ctr, 1u);
         item = __shfl_sync(FULL, item, 0);
         if (item >= total) break;
-        uint32_t lo = 0, hi = A.ntiles;
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (A.item_start[mid] <= item) lo = mid; else hi = mid;
-        }
+        const uint32_t lo = A.item_tile[item];
         const Tile T = A.tiles[lo];
         const uint32_t chunk = item - A.item_start[lo];
         const uint32_t c_lo = T.ulo + chunk * CH;
@@ -1863,7 +1871,7 @@ void launch_range(const RangeArgs &a, cudaStream_t s) {
 // build tiles + work items for schedule entries [lo, hi) of the sorted schedule
 // (the category counts in st describe the whole sorted schedule)
 uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, DBuf<Tile> &tiles,
-                    DBuf<uint32_t> &item_start, cudaStream_t s, int part_range = 0) {
+                    DBuf<uint32_t> &item_start, DBuf<uint32_t> &item_tile, cudaStream_t s, int part_range = 0) {
     uint32_t n = hi - lo;
     uint32_t max_tiles = n / 32 + 5;     // also bounds the tiles of any sub-range (part_range)
     tiles = DBuf<Tile>(max_tiles, s);
@@ -1875,6 +1883,10 @@ uint32_t plan_items(const Sched *sched, uint32_t lo, uint32_t hi, DevStats *st, 
     k_tile_chunks<<<nblk(max_tiles), 256, 0, s>>>(item_start.p, max_tiles, &st->union_total, st, target);
     TDS_CHECK_LAUNCH();
     exclusive_scan_u32(item_start.p, item_start.p, max_tiles + 1, nullptr, s);
+    const uint32_t cap = target + max_tiles + 1;   // bounds the items (k_tile_chunks)
+    item_tile = DBuf<uint32_t>(cap, s);
+    k_item_tiles<<<nblk((uint64_t)max_tiles * 32), 256, 0, s>>>(item_start.p, max_tiles, item_tile.p, cap);
+    TDS_CHECK_LAUNCH();
     return max_tiles;
 }
 
@@ -1942,7 +1954,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     DBuf<Sched> sched;
     DBuf<uint32_t> sp_cell, sp_qlo;      // GPUSpatial entries: cell, query-box low corner (packed)
     DBuf<Tile> tiles;
-    DBuf<uint32_t> item_start;
+    DBuf<uint32_t> item_start, item_tile;
     uint32_t ntiles = 0;
     uint32_t ns = n;                     // schedule entries
     int key_bits = 16;
@@ -2095,9 +2107,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             exclusive_scan_u64(w.p, w.p, ns + 1, nullptr, s);
             k_part_bounds<<<1, 32, 0, s>>>(w.p, ns, part, nparts, dst.p);
             TDS_CHECK_LAUNCH();
-            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, s, /*part_range=*/1);
+            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, item_tile, s, /*part_range=*/1);
         } else {
-            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, s);
+            ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, item_tile, s);
         }
     }
     tr.mark("schedule");
@@ -2230,7 +2242,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     tm.mark(2);
     if (ns && hs.pair_tests > 0) {
         RangeArgs a = range_args(o);
-        a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.ntiles = ntiles;
+        a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.item_tile = item_tile.p;
+        a.ntiles = ntiles;
         a.sp_cell = sp_cell.p; a.sp_qlo = sp_qlo.p;
         launch_range<false>(a, s);
         TDS_CHECK_LAUNCH();
@@ -2409,11 +2422,11 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             k_cat_counts<<<nblk(nb), 256, 0, s>>>(rsched.p, nb, bst.p);
             TDS_CHECK_LAUNCH();
             DBuf<Tile> bt;
-            DBuf<uint32_t> bis;
-            const uint32_t bnt = plan_items(rsched.p, 0, nb, bst.p, bt, bis, s);
+            DBuf<uint32_t> bis, bit;
+            const uint32_t bnt = plan_items(rsched.p, 0, nb, bst.p, bt, bis, bit, s);
             RangeArgs a = range_args(o);
             a.pc.o.st = bst.p;
-            a.sched = rsched.p; a.tiles = bt.p; a.item_start = bis.p; a.ntiles = bnt;
+            a.sched = rsched.p; a.tiles = bt.p; a.item_start = bis.p; a.item_tile = bit.p; a.ntiles = bnt;
             a.sp_cell = rcell.p; a.sp_qlo = rqlo.p;
             launch_range<true>(a, s);
             TDS_CHECK_LAUNCH();
