@@ -2112,6 +2112,18 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             ntiles = plan_items(sched.p, 0, ns, dst.p, tiles, item_start, item_tile, s);
         }
     }
+    const float4 *prec = spatial ? idx->fsg_rec : idx->rec;
+    const uint32_t *pperm = spatial ? idx->fsg_perm : idx->perm;
+    // result-size probe (automatic capacity): launched before the host reads the
+    // schedule's totals, so one synchronisation returns both (its estimate is used
+    // for large searches only, below); its counters start zeroed with the header
+    const bool probe_run = capacity == 0 && ns;
+    if (probe_run) {
+        k_density_probe<<<32, 256, 0, s>>>(sched.p, ns, Q, prec, spatial ? nullptr : idx->st_arr[0],
+                                           spatial ? nullptr : idx->st_arr[1], spatial ? nullptr : idx->st_arr[2], d,
+                                           T0, T1, spatial ? idx->fsg_ecell : nullptr, sp_cell.p, sp_qlo.p, dst.p);
+        TDS_CHECK_LAUNCH();
+    }
     tr.mark("schedule");
     // pair tests bound the result count: size the pass buffer
     DevStats &hs = *pinned_stats();
@@ -2135,17 +2147,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // result and a compaction copy after the pass
     uint64_t est_hits = 0;
     bool probed = false;
-    const float4 *prec = spatial ? idx->fsg_rec : idx->rec;
-    const uint32_t *pperm = spatial ? idx->fsg_perm : idx->perm;
-    if (capacity == 0 && hs.pair_tests >= CAP_PROBE_MIN && ns) {
-        TDS_CUDA(cudaMemsetAsync(&dst.p->probe_pass, 0, 8, s));
-        TDS_CUDA(cudaMemsetAsync(&dst.p->probe_est, 0, 12, s));
-        k_density_probe<<<32, 256, 0, s>>>(sched.p, ns, Q, prec, spatial ? nullptr : idx->st_arr[0],
-                                           spatial ? nullptr : idx->st_arr[1], spatial ? nullptr : idx->st_arr[2], d,
-                                           T0, T1, spatial ? idx->fsg_ecell : nullptr, sp_cell.p, sp_qlo.p, dst.p);
-        TDS_CHECK_LAUNCH();
-        TDS_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, s));
-        TDS_CUDA(cudaStreamSynchronize(s));
+    if (probe_run && hs.pair_tests >= CAP_PROBE_MIN) {
         if (hs.probe_total >= 1024 && hs.probe_entries) {
             // unbiased for entries sampled evenly over the schedule: the mean of the
             // sampled entries' estimated records times the number of entries
