@@ -42,6 +42,9 @@ constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range 
 #ifndef TDS_PRED_STORE
 #define TDS_PRED_STORE 1                 // appendK: predicated record stores (inline PTX)
 #endif
+#ifndef TDS_DENSE_START
+#define TDS_DENSE_START 8                // items start dense when the probe's pass fraction is >= this % (else
+#endif                                   // the dense/sparse state carries over from the warp's last item)
 #ifndef TDS_HYST_HI
 #define TDS_HYST_HI 25
 #endif
@@ -995,6 +998,7 @@ struct RangeArgs {
     const float4 *wb[4];
     int static_ok;                   // stationary-query filter allowed (default; TDS_NO_STATIC=1: off)
     int hyst_hi, hyst_lo;            // dense-window hysteresis, % of a window's evaluated pairs passing
+    int start_dense;                 // every work item starts with a dense window (hit-heavy search)
 };
 
 // GPUSpatial duplicate avoidance (replaces the host filter of P:558-559): a pair
@@ -1162,6 +1166,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
         const uint32_t lo = A.item_tile[item];
         const Tile T = A.tiles[lo];
         const uint32_t chunk = item - A.item_start[lo];
+        if (A.start_dense) dense = true;     // hit-heavy search (probe): every item starts dense
         const uint32_t c_lo = T.ulo + chunk * CH;
         const uint32_t c_hi = min(c_lo + CH, T.uhi);
         // ---- owner side: lane g stages query slot g of the group
@@ -2147,6 +2152,12 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // result and a compaction copy after the pass
     uint64_t est_hits = 0;
     bool probed = false;
+    int start_dense = 0;
+    if (probe_run && hs.probe_total >= 1024) {
+        const char *e = getenv("TDS_DENSE_START");            // A/B override (%)
+        const double thr = (e ? atof(e) : (double)TDS_DENSE_START) / 100.0;
+        start_dense = (double)hs.probe_pass >= thr * (double)hs.probe_total ? 1 : 0;
+    }
     if (probe_run && hs.pair_tests >= CAP_PROBE_MIN) {
         if (hs.probe_total >= 1024 && hs.probe_entries) {
             // unbiased for entries sampled evenly over the schedule: the mean of the
@@ -2236,6 +2247,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         const char *hh = getenv("TDS_HYST_HI"), *hl = getenv("TDS_HYST_LO");   // tuning (A/B)
         a.hyst_hi = hh ? atoi(hh) : HYST_HI;
         a.hyst_lo = hl ? atoi(hl) : HYST_LO;
+        a.start_dense = start_dense;
         return a;
     };
 
