@@ -2088,7 +2088,9 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     }
     if (ns) {
         // sort the entries by (category, range start): one stable radix sort
+        tr.mark("sched_kernel");
         radix_sort_pairs(keys.p, order.p, ns, 0, key_bits, s);
+        tr.mark("sort");
         {
             DBuf<Sched> tmp(ns, s);
             k_permute_sched<<<nblk(ns), 256, 0, s>>>(sched.p, order.p, ns, tmp.p);
@@ -2104,6 +2106,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             std::swap(sp_cell.p, tc.p);
             std::swap(sp_qlo.p, tq.p);
         }
+        tr.mark("permute");
         if (nparts > 1) {
             // this part's slice of the sorted schedule: equal shares of the exact pair tests
             DBuf<uint64_t> w(ns + 1, s);
@@ -2122,6 +2125,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     // result-size probe (automatic capacity): launched before the host reads the
     // schedule's totals, so one synchronisation returns both (its estimate is used
     // for large searches only, below); its counters start zeroed with the header
+    tr.mark("tiles");
     const bool probe_run = capacity == 0 && ns;
     if (probe_run) {
         k_density_probe<<<32, 256, 0, s>>>(sched.p, ns, Q, prec, spatial ? nullptr : idx->st_arr[0],
