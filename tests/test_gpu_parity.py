@@ -330,7 +330,8 @@ def test_dense_and_merger_subsample(tds, name, kinds):
 @pytest.mark.parametrize("name", ["tiny", "merger-small"])
 def test_fsg_time_trim_equals_literal(tds, name, monkeypatch):
     """GPUSpatial with per-cell time trimming returns exactly the paper-literal
-    FSG result (TDS_FSG_LITERAL=1: whole cells as candidates)."""
+    FSG result (TDS_FSG_LITERAL=1: whole cells as candidates), and
+    the literal result equals the oracle's."""
     w = synth.tiny() if name == "tiny" else synth.merger(n_per_disk=4096)
     d = w.d if name == "tiny" else 1.5
     idx = tds.Index(_cuda(w.D), kinds=tds.SPATIAL, m=10, grid=w.grid)
@@ -339,6 +340,14 @@ def test_fsg_time_trim_equals_literal(tds, name, monkeypatch):
     lit, st_l = _run(idx, w.Q, d, "spatial")
     monkeypatch.delenv("TDS_FSG_LITERAL")
     assert np.array_equal(np.sort(keys(got[0], got[1])), np.sort(keys(lit[0], lit[1])))
+    # the literal mode (and so the trimmed one) against the oracle: all queries on
+    # tiny, 64 time-stratified queries on the Merger-shaped case
+    from parity import stratified
+    sel = np.arange(w.Q.shape[0]) if name == "tiny" else stratified(w.Q, 64, seed=5)
+    ref = oracle.search(w.D, w.Q, d, qsel=sel)
+    lq = np.asarray(lit[0])
+    keep = np.isin(lq, sel)
+    check(tuple(np.asarray(x)[keep] for x in lit), ref, w.D, w.Q, d, label=f"FSG literal {name}")
     assert st["pair_tests"] <= st_l["pair_tests"]
     if name != "tiny":
         assert st["pair_tests"] < st_l["pair_tests"] / 4      # time trimming prunes most of a cell
