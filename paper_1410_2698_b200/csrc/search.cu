@@ -522,6 +522,7 @@ struct WarpState {
     unsigned long long ap_base;
     uint32_t ap_used, ap_size, ap_full;
     uint32_t refined, hits, r32;
+    unsigned long long exec, direct; // range kernel: executed pair tests, whole-span records (lane 0)
     uint32_t fn;                     // fp64 queue fill (< 32 between flushes)
     uint16_t rq[RQ_CAP];             // refine queue: group slot g | window slot << 5
     uint32_t fq[64], fj[64];         // fp64 queue: pairs the fp32 stages could not decide
@@ -530,6 +531,7 @@ struct WarpState {
 __device__ __forceinline__ void warp_state_init(WarpState &W, int lane) {
     if (lane == 0) {
         W.ap_base = 0; W.ap_used = 0; W.ap_size = 0; W.ap_full = 0; W.refined = 0; W.hits = 0; W.fn = 0; W.r32 = 0;
+        W.exec = 0; W.direct = 0;
     }
     __syncwarp();
 }
@@ -1156,7 +1158,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
     W.cnt[lane] = 0;
     uint32_t qn = 0;                         // refine queue fill (warp-uniform)
     __syncwarp();
-    unsigned long long exec = 0, direct_hits = 0;
+    uint32_t direct_hits = 0;               // per work item (added to the warp's total at the item end)
     bool dense = false;                      // warp-uniform: the last window was hit-heavy
     while (true) {
         uint32_t item = 0;
@@ -1259,7 +1261,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
             if (!mask) { base = cend; continue; }
             const unsigned mask_eval = mask;   // queries evaluated in this window
             const uint32_t wn = cend - max(base, wlo);   // candidates of the window inside the union
-            exec += (unsigned long long)wn * __popc(mask);
+            if (lane == 0) W.ws.exec += (unsigned long long)wn * __popc(mask);   // stats: executed pair tests
             // ---- worker side: lane = candidate
             const uint32_t c0 = base + lane, c1 = c0 + 32, c2 = c0 + 64, c3 = c0 + 96;
             uint32_t j0, j1, j2, j3;
@@ -1410,6 +1412,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
             qn = 0;
         }
         __syncwarp();
+        if (lane == 0) W.ws.direct += direct_hits;
+        direct_hits = 0;
         const uint32_t cq = owner_hits + W.cnt[lane];
         W.cnt[lane] = 0;
         if (active && cq) atomicAdd(&A.pc.o.qcount[S.qid], cq);
@@ -1418,8 +1422,8 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
     __syncwarp();
     if (W.ws.fn) flush64<EXACT>(&A.pc, &W.ws, W.ws.fn);
     warp_state_finish<EXACT>(A.pc.o, W.ws, lane);
-    if (lane == 0 && exec) atomicAdd(&st->executed, exec);
-    if (lane == 0 && direct_hits) { atomicAdd(&st->hits, direct_hits); atomicAdd(&st->direct, direct_hits); }
+    if (lane == 0 && W.ws.exec) atomicAdd(&st->executed, W.ws.exec);
+    if (lane == 0 && W.ws.direct) { atomicAdd(&st->hits, W.ws.direct); atomicAdd(&st->direct, W.ws.direct); }
 }
 
 // ---------------------------------------------------------------------------
