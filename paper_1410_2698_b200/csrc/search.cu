@@ -1416,7 +1416,9 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
         direct_hits = 0;
         const uint32_t cq = owner_hits + W.cnt[lane];
         W.cnt[lane] = 0;
-        if (active && cq) atomicAdd(&A.pc.o.qcount[S.qid], cq);
+        // an inactive slot never has a record (its mask bit is never set); its query
+        // row is read back from the staged slot instead of kept in a register
+        if (cq) atomicAdd(&A.pc.o.qcount[__float_as_uint(W.q[lane][5].w)], cq);
         __syncwarp();
     }
     __syncwarp();
