@@ -83,6 +83,7 @@ struct DevStats {
     unsigned int part_lo, part_hi;   // tds_search_part: schedule entries / query rows of this part
     double probe_est;                // result-size probe: sum over sampled entries of len x pass fraction
     unsigned int probe_entries;      // sampled live entries
+    unsigned int n_static;           // stationary query segments (k_count_static)
     unsigned long long part_slot_lo, part_slot_hi;   // GPUSpatial part: flattened slot range
     unsigned int pad[1];
 };
@@ -1140,7 +1141,7 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
 // queued (slot, candidate) and evaluated 32 at a time by range_refine.  Dense
 // windows (hysteresis on the window's pass fraction): the fused relative-form
 // step dense_test2 appends whole-span hits at once and queues the rest.
-template <bool EXACT>
+template <bool EXACT, bool STATIC>
 #ifdef TDS_RANGE_MAXNREG
 __global__ void __maxnreg__(TDS_RANGE_MAXNREG) k_pair_range(
 #else
@@ -1210,7 +1211,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
         bool stat = false;
         {
             const bool st_q = !active || (__float_as_uint(W.q[lane][1].w) == 0u);   // |v|_1 == +0
-            stat = A.static_ok && __all_sync(FULL, st_q);
+            stat = STATIC && A.static_ok && __all_sync(FULL, st_q);
         }
         const uint32_t *arr = (T.sel >= 0) ? A.arr[T.sel] : nullptr;
         uint32_t owner_hits = 0;             // whole-span hits of this lane's query slot (dense path)
@@ -1864,8 +1865,10 @@ int fsg_literal() {
     return (e && e[0] == '1') ? 1 : 0;
 }
 
-template <bool EXACT>
-void launch_range(const RangeArgs &a, cudaStream_t s) {
+// STATIC: the instantiation with the stationary-query filter (compiled only
+// where the query set holds a stationary segment: the path costs registers)
+template <bool EXACT, bool STATIC>
+void launch_range_k(const RangeArgs &a, cudaStream_t s) {
     constexpr size_t smem = sizeof(RangeWarpSmem) * (PT / 32);
     // RANGE_BPS resident blocks per SM: 228 KB of shared memory per SM, 1 KB reserved per block
     static_assert(RANGE_BPS * (smem + 1024) <= 228 * 1024, "range kernel shared memory exceeds RANGE_BPS blocks/SM");
@@ -1873,10 +1876,29 @@ void launch_range(const RangeArgs &a, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !attr_set[dev]) {
-        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT, STATIC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
         if (dev < 64) attr_set[dev] = true;
     }
-    k_pair_range<EXACT><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
+    k_pair_range<EXACT, STATIC><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
+}
+
+template <bool EXACT>
+void launch_range(const RangeArgs &a, bool with_static, cudaStream_t s) {
+    if (with_static) launch_range_k<EXACT, true>(a, s);
+    else launch_range_k<EXACT, false>(a, s);
+}
+
+// stationary query segments (P1 = P0, the supernova case of P:84-88) in Q
+__global__ void k_count_static(const float4 *__restrict__ Q, uint32_t n, DevStats *st) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    bool sq = false;
+    if (p < n) {
+        const float4 a = Q[2 * (uint64_t)p], b = Q[2 * (uint64_t)p + 1];
+        sq = a.x == b.x && a.y == b.y && a.z == b.z;
+    }
+    const unsigned m = __ballot_sync(FULL, sq);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&st->n_static, (unsigned)__popc(m));
 }
 
 // build tiles + work items for schedule entries [lo, hi) of the sorted schedule
@@ -1944,6 +1966,10 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     struct { DevStats *p; } dst{dstp};
     struct { uint32_t *p; } qcount{qcount_p};
     struct { uint8_t *p; } redo{redo_p};
+    // stationary query segments decide whether the pair kernel carries the
+    // stationary-query filter (launch_range)
+    k_count_static<<<nblk(n), 256, 0, s>>>(Q, n, dstp);
+    TDS_CHECK_LAUNCH();
 
     // ---- A6: queries are validated inside the schedule kernels; GPUTemporal /
     // GPUSpatioTemporal order them by (selector, range start) below, which subsumes
@@ -2149,6 +2175,8 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     tr.mark("sync");
     S.pair_tests = hs.pair_tests;
     S.fallback_queries = hs.fallback;
+    const char *ns_env0 = getenv("TDS_NO_STATIC");
+    const bool with_static = hs.n_static > 0 && !(ns_env0 && ns_env0[0] == '1');
     S.kind = kind;
     S.n_queries = spatial ? nq : (nq - hs.cat_cnt[4]);
     if (nparts > 1 && !spatial) {
@@ -2269,7 +2297,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.item_tile = item_tile.p;
         a.ntiles = ntiles;
         a.sp_cell = sp_cell.p; a.sp_qlo = sp_qlo.p;
-        launch_range<false>(a, s);
+        launch_range<false>(a, with_static, s);
         TDS_CHECK_LAUNCH();
     }
     tm.mark(3);
@@ -2452,7 +2480,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.pc.o.st = bst.p;
             a.sched = rsched.p; a.tiles = bt.p; a.item_start = bis.p; a.item_tile = bit.p; a.ntiles = bnt;
             a.sp_cell = rcell.p; a.sp_qlo = rqlo.p;
-            launch_range<true>(a, s);
+            launch_range<true>(a, with_static, s);
             TDS_CHECK_LAUNCH();
             TDS_CUDA(cudaStreamSynchronize(s));
             DevStats hb2;
