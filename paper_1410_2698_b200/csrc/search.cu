@@ -1082,7 +1082,7 @@ struct __align__(16) RangeWarpSmem {
 // Evaluate refine-queue entries [base, base + n), n <= 32 (lane k takes entry
 // k): (slot g, sorted entry position j) -> refine_rel with the query's terms from
 // shared memory; certain hits are appended, undecided pairs go to the fp64 queue.
-template <bool EXACT>
+template <bool EXACT, bool SPATIAL>
 __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, uint32_t n, uint32_t base) {
     const int lane = threadIdx.x & 31;
     const bool v = (uint32_t)lane < n;
@@ -1095,7 +1095,7 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
     if (v) {
         const float4 q0 = W->q[g][0], q1 = W->q[g][1], q2 = W->q[g][2];
         qid = __float_as_uint(W->q[g][5].w);
-        if (!A->ecell || ref_cell(id.z, W->spq[g], W->spc[g])) {
+        if (!SPATIAL || ref_cell(id.z, W->spq[g], W->spc[g])) {
             const float4 ep = W->cw[slot].p;
             const float4 ev = W->cw[slot].v;
             k = refine_rel(q0, q1, q2.x, q2.y, ep, ev.w, ev.x, ev.y, ev.z, A->pc.dlo, A->pc.d, A->pc.d2h, A->pc.d2l,
@@ -1121,12 +1121,12 @@ __device__ __noinline__ void range_refine(const RangeArgs *A, RangeWarpSmem *W, 
 }
 
 // warp-wide: evaluate the newest 32 queued pairs while >= 32 are queued
-template <bool EXACT>
+template <bool EXACT, bool SPATIAL>
 __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W, uint32_t &qn) {
     while (qn >= 32) {
         __syncwarp();
         qn -= 32;
-        range_refine<EXACT>(A, &W, 32, qn);
+        range_refine<EXACT, SPATIAL>(A, &W, 32, qn);
     }
 }
 
@@ -1141,7 +1141,7 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
 // queued (slot, candidate) and evaluated 32 at a time by range_refine.  Dense
 // windows (hysteresis on the window's pass fraction): the fused relative-form
 // step dense_test2 appends whole-span hits at once and queues the rest.
-template <bool EXACT, bool STATIC>
+template <bool EXACT, bool STATIC, bool SPATIAL>
 #ifdef TDS_RANGE_MAXNREG
 __global__ void __maxnreg__(TDS_RANGE_MAXNREG) k_pair_range(
 #else
@@ -1192,7 +1192,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
             W.q[lane][4] = make_float4(qf.vx, qf.vy, qf.vz, qc.t0c - A.tc);
             W.q[lane][5] = make_float4(qc.t1c - A.tc, __uint_as_float(my_lo), __uint_as_float(my_hi),
                                        __uint_as_float(S.qid));
-            if (A.ecell) {
+            if (SPATIAL) {
                 W.spc[lane] = active ? A.sp_cell[p] : 0xffffffffu;
                 W.spq[lane] = active ? A.sp_qlo[p] : 0u;
             }
@@ -1277,7 +1277,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                     RangeWarpSmem::Cand &cd = W.cw[lane + 32 * k];
                     cd.p = a;
                     cd.v = make_float4(f.vx, f.vy, f.vz, b.w);        // make_ecand's velocity (same rcp)
-                    cd.id = make_uint4(v ? __ldg(A.pc.perm + j) : 0u, j, (A.ecell && v) ? __ldg(A.ecell + j) : 0u, 0u);
+                    cd.id = make_uint4(v ? __ldg(A.pc.perm + j) : 0u, j, (SPATIAL && v) ? __ldg(A.ecell + j) : 0u, 0u);
                 };
                 float4 a0, b0, a1, b1;
                 load_cand(c0, c0 < cend, j0, a0, b0);
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                             in[k] &= ok;
                         }
                     }
-                    if (A.ecell) {                         // GPUSpatial: the pair's reference cell only
+                    if (SPATIAL) {                         // GPUSpatial: the pair's reference cell only
                         const uint32_t sq = W.spq[g], sc = W.spc[g];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -1355,7 +1355,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                         const uint32_t q0n = qn;
                         queue_add4(W.ws, qn, m[0], m[1], m[2], m[3], (uint32_t)g, s0, s1, s2, s3, lane);
                         wpass += qn - q0n;
-                        range_drain<EXACT>(&A, W, qn);
+                        range_drain<EXACT, SPATIAL>(&A, W, qn);
                     }
                 }
             } else {
@@ -1382,7 +1382,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                         m0 &= r0 < gw; m1 &= r0 + 32 < gw; m2 &= r0 + 64 < gw; m3 &= r0 + 96 < gw;
                     }
                     if (!__any_sync(FULL, (m0 | m1) | (m2 | m3))) continue;
-                    if (A.ecell) {                         // GPUSpatial: the pair's reference cell only
+                    if (SPATIAL) {                         // GPUSpatial: the pair's reference cell only
                         const uint32_t sq = W.spq[g], sc = W.spc[g];
                         m0 &= ref_cell(W.cw[s0].id.z, sq, sc);
                         m1 &= ref_cell(W.cw[s1].id.z, sq, sc);
@@ -1392,7 +1392,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                     const uint32_t q0n = qn;
                     queue_add4(W.ws, qn, m0, m1, m2, m3, (uint32_t)g, s0, s1, s2, s3, lane);
                     wpass += qn - q0n;
-                    range_drain<EXACT>(&A, W, qn);
+                    range_drain<EXACT, SPATIAL>(&A, W, qn);
                 }
             }
             // switch to the fused dense path once >= HYST_HI % of the window's pairs pass,
@@ -1400,7 +1400,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
             // threshold would toggle between the paths)
             if (qn) {                          // the queue refers to this window's slots
                 __syncwarp();
-                range_refine<EXACT>(&A, &W, qn, 0);
+                range_refine<EXACT, SPATIAL>(&A, &W, qn, 0);
                 qn = 0;
             }
             dense = 100u * wpass >= (uint32_t)(dense ? A.hyst_lo : A.hyst_hi) * __popc(mask_eval) * wn;
@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
         // ---- item end: the queue refers to this group's slots
         if (qn) {
             __syncwarp();
-            range_refine<EXACT>(&A, &W, qn, 0);
+            range_refine<EXACT, SPATIAL>(&A, &W, qn, 0);
             qn = 0;
         }
         __syncwarp();
@@ -1867,7 +1867,7 @@ int fsg_literal() {
 
 // STATIC: the instantiation with the stationary-query filter (compiled only
 // where the query set holds a stationary segment: the path costs registers)
-template <bool EXACT, bool STATIC>
+template <bool EXACT, bool STATIC, bool SPATIAL>
 void launch_range_k(const RangeArgs &a, cudaStream_t s) {
     constexpr size_t smem = sizeof(RangeWarpSmem) * (PT / 32);
     // RANGE_BPS resident blocks per SM: 228 KB of shared memory per SM, 1 KB reserved per block
@@ -1876,17 +1876,24 @@ void launch_range_k(const RangeArgs &a, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !attr_set[dev]) {
-        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT, STATIC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT, STATIC, SPATIAL>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (dev < 64) attr_set[dev] = true;
     }
-    k_pair_range<EXACT, STATIC><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
+    k_pair_range<EXACT, STATIC, SPATIAL><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
 }
 
 template <bool EXACT>
 void launch_range(const RangeArgs &a, bool with_static, cudaStream_t s) {
-    if (with_static) launch_range_k<EXACT, true>(a, s);
-    else launch_range_k<EXACT, false>(a, s);
+    // GPUSpatial (reference-cell rule) and the stationary-query filter are
+    // compile-time variants: each costs registers where it is not needed
+    if (a.ecell) {
+        if (with_static) launch_range_k<EXACT, true, true>(a, s);
+        else launch_range_k<EXACT, false, true>(a, s);
+    } else {
+        if (with_static) launch_range_k<EXACT, true, false>(a, s);
+        else launch_range_k<EXACT, false, false>(a, s);
+    }
 }
 
 // stationary query segments (P1 = P0, the supernova case of P:84-88) in Q
