@@ -37,7 +37,7 @@ constexpr int PT = TDS_RANGE_PT;         // threads per block of the pair kernel
 #endif
 constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range kernel)
 #ifndef TDS_ITEMS_PER_WARP
-#define TDS_ITEMS_PER_WARP 48             // measured: 4 -> 32 = -14 % (d=0.03 ST) .. -22 % (d=0.01); 48: -2 % Merger, else +-0.5 %
+#define TDS_ITEMS_PER_WARP 64             // measured: 4 -> 32 = -14 % (d=0.03 ST) .. -22 % (d=0.01); 64 (final kernel): -0.7 % d=0.03, -1.7 % Merger, +1.3 % d=0.01 vs 48
 #endif
 #ifndef TDS_PRED_STORE
 #define TDS_PRED_STORE 1                 // appendK: predicated record stores (inline PTX)
