@@ -45,6 +45,9 @@ constexpr int RANGE_BPS = TDS_RANGE_BPS;       // resident blocks per SM (range 
 #ifndef TDS_DENSE_START
 #define TDS_DENSE_START 8                // items start dense when the probe's pass fraction is >= this % (else
 #endif                                   // the dense/sparse state carries over from the warp's last item)
+#ifndef TDS_SPARSE_ONLY
+#define TDS_SPARSE_ONLY 3                // sparse-only kernel when the probe's pass fraction is below this %
+#endif
 #ifndef TDS_HYST_HI
 #define TDS_HYST_HI 25
 #endif
@@ -1141,7 +1144,7 @@ __device__ __forceinline__ void range_drain(const RangeArgs *A, RangeWarpSmem &W
 // queued (slot, candidate) and evaluated 32 at a time by range_refine.  Dense
 // windows (hysteresis on the window's pass fraction): the fused relative-form
 // step dense_test2 appends whole-span hits at once and queues the rest.
-template <bool EXACT, bool STATIC, bool SPATIAL>
+template <bool EXACT, bool STATIC, bool SPATIAL, bool SPARSE>
 #ifdef TDS_RANGE_MAXNREG
 __global__ void __maxnreg__(TDS_RANGE_MAXNREG) k_pair_range(
 #else
@@ -1299,7 +1302,7 @@ __global__ void __launch_bounds__(PT, RANGE_BPS) k_pair_range(
                 __syncwarp();
             }
             const uint32_t s0 = lane, s1 = lane + 32, s2 = lane + 64, s3 = lane + 96;   // window slots
-            if (dense) {
+            if (!SPARSE && dense) {
                 // fused step: the filter and the whole-span test for the lane's four
                 // candidates (two packed pairs); whole-span hits are appended at once
                 // with [a, b] from the raw times, other passes go to the refine queue
@@ -1867,7 +1870,7 @@ int fsg_literal() {
 
 // STATIC: the instantiation with the stationary-query filter (compiled only
 // where the query set holds a stationary segment: the path costs registers)
-template <bool EXACT, bool STATIC, bool SPATIAL>
+template <bool EXACT, bool STATIC, bool SPATIAL, bool SPARSE>
 void launch_range_k(const RangeArgs &a, cudaStream_t s) {
     constexpr size_t smem = sizeof(RangeWarpSmem) * (PT / 32);
     // RANGE_BPS resident blocks per SM: 228 KB of shared memory per SM, 1 KB reserved per block
@@ -1876,24 +1879,38 @@ void launch_range_k(const RangeArgs &a, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !attr_set[dev]) {
-        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT, STATIC, SPATIAL>,
+        TDS_CUDA(cudaFuncSetAttribute(k_pair_range<EXACT, STATIC, SPATIAL, SPARSE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (dev < 64) attr_set[dev] = true;
     }
-    k_pair_range<EXACT, STATIC, SPATIAL><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
+    k_pair_range<EXACT, STATIC, SPATIAL, SPARSE><<<persistent_blocks(RANGE_BPS), PT, smem, s>>>(a);
 }
 
-template <bool EXACT>
-void launch_range(const RangeArgs &a, bool with_static, cudaStream_t s) {
+template <bool EXACT, bool SPARSE>
+void launch_range_m(const RangeArgs &a, bool with_static, cudaStream_t s) {
     // GPUSpatial (reference-cell rule) and the stationary-query filter are
     // compile-time variants: each costs registers where it is not needed
     if (a.ecell) {
-        if (with_static) launch_range_k<EXACT, true, true>(a, s);
-        else launch_range_k<EXACT, false, true>(a, s);
+        if (with_static) launch_range_k<EXACT, true, true, SPARSE>(a, s);
+        else launch_range_k<EXACT, false, true, SPARSE>(a, s);
     } else {
-        if (with_static) launch_range_k<EXACT, true, false>(a, s);
-        else launch_range_k<EXACT, false, false>(a, s);
+        if (with_static) launch_range_k<EXACT, true, false, SPARSE>(a, s);
+        else launch_range_k<EXACT, false, false, SPARSE>(a, s);
     }
+}
+
+// hit-sparse searches (the probe's pass fraction below TDS_SPARSE_ONLY %) run the
+// instantiation without the dense-window step (first passes only)
+template <bool EXACT>
+void launch_range(const RangeArgs &a, bool with_static, bool sparse_only, cudaStream_t s) {
+    if constexpr (!EXACT) {
+        if (sparse_only) {
+            launch_range_m<EXACT, true>(a, with_static, s);
+            return;
+        }
+    }
+    (void)sparse_only;
+    launch_range_m<EXACT, false>(a, with_static, s);
 }
 
 // stationary query segments (P1 = P0, the supernova case of P:84-88) in Q
@@ -2198,10 +2215,14 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
     uint64_t est_hits = 0;
     bool probed = false;
     int start_dense = 0;
+    bool sparse_only = false;
     if (probe_run && hs.probe_total >= 1024) {
         const char *e = getenv("TDS_DENSE_START");            // A/B override (%)
         const double thr = (e ? atof(e) : (double)TDS_DENSE_START) / 100.0;
         start_dense = (double)hs.probe_pass >= thr * (double)hs.probe_total ? 1 : 0;
+        const char *e2 = getenv("TDS_SPARSE_ONLY");           // A/B override (%)
+        const double thr2 = (e2 ? atof(e2) : (double)TDS_SPARSE_ONLY) / 100.0;
+        sparse_only = (double)hs.probe_pass < thr2 * (double)hs.probe_total;
     }
     if (probe_run && hs.pair_tests >= CAP_PROBE_MIN) {
         if (hs.probe_total >= 1024 && hs.probe_entries) {
@@ -2304,7 +2325,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
         a.sched = sched.p; a.tiles = tiles.p; a.item_start = item_start.p; a.item_tile = item_tile.p;
         a.ntiles = ntiles;
         a.sp_cell = sp_cell.p; a.sp_qlo = sp_qlo.p;
-        launch_range<false>(a, with_static, s);
+        launch_range<false>(a, with_static, sparse_only, s);
         TDS_CHECK_LAUNCH();
     }
     tm.mark(3);
@@ -2487,7 +2508,7 @@ void search(tds_index_s *idx, int kind, const float4 *Q, uint64_t nq, double d64
             a.pc.o.st = bst.p;
             a.sched = rsched.p; a.tiles = bt.p; a.item_start = bis.p; a.item_tile = bit.p; a.ntiles = bnt;
             a.sp_cell = rcell.p; a.sp_qlo = rqlo.p;
-            launch_range<true>(a, with_static, s);
+            launch_range<true>(a, with_static, false, s);
             TDS_CHECK_LAUNCH();
             TDS_CUDA(cudaStreamSynchronize(s));
             DevStats hb2;
