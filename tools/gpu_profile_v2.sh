@@ -2,7 +2,7 @@
 # round-2 evidence pass: bench lines, the default bench's launch list, ncu --set full of the
 # headline pair kernel (kept as .ncu-rep for the source view) and single-pass DRAM bytes
 set -u
-tag=${1:-r2_v6}
+tag=${1:-r2_v8}
 out=gpurun_out/prof; mkdir -p $out gpurun_out/rep
 tools/profile_r2.sh $tag bench launches
 for a in "rdense003_st --variants spatiotemporal" "rdense009_t --d 0.09 --variants temporal" "merger1_s --config merger --d 1 --variants spatial"; do
